@@ -1,0 +1,317 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).  Plain C, no intrinsics,
+ * no blocking or fusion: each function is the definition it cites, written out.
+ */
+#include "oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int oracle_validate(const oracle_mapping* m) {
+  if (!m || m->n_leaves < 1 || !m->leaf_size || m->rank < 1 || !m->extents) return -1;
+  for (int32_t k = 0; k < m->n_leaves; ++k) {
+    int32_t s = m->leaf_size[k];
+    if (s != 1 && s != 2 && s != 4 && s != 8) return -1;
+  }
+  for (int32_t d = 0; d < m->rank; ++d)
+    if (m->extents[d] < 0) return -1;
+  if (m->kind < ORACLE_AOS || m->kind > ORACLE_AOSOA) return -1;
+  if (m->kind == ORACLE_AOSOA && m->lanes < 1) return -1;
+  return 0;
+}
+
+/* product of the extents. */
+int64_t oracle_record_count(const oracle_mapping* m) {
+  int64_t n = 1;
+  for (int32_t d = 0; d < m->rank; ++d) n *= m->extents[d];
+  return n;
+}
+
+/* P:414-416 (enumeration {0,0},{0,1},{0,2},{1,0}...): last index fastest. */
+int64_t oracle_linearize(const oracle_mapping* m, const int64_t* index) {
+  int64_t flat = 0;
+  for (int32_t d = 0; d < m->rank; ++d) {
+    if (index[d] < 0 || index[d] >= m->extents[d]) return -1;
+    flat = flat * m->extents[d] + index[d];
+  }
+  return flat;
+}
+
+/* S:60-66 sizeOfPacked / offsetOf(packed): leaves one after another, no padding. */
+uint64_t oracle_packed_offsets(const oracle_mapping* m, uint64_t* offsets) {
+  uint64_t off = 0;
+  for (int32_t k = 0; k < m->n_leaves; ++k) {
+    if (offsets) offsets[k] = off;
+    off += (uint64_t)m->leaf_size[k];
+  }
+  return off;
+}
+
+/* S:69-77 sizeOfAligned / offsetOf(aligned): each leaf starts at the next
+ * multiple of its alignment (= its size); the record size is rounded up to
+ * the maximum leaf alignment. */
+uint64_t oracle_aligned_offsets(const oracle_mapping* m, uint64_t* offsets) {
+  uint64_t off = 0, max_align = 1;
+  for (int32_t k = 0; k < m->n_leaves; ++k) {
+    uint64_t a = (uint64_t)m->leaf_size[k];
+    while (off % a != 0) off += 1;
+    if (offsets) offsets[k] = off;
+    off += a;
+    if (a > max_align) max_align = a;
+  }
+  while (off % max_align != 0) off += 1;
+  return off;
+}
+
+static uint64_t record_offsets(const oracle_mapping* m, uint64_t* offsets) {
+  return m->aligned ? oracle_aligned_offsets(m, offsets) : oracle_packed_offsets(m, offsets);
+}
+
+/* SoA single blob: leaf sub-arrays one after another in leaf order.
+ * With aligned=1 each sub-array start is rounded up to the leaf's size
+ * (reading #9).  starts[k] = byte start of leaf k's sub-array;
+ * returns the blob size. */
+static uint64_t soa_sb_starts(const oracle_mapping* m, uint64_t* starts) {
+  uint64_t n = (uint64_t)oracle_record_count(m);
+  uint64_t off = 0;
+  for (int32_t k = 0; k < m->n_leaves; ++k) {
+    uint64_t s = (uint64_t)m->leaf_size[k];
+    if (m->aligned)
+      while (off % s != 0) off += 1;
+    if (starts) starts[k] = off;
+    off += n * s;
+  }
+  return off;
+}
+
+/* "a compile time blob count". */
+int32_t oracle_blob_count(const oracle_mapping* m) {
+  return m->kind == ORACLE_SOA_MB ? m->n_leaves : 1; /* SoA MB blobCount = leafCount */
+}
+
+/* "for each blob the size in bytes can be queried". Closed forms from
+ * S:247 (AoS), S:263 (SoA MB), S:277 (SoA SB), S:281 (AoSoA, final block padded). */
+void oracle_blob_sizes(const oracle_mapping* m, uint64_t* sizes) {
+  uint64_t n = (uint64_t)oracle_record_count(m);
+  switch (m->kind) {
+    case ORACLE_AOS:
+      sizes[0] = n * record_offsets(m, NULL);
+      break;
+    case ORACLE_SOA_MB:
+      for (int32_t k = 0; k < m->n_leaves; ++k) sizes[k] = n * (uint64_t)m->leaf_size[k];
+      break;
+    case ORACLE_SOA_SB:
+      sizes[0] = soa_sb_starts(m, NULL);
+      break;
+    case ORACLE_AOSOA: {
+      uint64_t L = (uint64_t)m->lanes;
+      uint64_t blocks = (n + L - 1) / L;
+      sizes[0] = blocks * L * record_offsets(m, NULL);
+      break;
+    }
+  }
+}
+
+/* blobNrAndOffset, one case per mapping of P:460-473, written from the
+ * formulas of S:244-286:
+ *   AoS: blob 0, off = i*S + offsetOf(k)
+ *   SoA MB: blob k, off = i*s_k
+ *   SoA SB:     blob 0, off = start_k + i*s_k
+ *   AoSoA L: blob 0, off = (i/L)*L*S + offsetOf(k)*L + (i%L)*s_k
+ * where S / offsetOf are the packed or aligned record layout. */
+int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
+                              int32_t* blob, uint64_t* offset) {
+  if (k < 0 || k >= m->n_leaves) return -1;
+  if (i < 0 || i >= oracle_record_count(m)) return -1;
+  uint64_t s_k = (uint64_t)m->leaf_size[k];
+  uint64_t ui = (uint64_t)i;
+  switch (m->kind) {
+    case ORACLE_AOS: {
+      uint64_t* offs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)m->n_leaves);
+      uint64_t S = record_offsets(m, offs);
+      *blob = 0;
+      *offset = ui * S + offs[k];
+      free(offs);
+      return 0;
+    }
+    case ORACLE_SOA_MB:
+      *blob = k;
+      *offset = ui * s_k;
+      return 0;
+    case ORACLE_SOA_SB: {
+      uint64_t* starts = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)m->n_leaves);
+      soa_sb_starts(m, starts);
+      *blob = 0;
+      *offset = starts[k] + ui * s_k;
+      free(starts);
+      return 0;
+    }
+    case ORACLE_AOSOA: {
+      uint64_t* offs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)m->n_leaves);
+      uint64_t S = record_offsets(m, offs);
+      uint64_t L = (uint64_t)m->lanes;
+      uint64_t block = ui / L, lane = ui % L; /* i -> (i/L, i mod L) */
+      *blob = 0;
+      *offset = block * L * S + offs[k] * L + lane * s_k;
+      free(offs);
+      return 0;
+    }
+  }
+  return -1;
+}
+
+/* A faster, equivalent evaluation of oracle_blob_nr_and_offset for the copy
+ * loops: the per-leaf record offsets / sub-array starts are computed once
+ * instead of per call.  The arithmetic per kind is the same as above. */
+typedef struct {
+  const oracle_mapping* m;
+  uint64_t S;
+  uint64_t* offs;   /* record offsets (AoS/AoSoA) or sub-array starts (SoA SB) */
+} addr_ctx;
+
+static void addr_ctx_init(addr_ctx* c, const oracle_mapping* m) {
+  c->m = m;
+  c->offs = (uint64_t*)calloc((size_t)m->n_leaves, sizeof(uint64_t));
+  c->S = 0;
+  if (m->kind == ORACLE_AOS || m->kind == ORACLE_AOSOA) c->S = record_offsets(m, c->offs);
+  if (m->kind == ORACLE_SOA_SB) soa_sb_starts(m, c->offs);
+}
+
+static void addr_ctx_free(addr_ctx* c) { free(c->offs); }
+
+static void addr_of(const addr_ctx* c, uint64_t i, int32_t k, int32_t* blob, uint64_t* offset) {
+  const oracle_mapping* m = c->m;
+  uint64_t s_k = (uint64_t)m->leaf_size[k];
+  switch (m->kind) {
+    case ORACLE_AOS:
+      *blob = 0;
+      *offset = i * c->S + c->offs[k];
+      return;
+    case ORACLE_SOA_MB:
+      *blob = k;
+      *offset = i * s_k;
+      return;
+    case ORACLE_SOA_SB:
+      *blob = 0;
+      *offset = c->offs[k] + i * s_k;
+      return;
+    default: { /* ORACLE_AOSOA */
+      uint64_t L = (uint64_t)m->lanes;
+      *blob = 0;
+      *offset = (i / L) * L * c->S + c->offs[k] * L + (i % L) * s_k;
+      return;
+    }
+  }
+}
+
+/* splitmix64 output function (Steele, Lea, Flood 2014): the generator's mixer. */
+uint64_t oracle_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void oracle_generate(const oracle_mapping* m, uint8_t* const* blobs,
+                     const uint64_t* base, uint64_t seed, int64_t i0, int64_t i1) {
+  addr_ctx c;
+  addr_ctx_init(&c, m);
+  uint64_t K = (uint64_t)m->n_leaves;
+  for (int64_t i = i0; i < i1; ++i) {
+    for (int32_t k = 0; k < m->n_leaves; ++k) {
+      uint64_t v = oracle_splitmix64(seed ^ ((uint64_t)i * K + (uint64_t)k));
+      int32_t b;
+      uint64_t off;
+      addr_of(&c, (uint64_t)i, k, &b, &off);
+      uint8_t* p = blobs[b] + (off - (base ? base[b] : 0));
+      for (int32_t j = 0; j < m->leaf_size[k]; ++j) p[j] = (uint8_t)(v >> (8 * j));
+    }
+  }
+  addr_ctx_free(&c);
+}
+
+static int check_pair(const oracle_mapping* src, const oracle_mapping* dst) {
+  if (oracle_validate(src) || oracle_validate(dst)) return -1;
+  /* identical record dims and identical extents, else usage error. */
+  if (src->n_leaves != dst->n_leaves) return -3;
+  for (int32_t k = 0; k < src->n_leaves; ++k)
+    if (src->leaf_size[k] != dst->leaf_size[k]) return -3;
+  if (src->rank != dst->rank) return -2;
+  for (int32_t d = 0; d < src->rank; ++d)
+    if (src->extents[d] != dst->extents[d]) return -2;
+  return 0;
+}
+
+/* "nested loops over the array and record dimensions and copies field-wise". */
+static void copy_records(const addr_ctx* cs, const uint8_t* const* src_blobs, const uint64_t* src_base,
+                         const addr_ctx* cd, uint8_t* const* dst_blobs, const uint64_t* dst_base,
+                         int64_t i0, int64_t i1) {
+  int32_t K = cs->m->n_leaves;
+  for (int64_t i = i0; i < i1; ++i) {        /* array dimensions: outer loop */
+    for (int32_t k = 0; k < K; ++k) {        /* record leaves: inner loop */
+      int32_t bs, bd;
+      uint64_t os, od;
+      addr_of(cs, (uint64_t)i, k, &bs, &os);
+      addr_of(cd, (uint64_t)i, k, &bd, &od);
+      memcpy(dst_blobs[bd] + (od - (dst_base ? dst_base[bd] : 0)),
+             src_blobs[bs] + (os - (src_base ? src_base[bs] : 0)),
+             (size_t)cs->m->leaf_size[k]); /* bytes, never typed loads */
+    }
+  }
+}
+
+int oracle_copy_range(const oracle_mapping* src, const uint8_t* const* src_blobs,
+                      const uint64_t* src_base, const oracle_mapping* dst,
+                      uint8_t* const* dst_blobs, const uint64_t* dst_base,
+                      int64_t i0, int64_t i1) {
+  int rc = check_pair(src, dst);
+  if (rc) return rc;
+  int64_t n = oracle_record_count(src);
+  if (i0 < 0 || i1 > n || i0 > i1) return -1;
+  addr_ctx cs, cd;
+  addr_ctx_init(&cs, src);
+  addr_ctx_init(&cd, dst);
+  copy_records(&cs, src_blobs, src_base, &cd, dst_blobs, dst_base, i0, i1);
+  addr_ctx_free(&cs);
+  addr_ctx_free(&cd);
+  return 0;
+}
+
+int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
+                const oracle_mapping* dst, uint8_t* const* dst_blobs, int32_t nthreads) {
+  int rc = check_pair(src, dst);
+  if (rc) return rc;
+  /* Destination padding := 0 (reading #12): clear every dst blob first. */
+  int32_t nb = oracle_blob_count(dst);
+  uint64_t* sizes = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
+  oracle_blob_sizes(dst, sizes);
+  for (int32_t b = 0; b < nb; ++b) memset(dst_blobs[b], 0, (size_t)sizes[b]);
+  free(sizes);
+
+  addr_ctx cs, cd;
+  addr_ctx_init(&cs, src);
+  addr_ctx_init(&cd, dst);
+  int64_t n = oracle_record_count(src);
+  if (nthreads <= 1) {
+    copy_records(&cs, src_blobs, NULL, &cd, dst_blobs, NULL, 0, n);
+  } else {
+    /* (p) variant: the array loop split into contiguous ranges,
+     * one per thread. Result is independent of the partition. */
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads)
+    {
+      int64_t t = omp_get_thread_num(), T = omp_get_num_threads();
+      int64_t a = n * t / T, b = n * (t + 1) / T;
+      copy_records(&cs, src_blobs, NULL, &cd, dst_blobs, NULL, a, b);
+    }
+#else
+    copy_records(&cs, src_blobs, NULL, &cd, dst_blobs, NULL, 0, n);
+#endif
+  }
+  addr_ctx_free(&cs);
+  addr_ctx_free(&cd);
+  return 0;
+}

@@ -1,0 +1,101 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the LLAMA layout-aware
+ * copy (arXiv 2106.04284), used as the parity oracle for the CUDA path in
+ * paper_2106_04284_b200/.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or constant with the CUDA path, and must never be called
+ * from the product path.
+ *
+ * Citation convention: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * What it computes (§3.9 "Copying between views", §4.2 "naive copy"):
+ *   for every array index i (row-major) and every leaf k (DFS order,
+ *   P:296-309): dst[blob_d(i,k)][off_d(i,k) .. +s_k) = src[blob_s(i,k)][off_s(i,k) .. +s_k)
+ * where (blob, off) is the mapping's blobNrAndOffset (§3.7), written
+ * out per mapping kind directly from the definitions;
+ * destination padding bytes are written as 0 (reading #12).
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (worked examples, closed forms, C-compiler / numpy layouts, special cases,
+ * invariants, brute force).  No function is "parity unpinned".
+ */
+#ifndef LLAMA_ORACLE_H
+#define LLAMA_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mapping kinds. */
+enum { ORACLE_AOS = 0, ORACLE_SOA_SB = 1, ORACLE_SOA_MB = 2, ORACLE_AOSOA = 3 };
+
+/* A mapping as the oracle sees it: the flattened leaf sizes (DFS order; each
+ * leaf's alignment equals its size), the array extents (row-major),
+ * the kind, the AoSoA lane count L (ignored otherwise) and packed/aligned. */
+typedef struct {
+  int32_t n_leaves;
+  const int32_t* leaf_size; /* bytes, each in {1,2,4,8} */
+  int32_t rank;
+  const int64_t* extents;
+  int32_t kind;
+  int64_t lanes;
+  int32_t aligned; /* 0 = tightly packed, 1 = natural alignment */
+} oracle_mapping;
+
+/* Returns 0 if the mapping is well formed, -1 otherwise. */
+int oracle_validate(const oracle_mapping* m);
+
+/* Number of records = product of extents. */
+int64_t oracle_record_count(const oracle_mapping* m);
+
+/* Row-major linearisation, last index fastest.
+ * Returns -1 on an out-of-range index. */
+int64_t oracle_linearize(const oracle_mapping* m, const int64_t* index);
+
+/* Record-level offsets.  offsets[k] of leaf k within
+ * one record; return value = record size.  packed: sum of sizes, no padding.
+ * aligned: each leaf starts at the next multiple of its size; the record size
+ * is rounded up to the largest leaf alignment. */
+uint64_t oracle_packed_offsets(const oracle_mapping* m, uint64_t* offsets);
+uint64_t oracle_aligned_offsets(const oracle_mapping* m, uint64_t* offsets);
+
+/* Blob count and sizes. */
+int32_t oracle_blob_count(const oracle_mapping* m);
+void oracle_blob_sizes(const oracle_mapping* m, uint64_t* sizes);
+
+/* blobNrAndOffset for flat index i and leaf k. Returns 0 / -1. */
+int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
+                              int32_t* blob, uint64_t* offset);
+
+/* The seeded input generator (an input recipe, not the method): byte b of leaf
+ * k of record i is byte b (little endian) of splitmix64(seed ^ (i*K + k)).
+ * Writes the leaves of records [i0,i1) through the oracle's own address
+ * function.  Blob pointers are windows: blobs[b] holds the bytes starting at
+ * global blob offset base[b] (base may be NULL = all zero). */
+uint64_t oracle_splitmix64(uint64_t x);
+void oracle_generate(const oracle_mapping* m, uint8_t* const* blobs,
+                     const uint64_t* base, uint64_t seed, int64_t i0, int64_t i1);
+
+/* The copy (P:757 naive copy: array loop outer, leaf loop inner, one s_k-byte
+ * element copy per (i,k) via both mappings' blobNrAndOffset).  Copies records
+ * [i0,i1) only; does NOT clear dst (the caller supplies zeroed windows).
+ * Returns 0, or -2 shape mismatch (extents), -3 record mismatch (leaf sizes),
+ * -1 invalid. */
+int oracle_copy_range(const oracle_mapping* src, const uint8_t* const* src_blobs,
+                      const uint64_t* src_base, const oracle_mapping* dst,
+                      uint8_t* const* dst_blobs, const uint64_t* dst_base,
+                      int64_t i0, int64_t i1);
+
+/* Whole-view copy: zero-fills every dst blob (padding := 0), then copies all
+ * records. nthreads > 1 runs the paper's "(p)" variant: the array loop is
+ * split over OpenMP threads. */
+int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
+                const oracle_mapping* dst, uint8_t* const* dst_blobs, int32_t nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

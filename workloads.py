@@ -1,0 +1,54 @@
+"""Seeded synthetic workload recipes shared by tests/ and bench.py.
+
+This module holds only DATA (schema strings, extents, mapping-pair lists, seeds);
+it contains none of the method's arithmetic and imports neither the product
+package nor the oracle.  Both sides implement the same counter-based input
+generator themselves (splitmix64 of seed ^ (i*K + k)).
+"""
+
+# Particle7: "7 floats"; field order Pos, Vel, Mass as in the
+# n-body code.  DESIGN.md reading #11.
+PARTICLE7 = "Particle{Pos{X:f32,Y:f32,Z:f32},Vel{X:f32,Y:f32,Z:f32},Mass:f32}"
+
+# Listing 1: the paper's nested record with a static array.
+LISTING1 = "Particle{Id:u16,Pos{X:f32,Y:f32},Mass:f64,Flags:bool[3]}"
+
+# Vec of Listing 1.
+VEC = "Vec{X:f32,Y:f32}"
+
+# HEP100 stand-in for the CMS event record (P:775 is an internal dataset):
+# 10 groups of 10 mixed leaves -> 100 leaves (20 f64, 30 f32, 10 i32, 20 i16,
+# 20 bool); packed 380 B, aligned 480 B.  DESIGN.md reading #19.
+_HEP_GROUP = "{pt:f32,eta:f32,phi:f32,mass:f64,charge:i16,pdgId:i32,nHits:i16,isGood:bool,isTight:bool,weight:f64}"
+HEP100 = "Event{" + ",".join(f"G{g}{_HEP_GROUP}" for g in range(10)) + "}"
+
+# A nesting discriminator (SURVEY §8(c) reading #3): flattened per-leaf
+# alignment gives 16 B, C nested-struct rules would give 24 B.
+OUTER = "Outer{A{d:f64,b:bool},c:bool}"
+
+SCHEMAS = {"particle7": PARTICLE7, "listing1": LISTING1, "vec": VEC, "hep100": HEP100}
+
+# Mapping descriptors: (kind, lanes, aligned).  CLI names follow S:341.
+MAPPINGS = {
+    "aos": ("aos", 1, False),            # packed AoS  (reading #10: "AoS" := packed)
+    "aos_aligned": ("aos", 1, True),     # aligned AoS
+    "soa_mb": ("soa_mb", 1, False),      # SoA multi-blob (reading #10: "SoA" := MB)
+    "soa_sb": ("soa_sb", 1, False),      # SoA single-blob
+    "aosoa4": ("aosoa", 4, False),
+    "aosoa8": ("aosoa", 8, False),
+    "aosoa32": ("aosoa", 32, False),
+}
+
+SEEDS = (42, 1, 2)  # seed 42 default
+
+# BASELINE.json configs.
+C1 = dict(name="C1", schema="particle7", extents=(4096,), pairs=[("aos", "soa_mb")])
+_C2_KINDS = ["aos", "soa_mb", "aosoa8", "aosoa32"]
+C2 = dict(name="C2", schema="particle7", extents=(16_777_216,),
+          pairs=[(a, b) for a in _C2_KINDS for b in _C2_KINDS])
+C3 = dict(name="C3", schema="hep100", extents=(67_108_864,),
+          pairs=[(a, b) for a in ("aos", "aos_aligned", "soa_mb")
+                 for b in ("aos", "aos_aligned", "soa_mb") if a != b])
+C4 = dict(name="C4", schema="listing1", extents=(8192, 8192), pairs=[("aosoa32", "soa_sb")])
+C5 = dict(name="C5", schema="particle7", extents=(1 << 27,), pairs=[("aos", "soa_mb")])
+CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5}
