@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: layout-copy GB/s (read + write bytes) per mapping pair on B200.
+
+Default workload (BASELINE.json configs[1], "C2"): 16,777,216 Particle7
+records (7 x f32), all 16 ordered pairs of {packed AoS, SoA
+multi-blob, AoSoA8, AoSoA32}.  One step = the 16 layout-aware copies, each one
+llama_copy through the C ABI.  value = sum over pairs of (src footprint + dst
+footprint) / step time, summed over ranks (weak scaling: every rank relayouts
+its own 16M records; no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the CPU oracle (oracle/, plain C naive copy) on a
+bounded sample of the same workload; it needs no GPU.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = W_METRIC = "layout-copy GB/s (read+write) per mapping pair vs 8 TB/s HBM, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--per-pair", default=None, help="write per-pair timings (json) to this file")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_desc(cfg, world):
+    if cfg["name"] == "C2":
+        return dict(workload="C2: Particle7 (7x f32) x 16,777,216 records per GPU, 16 ordered pairs of "
+                             "{packed AoS, SoA MB, AoSoA8, AoSoA32}",
+                    records_per_gpu=cfg["extents"][0], pairs=len(cfg["pairs"]),
+                    l2="inputs larger than L2 (each pair reads 470 MB and writes 470 MB; L2 is 126 MB)",
+                    parallelism=f"dp{world} (independent per-GPU relayout, weak scaling)")
+    return dict(workload="C4: Listing-1 record (u16, f32 x2, f64, bool x3) 8192 x 8192, AoSoA32 -> SoA SB, "
+                         "rows sharded over GPUs", records=8192 * 8192, pairs=1,
+                l2="inputs larger than L2", parallelism=f"dp{world} (extent sharding, strong scaling)")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows if len(r) >= 9 for j in range(4)
+                          if r[5 + j].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg, target_s=12.0):
+    """The oracle (plain C naive copy, 1 thread) on a bounded prefix of the
+    workload: every pair on the same prefix of n' records."""
+    import oracle
+    schema = W.SCHEMAS[cfg["schema"]]
+    names = sorted({x for p in cfg["pairs"] for x in p})
+    # calibrate n' so that all pairs together take ~target_s
+    n_try = 1 << 16
+    views, maps = {}, {}
+
+    def setup(n):
+        for name in names:
+            maps[name] = oracle.Mapping(schema, [n], *W.MAPPINGS[name])
+            views[name] = oracle.make_view(maps[name], 42)
+
+    setup(n_try)
+    t0 = time.perf_counter()
+    for a, b in cfg["pairs"]:
+        oracle.copy(maps[a], views[a], maps[b])
+    dt = time.perf_counter() - t0
+    n = int(n_try * max(1.0, target_s / max(dt, 1e-6)))
+    n = max(1 << 16, min(n, cfg["extents"][0] if cfg["name"] == "C2" else 1 << 24))
+    n -= n % 32
+    setup(n)
+    dsts = {b: maps[b].alloc() for b in names}
+    total_bytes = 0
+    t0 = time.perf_counter()
+    for a, b in cfg["pairs"]:
+        oracle.copy(maps[a], views[a], maps[b], dsts[b])
+        total_bytes += sum(maps[a].blob_sizes()) + sum(maps[b].blob_sizes())
+    dt = time.perf_counter() - t0
+    return {"value": total_bytes / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg['name']} pairs on a prefix of {n} records ({total_bytes / 1e9:.2f} GB moved, "
+                      f"{dt:.1f} s, plain C naive copy, 1 thread)"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    schema = W.SCHEMAS[cfg["schema"]]
+    names = sorted({x for p in cfg["pairs"] for x in p})
+    # each step: all pairs on a bounded prefix, sized so steps+warmup take minutes at most
+    n = 1 << 20
+    maps = {k: oracle.Mapping(schema, [n], *W.MAPPINGS[k]) for k in names}
+    views = {k: oracle.make_view(maps[k], 42) for k in names}
+    dsts = {k: maps[k].alloc() for k in names}
+    step_bytes = sum(sum(maps[a].blob_sizes()) + sum(maps[b].blob_sizes()) for a, b in cfg["pairs"])
+
+    def step():
+        for a, b in cfg["pairs"]:
+            oracle.copy(maps[a], views[a], maps[b], dsts[b])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    value = step_bytes / dt / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64, seed 42)",
+            "config": dict(workload_desc(cfg, 1), sample_records=n), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{cfg['name']} pairs on a prefix of {n} records per step"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_04284_b200 as llama
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    schema = W.SCHEMAS[cfg["schema"]]
+    if cfg["name"] == "C4":
+        from paper_2106_04284_b200.shard import shard_extents
+        ext, _ = shard_extents(list(cfg["extents"]), world, rank, multiple=32)
+    else:
+        ext = list(cfg["extents"])
+    names = sorted({x for p in cfg["pairs"] for x in p})
+    maps = {k: llama.Mapping(schema, ext, *W.MAPPINGS[k]) for k in names}
+    src = {k: maps[k].alloc("cuda") for k in names}
+    dst = {k: maps[k].alloc("cuda") for k in names}
+    for k in names:
+        llama.generate(maps[k], src[k], 42)
+    stream = torch.cuda.current_stream()
+    pairs = cfg["pairs"]
+    pair_bytes = [sum(maps[a].blob_sizes()) + sum(maps[b].blob_sizes()) for a, b in pairs]
+    step_bytes = sum(pair_bytes)
+    plans = [llama.plan(maps[a], maps[b]) for a, b in pairs]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(events=None):
+        for j, (a, b) in enumerate(pairs):
+            if events is not None:
+                events[j][0].record(stream)
+            llama.copy(maps[a], src[a], maps[b], dst[b], stream=stream)
+            if events is not None:
+                events[j][1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # timed region: K steps; per-launch events on the launching stream
+    ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in pairs]
+          for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = llama.launch_count()
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(ev[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = llama.launch_count() - launches0
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = step_bytes * world / (ms * 1e-3) / 1e9
+
+    per_pair = []
+    for j, (a, b) in enumerate(pairs):
+        times = [ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(args.steps)]
+        per_pair.append({"src": a, "dst": b, "path": plans[j]["path"], "bytes": pair_bytes[j],
+                         "ms": statistics.median(times), "gbs": pair_bytes[j] / (statistics.median(times) * 1e6)})
+    # dominant kernel path = largest share of the step
+    share = {}
+    for p in per_pair:
+        share.setdefault(p["path"], [0.0, 0, 0])
+        share[p["path"]][0] += p["ms"]
+        share[p["path"]][1] += p["bytes"]
+        share[p["path"]][2] += 1
+    dom = max(share, key=lambda k: share[k][0])
+    peak, peak_src = hbm_peak()
+    dom_ms_avg = share[dom][0] / share[dom][2]
+    dom_bytes_avg = share[dom][1] / share[dom][2]
+    achieved = dom_bytes_avg / (dom_ms_avg * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": f"k_permute (path {dom})" if dom == "permute" else f"path {dom}",
+                "launches_per_step": share[dom][2], "algorithmic_bytes_per_launch": dom_bytes_avg,
+                "peak_source": peak_src, "share_of_step": share[dom][0] / sum(v[0] for v in share.values())}
+
+    extra = {}
+    if rank == 0:
+        # in-run references: naive element-wise GPU copy and a plain device memcpy of equal bytes
+        naive_ms = 0.0
+        for j, (a, b) in enumerate(pairs):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            llama.copy(maps[a], src[a], maps[b], dst[b], stream=stream, path="naive")
+            e0.record(stream)
+            llama.copy(maps[a], src[a], maps[b], dst[b], stream=stream, path="naive")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            naive_ms += e0.elapsed_time(e1)
+        nb = pair_bytes[0] // 2
+        x = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        y = torch.empty_like(x)
+        y.copy_(x)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            y.copy_(x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        memcpy_gbs = 2 * nb * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        del x, y
+        extra = {"naive_gpu_gbs": step_bytes / (naive_ms * 1e-3) / 1e9, "memcpy_gbs": memcpy_gbs,
+                 "frac_of_8tbs": value / world / 8000.0, "frac_of_measured_copy": value / world / peak}
+
+    # end to end through the public API with HOST buffers: H2D of each pair's
+    # source, the copy, D2H of its destination, every step
+    e2e = None
+    if not args.no_e2e:
+        hsrc = {k: [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in src[k]] for k in names}
+        hdst = {k: [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in dst[k]] for k in names}
+        for k in names:
+            for h, t in zip(hsrc[k], src[k]):
+                h.copy_(t)
+        h2d = sum(sum(maps[a].blob_sizes()) for a, b in pairs)
+        d2h = sum(sum(maps[b].blob_sizes()) for a, b in pairs)
+
+        def e2e_step():
+            for a, b in pairs:
+                for t, h in zip(src[a], hsrc[a]):
+                    t.copy_(h, non_blocking=True)
+                llama.copy(maps[a], src[a], maps[b], dst[b], stream=stream)
+                for h, t in zip(hdst[b], dst[b]):
+                    h.copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": step_bytes * world / (ems * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+        del hsrc, hdst
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak" if cfg["name"] == "C2" else "strong", "vs_baseline": None, "dtype": "u8",
+                "data": "synthetic (splitmix64 per leaf, seed 42)", "config": workload_desc(cfg, world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk, **extra}
+        print(json.dumps(line), flush=True)
+        if args.per_pair:
+            with open(args.per_pair, "w") as f:
+                json.dump(per_pair, f, indent=1)
+        else:
+            sys.stderr.write("\n".join(f"{p['src']:>8} -> {p['dst']:<8} {p['path']:<9} {p['ms']:.3f} ms "
+                                       f"{p['gbs']:.0f} GB/s" for p in per_pair) + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,200 @@
+/*
+ * llama_b200.h -- C ABI of the B200-native layout-aware copy.
+ *
+ * Implements the hot path of LLAMA (Gruber et al., arXiv 2106.04284): copying
+ * an N-dimensional array of nested records between two *views* of the same
+ * data space that use different *mappings* (§3.1 "layout-aware copy
+ * operations between instances of the same data space but with different
+ * mappings"; §3.9; §4.2).
+ *
+ * Citation convention: P:n = PAPER.md line n, S:n = SPEC.md line n (the
+ * reference texts of the paper).
+ *
+ * Conventions for every function:
+ *   - Thread safety: all functions are thread-safe. Mappings are immutable
+ *     after creation and may be shared between threads and devices.
+ *   - Ownership: the library owns llama_mapping objects (create/destroy).  The
+ *     caller owns all blob memory ("LLAMA ... function[s] orthogonally to
+ *     memory allocation"); the library never allocates or frees blobs.  Arrays
+ *     passed in (descriptors, blob pointer arrays, sizes) are read during the
+ *     call only.
+ *   - Errors: a function returns LLAMA_OK or a negative llama_status.  All
+ *     validation happens synchronously before any device work is enqueued,
+ *     and a failed call does no partial work.  llama_last_error_message()
+ *     returns a thread-local description of the last failure.  No C++
+ *     exception crosses this ABI.
+ *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = the legacy
+ *     default stream) that belongs to the calling thread's current device.
+ *     Device functions enqueue and return; ordering follows CUDA stream
+ *     semantics.  Blobs must stay alive until the enqueued work completes.
+ */
+#ifndef LLAMA_B200_H
+#define LLAMA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LLAMA_OK = 0,
+  LLAMA_ERR_INVALID_ARGUMENT = -1, /* NULL pointer, bad enum, too few blobs, ... */
+  LLAMA_ERR_SHAPE_MISMATCH = -2,   /* different array extents */
+  LLAMA_ERR_RECORD_MISMATCH = -3,  /* different leaf type lists */
+  LLAMA_ERR_UNSUPPORTED = -4,      /* beyond the implemented limits (see below) */
+  LLAMA_ERR_ALIGNMENT = -5,        /* a blob base address not 16-byte aligned */
+  LLAMA_ERR_OVERLAP = -6,          /* src and dst byte ranges overlap (in-situ is out of scope) */
+  LLAMA_ERR_CUDA = -7,             /* a CUDA launch / runtime call failed */
+  LLAMA_ERR_OOM = -8               /* host allocation failed */
+} llama_status;
+
+/* Leaf scalar types.  Size = alignment; bool is one
+ * byte.  Leaf bytes are copied verbatim: no bool normalisation, no
+ * floating-point canonicalisation (NaN payloads survive). */
+typedef enum {
+  LLAMA_BOOL = 0, LLAMA_I8, LLAMA_U8, LLAMA_I16, LLAMA_U16, LLAMA_I32, LLAMA_U32,
+  LLAMA_I64, LLAMA_U64, LLAMA_F32, LLAMA_F64
+} llama_scalar;
+
+/* Mapping kinds. */
+typedef enum {
+  LLAMA_AOS = 0,             /* P:460-463 fields after each other, repeated per record */
+  LLAMA_SOA_SINGLE_BLOB = 1, /* P:465-468 one sub-array per leaf, all in one blob */
+  LLAMA_SOA_MULTI_BLOB = 2,  /* P:465-468 one blob per leaf ("SoA MB") */
+  LLAMA_AOSOA = 3            /* P:470-473 AoS of blocks that repeat each field L times */
+} llama_kind;
+
+/* A mapping description (a mapping is configured on the array and
+ * record dimensions).
+ *   leaf_types/n_leaves: the record dimension flattened depth-first in
+ *     declaration order, 1 <= n_leaves <= LLAMA_MAX_LEAVES.
+ *   extents/rank: the array dimensions, row-major (last index fastest,
+ *     P:414-416), 1 <= rank <= LLAMA_MAX_RANK, every extent >= 0.
+ *   kind: see llama_kind.  lanes: AoSoA lane count L >= 1 (any L, not only
+ *     powers of two; ignored for other kinds).
+ *   aligned: 0 = tightly packed, 1 = each leaf at a multiple of its size and
+ *     the record rounded up to the largest leaf.  For SoA
+ *     single-blob, aligned=1 rounds each leaf sub-array start up to the leaf
+ *     size (reading #9); for SoA multi-blob it has no effect. */
+typedef struct {
+  const llama_scalar* leaf_types;
+  int32_t n_leaves;
+  const int64_t* extents;
+  int32_t rank;
+  llama_kind kind;
+  int64_t lanes;
+  int32_t aligned;
+} llama_mapping_desc;
+
+#define LLAMA_MAX_LEAVES 128
+#define LLAMA_MAX_RANK 8
+#define LLAMA_MAX_BLOBS 128
+
+typedef struct llama_mapping llama_mapping; /* opaque, immutable */
+
+/* Creates a mapping.  *out receives a new mapping on LLAMA_OK.
+ * Errors: INVALID_ARGUMENT (NULL, bad enum, extent < 0, lanes < 1),
+ * UNSUPPORTED (n_leaves or rank beyond the limits, blob sizes overflowing 64
+ * bits). */
+llama_status llama_mapping_create(const llama_mapping_desc* desc, llama_mapping** out);
+
+/* Convenience: parses a schema string in the grammar of S:122-126, e.g.
+ * "Particle{Id:u16,Pos{X:f32,Y:f32},Mass:f64,Flags:bool[3]}" (Listing 1,
+ * P:296-313); static arrays become n fields.  Same errors as
+ * llama_mapping_create, plus INVALID_ARGUMENT on a malformed schema. */
+llama_status llama_mapping_create_from_schema(const char* schema, const int64_t* extents,
+                                              int32_t rank, llama_kind kind, int64_t lanes,
+                                              int32_t aligned, llama_mapping** out);
+
+/* Destroys a mapping; NULL-safe.  Plans cached for pairs involving it are
+ * released. */
+void llama_mapping_destroy(llama_mapping* m);
+
+/* Blob count ("a compile time blob count"): 1, or n_leaves for SoA MB.
+ * Returns -1 for a NULL mapping. */
+int32_t llama_blob_count(const llama_mapping* m);
+
+/* Blob sizes in bytes.  Writes llama_blob_count(m) values into sizes;
+ * capacity is the array length.  INVALID_ARGUMENT if capacity is too small. */
+llama_status llama_blob_sizes(const llama_mapping* m, uint64_t* sizes, int32_t capacity);
+
+/* Record count = product of the extents; -1 for a NULL mapping. */
+int64_t llama_record_count(const llama_mapping* m);
+
+/* Number of leaves; writes the leaf types into types[0..capacity) if non-NULL. */
+int32_t llama_leaf_types(const llama_mapping* m, llama_scalar* types, int32_t capacity);
+
+/* blobNrAndOffset: the blob number and byte offset of leaf `leaf` of
+ * the record at the rank-dimensional `index`.  Host-side, for tests and tools.
+ * INVALID_ARGUMENT on a NULL argument or an out-of-range index / leaf. */
+llama_status llama_blob_nr_and_offset(const llama_mapping* m, const int64_t* index, int32_t leaf,
+                                      int32_t* blob, uint64_t* offset);
+
+/* The layout-aware copy.
+ *   src_blobs: llama_blob_count(src_map) device pointers, each 16-byte aligned,
+ *     each at least the corresponding blob size.  Never written.
+ *   dst_blobs: llama_blob_count(dst_map) device (or peer-mapped) pointers,
+ *     16-byte aligned.
+ * Result: for every record i and leaf k the s_k bytes of the leaf land at the
+ * destination mapping's blob/offset, bit-exactly; every destination byte in
+ * [0, blob size) of every destination blob is written, padding bytes with 0
+ * (reading #12).  Source padding never influences the result.
+ * Errors (synchronous, before any launch): RECORD_MISMATCH, SHAPE_MISMATCH,
+ * INVALID_ARGUMENT (NULL mapping/pointer array/pointer), ALIGNMENT, OVERLAP,
+ * UNSUPPORTED; CUDA on a launch failure. */
+llama_status llama_copy(const llama_mapping* src_map, void* const* src_blobs,
+                        const llama_mapping* dst_map, void* const* dst_blobs, void* stream);
+
+/* Copy paths. */
+typedef enum {
+  LLAMA_PATH_AUTO = 0,     /* planner's choice */
+  LLAMA_PATH_NAIVE = 1,    /* element-wise: thread per record, leaf loop */
+  LLAMA_PATH_BLOBCOPY = 2, /* identical layout without padding: raw blob copy */
+  LLAMA_PATH_RUN = 3,      /* field-run copy: common contiguous runs >= 16 B */
+  LLAMA_PATH_PERMUTE = 4   /* TMA-staged tile permute through shared memory */
+} llama_path;
+
+typedef struct {
+  llama_path path;      /* forced path; UNSUPPORTED if not applicable to the pair */
+  int32_t tile_records; /* PERMUTE only: records per tile, 0 = planner's choice */
+} llama_copy_options;
+
+/* llama_copy with options (NULL = defaults = llama_copy). */
+llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
+                           const llama_mapping* dst_map, void* const* dst_blobs, void* stream,
+                           const llama_copy_options* options);
+
+/* What the planner chooses for a pair (no device work). */
+typedef struct {
+  llama_path path;
+  int32_t tile_records;     /* PERMUTE: records per tile */
+  int32_t smem_bytes;       /* PERMUTE: dynamic shared memory per CTA */
+  int32_t moves;            /* PERMUTE: per-record move table length */
+  int32_t tma;              /* PERMUTE: 1 if every segment is moved by TMA bulk copies */
+  uint64_t src_bytes;       /* sum of source blob sizes */
+  uint64_t dst_bytes;       /* sum of destination blob sizes */
+} llama_plan_info;
+
+llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_map,
+                        const llama_copy_options* options, llama_plan_info* out);
+
+/* Seeded synthetic input (an input recipe, not the method): fills every blob
+ * byte with pad_byte, then writes byte b of leaf k of record i as byte b
+ * (little endian) of splitmix64(seed ^ (i*K + k)), K = n_leaves.  Same blob
+ * requirements as llama_copy's dst_blobs. */
+llama_status llama_generate(const llama_mapping* m, void* const* blobs, uint64_t seed,
+                            uint8_t pad_byte, void* stream);
+
+/* Number of kernels this library has launched in this process (monotonic). */
+uint64_t llama_launch_count(void);
+
+const char* llama_status_string(llama_status s);
+const char* llama_last_error_message(void); /* thread-local, never NULL */
+const char* llama_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LLAMA_B200_H */

@@ -1,0 +1,242 @@
+"""B200-native layout-aware copy (LLAMA, arXiv 2106.04284) -- Python binding.
+
+Thin ctypes marshalling over the C ABI in include/llama_b200.h (the in-tree
+libllama_b200.so, sm_100a kernels).  Every step of the copy runs in the
+library's CUDA kernels; this module only converts arguments.  There is no CPU
+fallback: if the library cannot be loaded, import fails loudly.
+
+PyTorch provides device memory (torch.uint8 tensors as blobs) and
+streams; it is plumbing, not the product.
+
+    import paper_2106_04284_b200 as llama
+    src = llama.Mapping("Particle{Pos{X:f32,Y:f32,Z:f32},Vel{X:f32,Y:f32,Z:f32},Mass:f32}",
+                        [1 << 20], "aos")
+    dst = llama.Mapping(src.schema, [1 << 20], "soa_mb")
+    a, b = src.alloc("cuda"), dst.alloc("cuda")
+    llama.generate(src, a, seed=42)
+    llama.copy(src, a, dst, b)
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libllama_b200.so")
+
+KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3}
+PATHS = {"auto": 0, "naive": 1, "blobcopy": 2, "run": 3, "permute": 4}
+PATH_NAMES = {v: k for k, v in PATHS.items()}
+STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_MISMATCH",
+          -3: "LLAMA_ERR_RECORD_MISMATCH", -4: "LLAMA_ERR_UNSUPPORTED", -5: "LLAMA_ERR_ALIGNMENT",
+          -6: "LLAMA_ERR_OVERLAP", -7: "LLAMA_ERR_CUDA", -8: "LLAMA_ERR_OOM"}
+
+# Symbols declared in include/llama_b200.h (checked by tests/test_capi_host.py).
+EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_mapping_destroy",
+           "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
+           "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
+           "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version"]
+
+
+class LlamaError(RuntimeError):
+    def __init__(self, status, message):
+        self.status = status
+        self.status_name = STATUS.get(status, str(status))
+        super().__init__(f"{self.status_name}: {message}")
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("leaf_types", ctypes.POINTER(ctypes.c_int)), ("n_leaves", ctypes.c_int32),
+                ("extents", ctypes.POINTER(ctypes.c_int64)), ("rank", ctypes.c_int32),
+                ("kind", ctypes.c_int), ("lanes", ctypes.c_int64), ("aligned", ctypes.c_int32)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32)]
+
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("moves", ctypes.c_int32), ("tma", ctypes.c_int32), ("src_bytes", ctypes.c_uint64),
+                ("dst_bytes", ctypes.c_uint64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        from . import _build
+        _build.build()
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    vpp = P(ctypes.c_void_p)
+    lib.llama_mapping_create.argtypes = [P(_Desc), P(ctypes.c_void_p)]
+    lib.llama_mapping_create_from_schema.argtypes = [ctypes.c_char_p, P(ctypes.c_int64), ctypes.c_int32,
+                                                     ctypes.c_int, ctypes.c_int64, ctypes.c_int32,
+                                                     P(ctypes.c_void_p)]
+    lib.llama_mapping_destroy.argtypes = [ctypes.c_void_p]
+    lib.llama_mapping_destroy.restype = None
+    lib.llama_blob_count.argtypes = [ctypes.c_void_p]
+    lib.llama_blob_sizes.argtypes = [ctypes.c_void_p, P(ctypes.c_uint64), ctypes.c_int32]
+    lib.llama_record_count.argtypes = [ctypes.c_void_p]
+    lib.llama_record_count.restype = ctypes.c_int64
+    lib.llama_leaf_types.argtypes = [ctypes.c_void_p, P(ctypes.c_int), ctypes.c_int32]
+    lib.llama_blob_nr_and_offset.argtypes = [ctypes.c_void_p, P(ctypes.c_int64), ctypes.c_int32,
+                                             P(ctypes.c_int32), P(ctypes.c_uint64)]
+    lib.llama_copy.argtypes = [ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
+    lib.llama_copy_ex.argtypes = [ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p, P(_Options)]
+    lib.llama_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(_Options), P(_PlanInfo)]
+    lib.llama_generate.argtypes = [ctypes.c_void_p, vpp, ctypes.c_uint64, ctypes.c_uint8, ctypes.c_void_p]
+    lib.llama_launch_count.restype = ctypes.c_uint64
+    lib.llama_status_string.restype = ctypes.c_char_p
+    lib.llama_status_string.argtypes = [ctypes.c_int]
+    lib.llama_last_error_message.restype = ctypes.c_char_p
+    lib.llama_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        raise LlamaError(status, _lib.llama_last_error_message().decode())
+
+
+class Mapping:
+    """A mapping of a record dimension (schema string)
+    over array extents.  kind: 'aos' | 'soa_sb' | 'soa_mb' | 'aosoa'."""
+
+    def __init__(self, schema, extents, kind="aos", lanes=1, aligned=False):
+        self.schema = schema
+        self.extents = [int(e) for e in extents]
+        self.kind = kind
+        self.lanes = int(lanes)
+        self.aligned = bool(aligned)
+        if kind not in KINDS:
+            raise ValueError(f"unknown mapping kind {kind!r}")
+        ext = (ctypes.c_int64 * len(self.extents))(*self.extents)
+        h = ctypes.c_void_p()
+        _check(_lib.llama_mapping_create_from_schema(schema.encode(), ext, len(self.extents), KINDS[kind],
+                                                     self.lanes, int(self.aligned), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.llama_mapping_destroy(h)
+            self._h = None
+
+    def __repr__(self):
+        return f"Mapping({self.kind}, lanes={self.lanes}, aligned={self.aligned}, extents={self.extents})"
+
+    @property
+    def blob_count(self):
+        return int(_lib.llama_blob_count(self._h))
+
+    def blob_sizes(self):
+        n = self.blob_count
+        out = (ctypes.c_uint64 * n)()
+        _check(_lib.llama_blob_sizes(self._h, out, n))
+        return [int(v) for v in out]
+
+    @property
+    def record_count(self):
+        return int(_lib.llama_record_count(self._h))
+
+    @property
+    def leaf_count(self):
+        return int(_lib.llama_leaf_types(self._h, None, 0))
+
+    def leaf_types(self):
+        n = self.leaf_count
+        out = (ctypes.c_int * n)()
+        _lib.llama_leaf_types(self._h, out, n)
+        return list(out)
+
+    def blob_nr_and_offset(self, index, leaf):
+        if isinstance(index, int):
+            index = [index]
+        idx = (ctypes.c_int64 * len(index))(*[int(i) for i in index])
+        b = ctypes.c_int32()
+        o = ctypes.c_uint64()
+        _check(_lib.llama_blob_nr_and_offset(self._h, idx, int(leaf), ctypes.byref(b), ctypes.byref(o)))
+        return int(b.value), int(o.value)
+
+    def footprint(self):
+        return sum(self.blob_sizes())
+
+    def alloc(self, device="cuda"):
+        """One torch.uint8 tensor per blob (torch allocations are >= 256-B aligned)."""
+        import torch
+        return [torch.empty(max(s, 1), dtype=torch.uint8, device=device)[:s] if s else
+                torch.empty(16, dtype=torch.uint8, device=device) for s in self.blob_sizes()]
+
+
+def _ptrs(blobs, sizes, what):
+    if len(blobs) < len(sizes):
+        raise LlamaError(-1, f"{what}: {len(sizes)} blobs needed, {len(blobs)} given")
+    arr = (ctypes.c_void_p * max(1, len(blobs)))()
+    for j, b in enumerate(blobs):
+        if isinstance(b, int):
+            arr[j] = b
+            continue
+        if j < len(sizes) and b.numel() * b.element_size() < sizes[j]:
+            raise LlamaError(-1, f"{what}[{j}] holds {b.numel() * b.element_size()} bytes, needs {sizes[j]}")
+        if not b.is_cuda:
+            raise LlamaError(-1, f"{what}[{j}] is not a CUDA tensor")
+        arr[j] = b.data_ptr()
+    return arr
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _options(path, tile_records):
+    return _Options(PATHS[path or "auto"], int(tile_records))
+
+
+def copy(src_map, src_blobs, dst_map, dst_blobs, stream=None, path=None, tile_records=0):
+    """The layout-aware copy (llama_copy / llama_copy_ex), enqueued on `stream`
+    (default: torch's current stream)."""
+    s = _ptrs(src_blobs, src_map.blob_sizes(), "src_blobs")
+    d = _ptrs(dst_blobs, dst_map.blob_sizes(), "dst_blobs")
+    opt = _options(path, tile_records)
+    _check(_lib.llama_copy_ex(src_map.handle, s, dst_map.handle, d, _stream(stream), ctypes.byref(opt)))
+
+
+def plan(src_map, dst_map, path=None, tile_records=0):
+    """The planner's decision for a pair (no device work)."""
+    info = _PlanInfo()
+    opt = _options(path, tile_records)
+    _check(_lib.llama_plan(src_map.handle, dst_map.handle, ctypes.byref(opt), ctypes.byref(info)))
+    return {"path": PATH_NAMES[info.path], "tile_records": info.tile_records, "smem_bytes": info.smem_bytes,
+            "moves": info.moves, "tma": bool(info.tma), "src_bytes": int(info.src_bytes),
+            "dst_bytes": int(info.dst_bytes)}
+
+
+def generate(m, blobs, seed=42, pad_byte=0, stream=None):
+    """Seeded synthetic input (llama_generate): padding := pad_byte, leaf bytes
+    from splitmix64(seed ^ (i*K + k))."""
+    p = _ptrs(blobs, m.blob_sizes(), "blobs")
+    _check(_lib.llama_generate(m.handle, p, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(pad_byte) & 0xFF,
+                               _stream(stream)))
+
+
+def launch_count():
+    """Kernels launched by the library in this process."""
+    return int(_lib.llama_launch_count())
+
+
+def version():
+    return _lib.llama_version().decode()

@@ -1,0 +1,102 @@
+// device.cuh -- device helpers shared by the sm_100a kernels: the normal-form
+// address function (P:451 blobNrAndOffset) and thin PTX wrappers for mbarrier
+// and TMA bulk copies (cp.async.bulk, SASS UBLKCP).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "params.hpp"
+
+namespace llb {
+
+// i -> (i / L, i % L): shift/mask when L is a power of two.
+__device__ __forceinline__ uint64_t block_of(uint64_t i, const DevSide& s) {
+  return s.lshift != kNoShift ? (i >> s.lshift) : (i / s.L);
+}
+
+// off(i,k) = base_k + (i / L) * B + F_k + (i % L) * s_k
+__device__ __forceinline__ uint64_t nf_offset(uint64_t i, const DevSide& s, const DevLeaf& l) {
+  const uint64_t q = block_of(i, s);
+  return l.base + q * s.B + l.F + (i - q * s.L) * l.size;
+}
+
+// Copies n bytes between arbitrary addresses using the widest naturally
+// aligned access both pointers allow (never assumes alignment; packed
+// layouts put f64 at odd offsets).
+__device__ __forceinline__ void copy_elem(uint8_t* d, const uint8_t* s, uint32_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s);
+  if (n == 8 && (a & 7) == 0) { *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const uint64_t*>(s); return; }
+  if (n == 4 && (a & 3) == 0) { *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(s); return; }
+  if (n == 2 && (a & 1) == 0) { *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s); return; }
+  for (uint32_t j = 0; j < n; ++j) d[j] = s[j];
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LLB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LLB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA bulk copy global -> shared, completion counted on an mbarrier.
+// Requires 16-B aligned addresses and a 16-B multiple size.
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA bulk copy shared -> global, tracked by the issuing thread's bulk groups.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// Wait until at most N of this thread's bulk groups still read shared memory.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Orders this thread's generic-proxy shared-memory writes before later
+// async-proxy (TMA) reads of them.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace llb

@@ -1,0 +1,55 @@
+// mapping.hpp -- the runtime mapping descriptor (§3.7) in the AoSoA
+// normal form, plus the record-dimension schema parser.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "llama_b200.h"
+#include "params.hpp"
+
+namespace llb {
+
+uint32_t scalar_size(llama_scalar t);
+
+// Parses the schema grammar of S:122-126 and flattens it depth-first
+// (P:290 static arrays -> n fields; P:296-309 declaration order).
+// Returns false with a message on a malformed schema.
+bool parse_schema(const std::string& schema, std::vector<llama_scalar>* leaves, std::string* err);
+
+struct Mapping {
+  uint64_t id = 0;  // unique per process, keys the plan cache
+  std::vector<llama_scalar> types;
+  std::vector<uint32_t> sizes;
+  std::vector<int64_t> extents;
+  llama_kind kind = LLAMA_AOS;
+  int64_t lanes = 1;
+  bool aligned = false;
+
+  uint64_t N = 0;            // product of extents
+  uint64_t record_bytes = 0; // S (packed or aligned record size)
+  std::vector<uint64_t> rec_off;  // leaf offsets inside one record
+
+  // normal form: off(i,k) = base_k + (i / L) * B + F_k + (i % L) * s_k
+  uint64_t L = 1, B = 0;
+  std::vector<uint64_t> base, F;
+  std::vector<uint32_t> blob;
+  std::vector<uint64_t> blob_sizes;
+  uint64_t E = 0;            // records covered by the blobs (blocked: nblocks*L; SoA: N)
+
+  int K() const { return (int)sizes.size(); }
+  int nblobs() const { return (int)blob_sizes.size(); }
+  bool soa() const { return kind == LLAMA_SOA_SINGLE_BLOB || kind == LLAMA_SOA_MULTI_BLOB; }
+  uint64_t payload_bytes() const;   // N * sum s_k
+  uint64_t footprint_bytes() const; // sum of blob sizes
+  bool has_padding() const { return footprint_bytes() != payload_bytes(); }
+  uint64_t offset(uint64_t i, int k) const { return base[k] + (i / L) * B + F[k] + (i % L) * sizes[k]; }
+  DevSide dev_side() const;
+  DevLeaf dev_leaf(int k) const;
+};
+
+// Builds the descriptor; returns LLAMA_OK or an error with *err set.
+llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string* err);
+
+}  // namespace llb

@@ -1,0 +1,133 @@
+// params.hpp -- kernel parameter blocks shared by the host planner (plan.cpp)
+// and the sm_100a kernels (*.cu).  Plain C++ (no CUDA types) so g++ and nvcc
+// both compile it.  Every kernel receives one of these by value as a
+// __grid_constant__ parameter (<= 32 KB kernel parameter space, CUDA >= 12.1).
+#pragma once
+#include <stdint.h>
+
+#include "llama_b200.h"
+
+namespace llb {
+
+constexpr int kMaxLeaves = LLAMA_MAX_LEAVES;
+constexpr int kMaxBlobs = LLAMA_MAX_BLOBS;
+constexpr int kMaxMoves = 512;
+constexpr uint32_t kNoShift = 0xFFFFFFFFu;
+
+// One side's mapping in the AoSoA normal form:
+//   off(i,k) = base_k + (i / L) * B + F_k + (i % L) * s_k   in blob blob_k
+// AoS: L=1, B=S; AoSoA: L=lanes, B=L*S, F_k=L*off_k; SoA: L>=N (one block), B=0.
+struct DevSide {
+  uint64_t L;       // lanes per block
+  uint64_t B;       // block stride in bytes
+  uint32_t lshift;  // log2(L) when L is a power of two, else kNoShift
+  uint32_t pad_;
+};
+
+struct DevLeaf {
+  uint64_t base;
+  uint64_t F;
+  uint32_t blob;
+  uint32_t size;
+};
+
+// ---------------------------------------------------------------- naive / gen
+struct NaiveParams {
+  uint64_t N;
+  int32_t K;
+  int32_t pad_;
+  DevSide s, d;
+  DevLeaf sl[kMaxLeaves];
+  DevLeaf dl[kMaxLeaves];
+  const uint8_t* sb[kMaxBlobs];
+  uint8_t* db[kMaxBlobs];
+};
+
+struct GenParams {
+  uint64_t N;
+  uint64_t seed;
+  int32_t K;
+  int32_t pad_;
+  DevSide d;
+  DevLeaf dl[kMaxLeaves];
+  uint8_t* db[kMaxBlobs];
+};
+
+// Fill every byte of nb blobs with one value (padding pre-fill).
+struct FillParams {
+  int32_t nb;
+  uint32_t value;  // byte replicated
+  uint64_t vstart[kMaxBlobs + 1];  // prefix of 16-byte vectors per blob
+  uint64_t bytes[kMaxBlobs];
+  uint8_t* ptr[kMaxBlobs];
+};
+
+// Identity copy of whole blobs ("trivial" copy).
+struct BlobCopyParams {
+  int32_t nb;
+  int32_t pad_;
+  uint64_t vstart[kMaxBlobs + 1];
+  uint64_t bytes[kMaxBlobs];
+  const uint8_t* src[kMaxBlobs];
+  uint8_t* dst[kMaxBlobs];
+};
+
+// ------------------------------------------------------------------ run copy
+// Field-run copy: per leaf, records come in runs of
+// g = gcd(L_s, L_d) that are contiguous on both sides; g*s_k % 16 == 0 and all
+// offsets are 16-byte aligned, so one 16-byte vector never straddles a run.
+struct RunParams {
+  uint64_t N;
+  int32_t K;
+  int32_t pad_;
+  DevSide s, d;
+  DevLeaf sl[kMaxLeaves];
+  DevLeaf dl[kMaxLeaves];
+  uint64_t vstart[kMaxLeaves + 1];  // prefix of ceil(N*s_k/16) vectors per leaf
+  const uint8_t* sb[kMaxBlobs];
+  uint8_t* db[kMaxBlobs];
+};
+
+// ------------------------------------------------------------ tile permute
+// A tile is T consecutive records.  Each side keeps one shared-memory image
+// per tile: an "AoS-like" side (L divides T) as the single contiguous byte
+// range of its T/L blocks; a "SoA-like" side (T divides L, or SoA) as one
+// segment of T*s_k bytes per leaf.  Inside the image, leaf k of tile record r
+// sits at  (r / Limg) * Bimg + imgF_k + (r % Limg) * s_k.
+struct PermSide {
+  DevSide g;          // global normal form (segment addresses)
+  uint64_t E;         // records the side's blobs cover (padded block extent / N)
+  uint32_t soa_like;  // 1: per-leaf segments
+  uint32_t Limg;      // image lanes (AoS-like: L; SoA-like: T)
+  uint32_t limg_shift;
+  uint32_t Bimg;      // image block stride
+  uint32_t img_bytes; // image bytes of a full tile
+  uint32_t pad_;
+};
+
+struct Move {        // one unit move of the per-record permutation
+  uint32_t soff;     // src image offset of leaf part for r = 0
+  uint32_t doff;     // dst image offset
+  uint16_t size;     // leaf size s_k (multiplies r % Limg)
+  uint8_t unit;      // bytes moved: 1, 2, 4 or 8
+  uint8_t pad_;
+};
+
+struct PermParams {
+  uint64_t N;         // records
+  uint64_t n_tiles;   // ceil(R / T), R = records the dst image must cover
+  uint32_t T;         // records per tile (multiple of 32)
+  uint32_t n_moves;
+  uint32_t K;
+  uint32_t tma;       // 1: segment starts 16-B aligned for every tile -> TMA bulk
+  uint32_t src_stage; // bytes of one src image buffer (16-B multiple)
+  uint32_t dst_stage; // bytes of one dst image buffer
+  uint32_t ns, nd;    // src stages, dst buffers
+  PermSide side[2];   // 0 = src, 1 = dst
+  DevLeaf leaf[2][kMaxLeaves];
+  uint32_t imgF[2][kMaxLeaves];
+  Move moves[kMaxMoves];
+  uint8_t* blobs[2][kMaxBlobs];
+};
+
+}  // namespace llb

@@ -1,0 +1,295 @@
+// plan.cpp -- chooses the kernel path for a mapping pair and precomputes its
+// parameter block.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace llb {
+
+namespace {
+
+constexpr uint64_t kAosLikeMaxBlock = 16384;  // larger AoSoA blocks are tiled inside a block
+constexpr uint64_t kTileTarget = 24 * 1024;   // src + dst image bytes per tile
+constexpr int kBarBytes = 128;
+constexpr int kSmemPerCtaBudget = 112 * 1024; // aim for >= 2 CTAs per SM
+
+uint64_t gcd64(uint64_t a, uint64_t b) {
+  while (b) { uint64_t t = a % b; a = b; b = t; }
+  return a;
+}
+uint64_t lcm64(uint64_t a, uint64_t b) { return a / gcd64(a, b) * b; }
+uint64_t lowbit(uint64_t x) { return x ? (x & (~x + 1)) : (1ull << 62); }
+uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+bool same_layout(const Mapping& s, const Mapping& d) {
+  if (s.L != d.L || s.B != d.B || s.blob_sizes != d.blob_sizes) return false;
+  for (int k = 0; k < s.K(); ++k)
+    if (s.base[k] != d.base[k] || s.F[k] != d.F[k] || s.blob[k] != d.blob[k]) return false;
+  return true;
+}
+
+DevSide side_of(const Mapping& m) {
+  DevSide ds = m.dev_side();
+  if (m.soa()) ds.lshift = 63;  // one block: i / L == 0 for every valid i
+  return ds;
+}
+
+}  // namespace
+
+llama_status check_compatible(const Mapping& s, const Mapping& d, std::string* err) {
+  if (s.types != d.types) {
+    *err = "record dimensions differ (leaf type lists are not identical)";
+    return LLAMA_ERR_RECORD_MISMATCH;
+  }
+  if (s.extents != d.extents) {
+    *err = "array extents differ";
+    return LLAMA_ERR_SHAPE_MISMATCH;
+  }
+  return LLAMA_OK;
+}
+
+FillParams make_fill(const Mapping& m, uint8_t value) {
+  FillParams f;
+  std::memset(&f, 0, sizeof(f));
+  f.nb = m.nblobs();
+  f.value = value;
+  f.vstart[0] = 0;
+  for (int b = 0; b < f.nb; ++b) {
+    f.bytes[b] = m.blob_sizes[b];
+    f.vstart[b + 1] = f.vstart[b] + ceil_div(m.blob_sizes[b], 16);
+  }
+  return f;
+}
+
+void plan_naive(const Mapping& s, const Mapping& d, Plan* p) {
+  p->path = LLAMA_PATH_NAIVE;
+  p->naive.reset(new NaiveParams);
+  NaiveParams& n = *p->naive;
+  std::memset(&n, 0, sizeof(n));
+  n.N = s.N;
+  n.K = s.K();
+  n.s = side_of(s);
+  n.d = side_of(d);
+  for (int k = 0; k < s.K(); ++k) {
+    n.sl[k] = s.dev_leaf(k);
+    n.dl[k] = d.dev_leaf(k);
+  }
+  p->naive_zero_fill = d.has_padding();  // padding := 0 (reading #12)
+  if (p->naive_zero_fill) p->fill.reset(new FillParams(make_fill(d, 0)));
+}
+
+bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
+  if (!same_layout(s, d)) { *why = "layouts differ"; return false; }
+  if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
+  p->path = LLAMA_PATH_BLOBCOPY;
+  p->blobcopy.reset(new BlobCopyParams);
+  BlobCopyParams& b = *p->blobcopy;
+  std::memset(&b, 0, sizeof(b));
+  b.nb = d.nblobs();
+  for (int j = 0; j < b.nb; ++j) {
+    b.bytes[j] = d.blob_sizes[j];
+    b.vstart[j + 1] = b.vstart[j] + ceil_div(d.blob_sizes[j], 16);
+  }
+  return true;
+}
+
+bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
+  if (d.has_padding()) { *why = "destination has padding"; return false; }
+  const Mapping* side[2] = {&s, &d};
+  for (int k = 0; k < s.K(); ++k) {
+    const uint64_t sz = s.sizes[k];
+    // records per common run ("min(N,M)"; gcd for lane counts that do
+    // not divide each other); a single block counts as L = N
+    const uint64_t n1 = std::max<uint64_t>(s.N, 1);
+    const uint64_t g = gcd64(std::min(s.L, n1), std::min(d.L, n1));
+    const bool single_run = g >= s.N;    // the whole leaf is one run on both sides
+    if (!single_run && (g * sz) % 16 != 0) { *why = "common runs shorter than 16 B"; return false; }
+    for (int X = 0; X < 2; ++X) {
+      const Mapping& m = *side[X];
+      if ((m.base[k] + m.F[k]) % 16 != 0 || (!single_run && (m.base[k] % 16 || m.F[k] % 16))) {
+        *why = "run starts not 16-B aligned";
+        return false;
+      }
+      if (!single_run && m.E > m.L && m.B % 16 != 0) { *why = "block stride not 16-B aligned"; return false; }
+    }
+  }
+  p->path = LLAMA_PATH_RUN;
+  p->run.reset(new RunParams);
+  RunParams& r = *p->run;
+  std::memset(&r, 0, sizeof(r));
+  r.N = s.N;
+  r.K = s.K();
+  r.s = side_of(s);
+  r.d = side_of(d);
+  r.vstart[0] = 0;
+  for (int k = 0; k < s.K(); ++k) {
+    r.sl[k] = s.dev_leaf(k);
+    r.dl[k] = d.dev_leaf(k);
+    r.vstart[k + 1] = r.vstart[k] + ceil_div(s.N * s.sizes[k], 16);
+  }
+  return true;
+}
+
+bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
+  const Mapping* side[2] = {&s, &d};
+  bool soa_like[2];
+  uint64_t Tmult = 32;
+  std::vector<uint64_t> Tdiv;
+  uint64_t rec_img[2];
+  for (int X = 0; X < 2; ++X) {
+    const Mapping& m = *side[X];
+    if (m.soa()) {
+      soa_like[X] = true;
+    } else if (m.B <= kAosLikeMaxBlock) {
+      soa_like[X] = false;
+      Tmult = lcm64(Tmult, m.L);
+    } else {
+      soa_like[X] = true;  // huge AoSoA blocks: a tile stays inside one block
+      Tdiv.push_back(m.L);
+    }
+    uint64_t sum = 0;
+    for (auto v : m.sizes) sum += v;
+    rec_img[X] = soa_like[X] ? sum : m.record_bytes;
+  }
+  if (Tmult > 8192) { *why = "lane counts need tiles above 8192 records"; return false; }
+  const uint64_t R = d.E;  // records the destination blobs cover
+  uint64_t T;
+  if (tile_records > 0) {
+    T = (uint64_t)tile_records;
+    if (T % Tmult) { *why = "tile_records must be a multiple of 32 and of every AoS-like lane count"; return false; }
+  } else {
+    const uint64_t per = rec_img[0] + rec_img[1];
+    uint64_t c = std::max<uint64_t>(1, kTileTarget / (per * Tmult));
+    const uint64_t cmax = std::max<uint64_t>(1, ceil_div(R, Tmult));
+    c = std::min(c, cmax);
+    T = 0;
+    for (; c >= 1; --c) {
+      bool ok = true;
+      for (auto L : Tdiv) ok = ok && (L % (c * Tmult) == 0);
+      if (ok) { T = c * Tmult; break; }
+    }
+    if (!T) { *why = "no tile size divides the AoSoA lane count"; return false; }
+  }
+  for (auto L : Tdiv)
+    if (L % T) { *why = "tile must divide the lane count of a large-block AoSoA side"; return false; }
+
+  p->perm.reset(new PermParams);
+  PermParams& pp = *p->perm;
+  std::memset(&pp, 0, sizeof(pp));
+  pp.N = s.N;
+  pp.T = (uint32_t)T;
+  pp.K = (uint32_t)s.K();
+  pp.n_tiles = ceil_div(R, T);
+  bool tma = true;
+  for (int X = 0; X < 2; ++X) {
+    const Mapping& m = *side[X];
+    PermSide& ps = pp.side[X];
+    ps.g = side_of(m);
+    ps.E = m.E;
+    ps.soa_like = soa_like[X] ? 1 : 0;
+    for (int k = 0; k < m.K(); ++k) pp.leaf[X][k] = m.dev_leaf(k);
+    uint64_t img;
+    if (!soa_like[X]) {
+      ps.Limg = (uint32_t)m.L;
+      ps.limg_shift = (m.L & (m.L - 1)) == 0 ? (uint32_t)__builtin_ctzll(m.L) : kNoShift;
+      ps.Bimg = (uint32_t)m.B;
+      img = T / m.L * m.B;
+      for (int k = 0; k < m.K(); ++k) pp.imgF[X][k] = (uint32_t)m.F[k];
+      if (m.base[0] % 16 || img % 16) tma = false;
+    } else {
+      ps.Limg = (uint32_t)T;
+      ps.limg_shift = 31;  // r < T: one image block
+      ps.Bimg = 0;
+      uint64_t off = 0;
+      for (int k = 0; k < m.K(); ++k) {
+        off = align16(off);
+        pp.imgF[X][k] = (uint32_t)off;
+        off += T * m.sizes[k];
+        if (m.base[k] % 16) tma = false;
+        if (!m.soa() && (m.F[k] % 16 || m.B % 16)) tma = false;
+      }
+      img = align16(off);
+    }
+    ps.img_bytes = (uint32_t)img;
+  }
+  pp.tma = tma ? 1 : 0;
+  pp.src_stage = (uint32_t)align16(pp.side[0].img_bytes);
+  pp.dst_stage = (uint32_t)align16(pp.side[1].img_bytes);
+  pp.nd = 2;
+  uint64_t smem = 0;
+  for (uint32_t ns = 4; ns >= 2; --ns) {
+    smem = kBarBytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
+    pp.ns = ns;
+    if (smem <= (uint64_t)kSmemPerCtaBudget) break;
+  }
+  if (smem > 227 * 1024) { *why = "tile images exceed shared memory"; return false; }
+
+  // per-record move table: leaf k moves in units of the widest power of two
+  // that divides its size and both image offsets for every record
+  uint32_t nm = 0;
+  for (int k = 0; k < s.K(); ++k) {
+    uint64_t unit = std::min<uint64_t>(8, s.sizes[k]);
+    for (int X = 0; X < 2; ++X) {
+      const PermSide& ps = pp.side[X];
+      uint64_t a = std::min<uint64_t>(16, lowbit(pp.imgF[X][k]));
+      if (ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(s.sizes[k]));
+      if (T / ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(ps.Bimg));
+      unit = std::min(unit, a);
+    }
+    for (uint64_t j = 0; j < s.sizes[k] / unit; ++j) {
+      if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
+      Move& mv = pp.moves[nm++];
+      mv.soff = (uint32_t)(pp.imgF[0][k] + j * unit);
+      mv.doff = (uint32_t)(pp.imgF[1][k] + j * unit);
+      mv.size = (uint16_t)s.sizes[k];
+      mv.unit = (uint8_t)unit;
+    }
+  }
+  pp.n_moves = nm;
+  p->path = LLAMA_PATH_PERMUTE;
+  p->smem_bytes = (int)smem;
+  return true;
+}
+
+llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int tile_records, Plan* out,
+                       std::string* err) {
+  llama_status st = check_compatible(s, d, err);
+  if (st != LLAMA_OK) return st;
+  out->src_bytes = s.footprint_bytes();
+  out->dst_bytes = d.footprint_bytes();
+  if (out->dst_bytes == 0) {
+    out->empty = true;
+    out->path = path == LLAMA_PATH_AUTO ? LLAMA_PATH_BLOBCOPY : path;
+    return LLAMA_OK;
+  }
+  std::string why;
+  switch (path) {
+    case LLAMA_PATH_AUTO:
+      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      if (plan_run(s, d, out, &why)) return LLAMA_OK;
+      if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
+      plan_naive(s, d, out);
+      return LLAMA_OK;
+    case LLAMA_PATH_NAIVE:
+      plan_naive(s, d, out);
+      return LLAMA_OK;
+    case LLAMA_PATH_BLOBCOPY:
+      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      break;
+    case LLAMA_PATH_RUN:
+      if (plan_run(s, d, out, &why)) return LLAMA_OK;
+      break;
+    case LLAMA_PATH_PERMUTE:
+      if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
+      break;
+    default:
+      *err = "bad path";
+      return LLAMA_ERR_INVALID_ARGUMENT;
+  }
+  *err = "path not applicable to this mapping pair: " + why;
+  return LLAMA_ERR_UNSUPPORTED;
+}
+
+}  // namespace llb

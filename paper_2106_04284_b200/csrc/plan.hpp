@@ -1,0 +1,43 @@
+// plan.hpp -- the copy planner (specialised copies for related
+// mappings, "run time analysis of the two views to find contiguous memory
+// chunks").  A plan is computed once per (src mapping, dst mapping, options)
+// and cached; per call only the blob pointers are patched in.
+#pragma once
+#include <memory>
+#include <string>
+
+#include "mapping.hpp"
+#include "params.hpp"
+
+namespace llb {
+
+struct Plan {
+  llama_path path = LLAMA_PATH_NAIVE;
+  bool empty = false;         // nothing to do (no destination bytes)
+  bool naive_zero_fill = false;
+  int smem_bytes = 0;
+  uint64_t src_bytes = 0, dst_bytes = 0;
+  std::unique_ptr<NaiveParams> naive;
+  std::unique_ptr<FillParams> fill;
+  std::unique_ptr<BlobCopyParams> blobcopy;
+  std::unique_ptr<RunParams> run;
+  std::unique_ptr<PermParams> perm;
+};
+
+// Checks S:484-486 (same leaf types, same extents).
+llama_status check_compatible(const Mapping& s, const Mapping& d, std::string* err);
+
+// Builds a plan for `path` (LLAMA_PATH_AUTO = the planner's choice).
+// UNSUPPORTED if a forced path does not apply to the pair.
+llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int tile_records, Plan* out,
+                       std::string* err);
+
+// Path-specific builders; return false (with *why) when not applicable.
+bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
+bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
+bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why);
+void plan_naive(const Mapping& s, const Mapping& d, Plan* p);
+
+FillParams make_fill(const Mapping& m, uint8_t value);
+
+}  // namespace llb

@@ -1,0 +1,162 @@
+"""CPU-side tests of the C-ABI library: it loads, exports every symbol the
+header declares, and its host-side descriptor (the AoSoA normal form,
+mapping.cpp) agrees with the oracle's independent per-kind formulas
+(oracle.c) exhaustively on small extents (SURVEY P11 brute force).  Validation
+errors are raised before any device work, so no GPU is needed here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+from conftest import ROOT
+
+llama = pytest.importorskip("paper_2106_04284_b200")
+
+
+def test_exports_every_declared_symbol():
+    with open(os.path.join(ROOT, "include", "llama_b200.h")) as f:
+        text = f.read()
+    declared = set(re.findall(r"\b(llama_[a-z_]+)\s*\(", text))
+    assert declared == set(llama.EXPORTS)
+    lib = llama.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert "sm_100a" in llama.version()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", llama.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+KINDS = [("aos", 1, False), ("aos", 1, True), ("soa_sb", 1, False), ("soa_sb", 1, True), ("soa_mb", 1, False),
+         ("aosoa", 1, False), ("aosoa", 2, False), ("aosoa", 3, False), ("aosoa", 4, False), ("aosoa", 8, True),
+         ("aosoa", 32, False)]
+
+
+@pytest.mark.parametrize("schema", [W.LISTING1, W.PARTICLE7, W.OUTER, W.HEP100, W.VEC])
+@pytest.mark.parametrize("ext", [[1], [5], [33], [4, 3], [2, 3, 5]])
+def test_descriptor_matches_oracle(oracle_mod, schema, ext):
+    n = int(np.prod(ext))
+    for kind, L, aligned in KINDS + [("aosoa", n, False)]:
+        m = llama.Mapping(schema, ext, kind, L, aligned)
+        o = oracle_mod.Mapping(schema, ext, kind, L, aligned)
+        assert m.blob_sizes() == o.blob_sizes()
+        assert m.record_count == o.record_count == n
+        assert m.leaf_count == o.n_leaves
+        for flat in range(n):
+            idx = list(np.unravel_index(flat, ext))
+            for k in range(o.n_leaves):
+                assert m.blob_nr_and_offset([int(x) for x in idx], k) == o.addr(flat, k)
+
+
+def test_big_extents_blob_sizes(oracle_mod):
+    for cfg in W.CONFIGS.values():
+        schema = W.SCHEMAS[cfg["schema"]]
+        for a, b in cfg["pairs"]:
+            for name in (a, b):
+                kind, L, al = W.MAPPINGS[name]
+                m = llama.Mapping(schema, cfg["extents"], kind, L, al)
+                o = oracle_mod.Mapping(schema, cfg["extents"], kind, L, al)
+                assert m.blob_sizes() == o.blob_sizes()
+
+
+def test_schema_parser_matches_oracle(oracle_mod):
+    for schema in [W.LISTING1, W.HEP100, W.OUTER, "R{a:f32[2][3],b{c:bool[2],d:u16}}", "f64"]:
+        m = llama.Mapping(schema, [3], "aos")
+        sizes = [{0: 1, 1: 1, 2: 1, 3: 2, 4: 2, 5: 4, 6: 4, 7: 8, 8: 8, 9: 4, 10: 8}[t] for t in m.leaf_types()]
+        assert sizes == oracle_mod.leaf_sizes(schema)
+    for bad in ["R{a:f16}", "R{a:f32,a:f32}", "R{a:f32[0]}", "R{", "R{a:f32}}"]:
+        with pytest.raises(llama.LlamaError) as e:
+            llama.Mapping(bad, [3], "aos")
+        assert e.value.status == -1
+
+
+def test_mapping_errors():
+    with pytest.raises(llama.LlamaError) as e:
+        llama.Mapping(W.VEC, [-1], "aos")
+    assert e.value.status == -1
+    with pytest.raises(llama.LlamaError) as e:
+        llama.Mapping(W.VEC, [4], "aosoa", lanes=0)
+    assert e.value.status == -1
+    big = "R{" + ",".join(f"f{j}:u8" for j in range(200)) + "}"
+    with pytest.raises(llama.LlamaError) as e:
+        llama.Mapping(big, [4], "aos")
+    assert e.value.status == -4
+    m = llama.Mapping(W.VEC, [4, 3], "aos")
+    with pytest.raises(llama.LlamaError):
+        m.blob_nr_and_offset([4, 0], 0)
+    with pytest.raises(llama.LlamaError):
+        m.blob_nr_and_offset([0, 0], 2)
+
+
+def _copy_raw(src, sp, dst, dp):
+    lib = llama.lib()
+    a = (ctypes.c_void_p * max(1, len(sp)))(*sp)
+    b = (ctypes.c_void_p * max(1, len(dp)))(*dp)
+    rc = lib.llama_copy(src.handle, a, dst.handle, b, None)
+    return rc, lib.llama_last_error_message().decode()
+
+
+def test_copy_validation_errors_are_synchronous():
+    """S:484-486 and the ABI's validation rules; all rejected before launch."""
+    a = llama.Mapping(W.LISTING1, [64], "aos")
+    b = llama.Mapping(W.LISTING1, [64], "soa_mb")
+    rc, _ = _copy_raw(a, [0x10000], llama.Mapping(W.LISTING1, [65], "aos"), [0x90000])
+    assert rc == -2
+    rc, _ = _copy_raw(a, [0x10000], llama.Mapping(W.VEC, [64], "aos"), [0x90000])
+    assert rc == -3
+    rc, msg = _copy_raw(a, [0x10008], b, [0x100000 + 0x1000 * j for j in range(7)])
+    assert rc == -5 and "src_blobs[0]" in msg
+    rc, _ = _copy_raw(a, [0x10000], b, [0x100000 + 0x1000 * j for j in range(6)] + [0])
+    assert rc == -1
+    # overlapping src/dst (in-situ copies are out of scope)
+    rc, _ = _copy_raw(a, [0x10000], b, [0x10000 + 0x100] + [0x100000 + 0x1000 * j for j in range(6)])
+    assert rc == -6
+    # overlapping destination blobs
+    rc, _ = _copy_raw(a, [0x10000], b, [0x100000] * 7)
+    assert rc == -6
+    lib = llama.lib()
+    assert lib.llama_copy(None, None, None, None, None) == -1
+    assert lib.llama_status_string(-6) == b"LLAMA_ERR_OVERLAP"
+
+
+def _plan(src_name, dst_name, schema=W.PARTICLE7, ext=(16_777_216,)):
+    s = llama.Mapping(schema, ext, *W.MAPPINGS[src_name])
+    d = llama.Mapping(schema, ext, *W.MAPPINGS[dst_name])
+    return llama.plan(s, d)
+
+
+def test_planner_choices_c2():
+    """Identity -> blob copy; shared >=16 B runs -> run copy
+    (P:759-761); AoS <-> anything -> staged permute."""
+    assert _plan("aos", "aos")["path"] == "blobcopy"
+    assert _plan("soa_mb", "soa_mb")["path"] == "blobcopy"
+    assert _plan("aosoa8", "aosoa32")["path"] == "run"
+    assert _plan("soa_mb", "aosoa8")["path"] == "run"
+    assert _plan("aosoa32", "soa_mb")["path"] == "run"
+    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos")]:
+        p = _plan(a, b)
+        assert p["path"] == "permute" and p["tma"] and p["tile_records"] % 32 == 0
+    assert _plan("aosoa32", "soa_sb", W.LISTING1, (8192, 8192))["path"] == "run"  # C4
+    for a, b in W.C3["pairs"]:
+        p = _plan(a, b, W.HEP100, (67_108_864,))
+        assert p["path"] == "permute", (a, b, p)
+    assert _plan("aos", "soa_mb", ext=(4096,))["path"] == "permute"  # C1
+
+
+def test_planner_forced_paths():
+    s = llama.Mapping(W.PARTICLE7, [1000], "aos")
+    d = llama.Mapping(W.PARTICLE7, [1000], "soa_mb")
+    assert llama.plan(s, d, path="naive")["path"] == "naive"
+    with pytest.raises(llama.LlamaError) as e:
+        llama.plan(s, d, path="run")
+    assert e.value.status == -4
+    with pytest.raises(llama.LlamaError):
+        llama.plan(s, d, path="permute", tile_records=48)
+    assert llama.plan(s, d, path="permute", tile_records=64)["tile_records"] == 64

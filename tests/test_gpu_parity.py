@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, byte
+for byte (the copy is integer/byte work: bit-exact is the bar).
+
+Each case generates the source on the GPU (llama_generate) and on the CPU
+(oracle.generate), checks the two sources are identical, copies on
+the GPU into destination blobs pre-filled with garbage (so an unwritten byte
+cannot pass), and compares every byte of every destination blob with the
+oracle's copy.  Source padding is poisoned with 0xCD (reading #13)."""
+import random
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def llama():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_04284_b200 as m
+    return m
+
+
+KINDS = {
+    "aos": ("aos", 1, False), "aos_aligned": ("aos", 1, True), "soa_sb": ("soa_sb", 1, False),
+    "soa_sb_aligned": ("soa_sb", 1, True), "soa_mb": ("soa_mb", 1, False), "aosoa4": ("aosoa", 4, False),
+    "aosoa8": ("aosoa", 8, False), "aosoa32": ("aosoa", 32, False), "aosoa3": ("aosoa", 3, False),
+    "aosoa8_aligned": ("aosoa", 8, True), "aosoa64": ("aosoa", 64, False),
+}
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def run_case(llama, oracle, schema, ext, sk, dk, seed=42, paths=("auto",), pad=0xCD, check_src=True):
+    sm = llama.Mapping(schema, ext, *sk)
+    dm = llama.Mapping(schema, ext, *dk)
+    so = oracle.Mapping(schema, ext, *sk)
+    do = oracle.Mapping(schema, ext, *dk)
+    sb = sm.alloc("cuda")
+    llama.generate(sm, sb, seed, pad_byte=pad)
+    src_host = oracle.make_view(so, seed, pad_fill=pad)
+    if check_src:
+        for j, t in enumerate(sb):
+            assert np.array_equal(_host(t), src_host[j]), f"generated source differs in blob {j}"
+    exp = oracle.copy(so, src_host, do)
+    for path in paths:
+        if path != "auto":
+            try:
+                llama.plan(sm, dm, path=path)
+            except llama.LlamaError:
+                continue  # path not applicable to this pair
+        db = dm.alloc("cuda")
+        for t in db:
+            t.fill_(0x5A)
+        llama.copy(sm, sb, dm, db, path=path)
+        torch.cuda.synchronize()
+        for j, t in enumerate(db):
+            got = _host(t)
+            if not np.array_equal(got, exp[j]):
+                bad = np.nonzero(got != exp[j])[0]
+                raise AssertionError(f"{sk}->{dk} ext={ext} path={path} plan={llama.plan(sm, dm, path=path)}: "
+                                     f"blob {j}: {bad.size} bytes differ, first at {bad[:8]}")
+
+
+ALL_PATHS = ("auto", "naive", "permute", "run", "blobcopy")
+
+
+@pytest.mark.parametrize("n", [1, 7, 31, 32, 33, 100, 4095, 4097, 65537])
+@pytest.mark.parametrize("schema_name", ["particle7", "listing1"])
+def test_all_pairs_small(llama, oracle_mod, schema_name, n):
+    schema = W.SCHEMAS[schema_name]
+    for a in KINDS:
+        for b in KINDS:
+            run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b], seed=42 + n, paths=ALL_PATHS)
+
+
+@pytest.mark.parametrize("n", [1, 33, 1000, 4097])
+def test_all_pairs_hep100(llama, oracle_mod, n):
+    kinds = ["aos", "aos_aligned", "soa_mb", "soa_sb", "aosoa8", "aosoa32", "aosoa3"]
+    for a in kinds:
+        for b in kinds:
+            run_case(llama, oracle_mod, W.HEP100, [n], KINDS[a], KINDS[b], seed=1, paths=ALL_PATHS)
+
+
+@pytest.mark.parametrize("ext", [[4, 3], [64, 33], [7, 5, 9], [128, 256]])
+def test_multidim_extents(llama, oracle_mod, ext):
+    for schema in (W.LISTING1, W.VEC, W.OUTER):
+        for a, b in [("aos", "soa_mb"), ("aosoa32", "soa_sb"), ("soa_sb", "aos_aligned"), ("aosoa8", "aosoa4")]:
+            run_case(llama, oracle_mod, schema, ext, KINDS[a], KINDS[b], seed=2, paths=ALL_PATHS)
+
+
+def _random_schema(rng):
+    types = ["i8", "u8", "bool", "i16", "u16", "i32", "u32", "f32", "i64", "u64", "f64"]
+    fields = []
+    for j in range(rng.randint(1, 24)):
+        t = rng.choice(types)
+        if rng.random() < 0.15:
+            t += f"[{rng.randint(1, 4)}]"
+        fields.append(f"f{j}:{t}")
+    if rng.random() < 0.3:
+        fields.append("n{" + ",".join(f"g{j}:{rng.choice(types)}" for j in range(rng.randint(1, 4))) + "}")
+    return "R{" + ",".join(fields) + "}"
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_schema_fuzz(llama, oracle_mod, seed):
+    rng = random.Random(seed)
+    schema = _random_schema(rng)
+    n = rng.choice([1, 5, 17, 64, 333, 1024, 5000])
+    names = list(KINDS)
+    for _ in range(12):
+        a, b = rng.choice(names), rng.choice(names)
+        run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b], seed=seed, paths=ALL_PATHS)
+
+
+def test_tile_sizes_and_empty(llama, oracle_mod):
+    for t in (32, 64, 96, 256, 1024):
+        for a, b in [("aos", "soa_mb"), ("aos_aligned", "aos"), ("soa_sb", "aosoa32")]:
+            sm = llama.Mapping(W.LISTING1, [3000], *KINDS[a])
+            dm = llama.Mapping(W.LISTING1, [3000], *KINDS[b])
+            try:
+                llama.plan(sm, dm, path="permute", tile_records=t)
+            except llama.LlamaError:
+                continue
+            so = oracle_mod.Mapping(W.LISTING1, [3000], *KINDS[a])
+            do = oracle_mod.Mapping(W.LISTING1, [3000], *KINDS[b])
+            sb = sm.alloc()
+            llama.generate(sm, sb, 3, pad_byte=0xCD)
+            db = dm.alloc()
+            for x in db:
+                x.fill_(0x5A)
+            llama.copy(sm, sb, dm, db, path="permute", tile_records=t)
+            exp = oracle_mod.copy(so, oracle_mod.make_view(so, 3, 0xCD), do)
+            for j, x in enumerate(db):
+                assert np.array_equal(_host(x), exp[j]), (t, a, b)
+    e = llama.Mapping(W.LISTING1, [0], "aos")
+    llama.copy(e, e.alloc(), llama.Mapping(W.LISTING1, [0], "soa_mb"),
+               llama.Mapping(W.LISTING1, [0], "soa_mb").alloc())
+
+
+def test_streams_and_launch_count(llama, oracle_mod):
+    sm = llama.Mapping(W.PARTICLE7, [100000], "aos")
+    dm = llama.Mapping(W.PARTICLE7, [100000], "soa_mb")
+    sb, db = sm.alloc(), dm.alloc()
+    s = torch.cuda.Stream()
+    before = llama.launch_count()
+    with torch.cuda.stream(s):
+        llama.generate(sm, sb, 42)
+        llama.copy(sm, sb, dm, db)
+    s.synchronize()
+    assert llama.launch_count() - before >= 2
+    exp = oracle_mod.copy(oracle_mod.Mapping(W.PARTICLE7, [100000], "aos"),
+                          oracle_mod.make_view(oracle_mod.Mapping(W.PARTICLE7, [100000], "aos"), 42),
+                          oracle_mod.Mapping(W.PARTICLE7, [100000], "soa_mb"))
+    for j, x in enumerate(db):
+        assert np.array_equal(_host(x), exp[j])
+
+
+# ------------------------------------------------------- full BASELINE sizes
+def test_c1_parity(llama, oracle_mod):
+    cfg = W.C1
+    for a, b in cfg["pairs"]:
+        run_case(llama, oracle_mod, W.SCHEMAS[cfg["schema"]], list(cfg["extents"]), W.MAPPINGS[a],
+                 W.MAPPINGS[b], seed=42, paths=("auto", "naive"))
+
+
+def test_c2_full_size_all_pairs(llama, oracle_mod):
+    """C2 at its full size (16M particles), all 16 ordered pairs, in the
+    launch configuration bench.py times (AUTO plan), every byte compared."""
+    cfg = W.C2
+    schema, ext = W.SCHEMAS[cfg["schema"]], list(cfg["extents"])
+    views = {}
+    for name in ("aos", "soa_mb", "aosoa8", "aosoa32"):
+        om = oracle_mod.Mapping(schema, ext, *W.MAPPINGS[name])
+        views[name] = oracle_mod.make_view(om, 42)
+    for a, b in cfg["pairs"]:
+        sm = llama.Mapping(schema, ext, *W.MAPPINGS[a])
+        dm = llama.Mapping(schema, ext, *W.MAPPINGS[b])
+        sb = sm.alloc()
+        llama.generate(sm, sb, 42)
+        db = dm.alloc()
+        for x in db:
+            x.fill_(0x5A)
+        llama.copy(sm, sb, dm, db)
+        torch.cuda.synchronize()
+        for j, x in enumerate(db):
+            assert np.array_equal(_host(x), views[b][j]), (a, b, j)
+        del sb, db
+
+
+def _window(m, om, a, b):
+    """Byte window [lo, hi) per blob that records [a,b) occupy (AoS and SoA MB:
+    exactly the records' bytes)."""
+    lo = [None] * m.blob_count
+    hi = [0] * m.blob_count
+    for k in range(m.leaf_count):
+        for i in (a, b - 1):
+            blob, off = m.blob_nr_and_offset(i, k)
+            lo[blob] = off if lo[blob] is None else min(lo[blob], off)
+            hi[blob] = max(hi[blob], off + om.sizes[k])
+    return [x or 0 for x in lo], hi
+
+
+def test_c3_full_size_sampled(llama, oracle_mod):
+    """C3 (HEP100, 64M records, 25-32 GB per side) in bench.py's launch
+    configuration; sampled slabs compared with the oracle's windowed copy."""
+    cfg = W.C3
+    schema, ext = W.SCHEMAS[cfg["schema"]], list(cfg["extents"])
+    n = ext[0]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 64e9:
+        pytest.skip("needs ~58 GB of device memory")
+    slabs = [(0, 4096), (n // 2 - 1000, n // 2 + 3096), (n - 4096, n)]
+    for a, b in cfg["pairs"]:
+        sm = llama.Mapping(schema, ext, *W.MAPPINGS[a])
+        dm = llama.Mapping(schema, ext, *W.MAPPINGS[b])
+        so = oracle_mod.Mapping(schema, ext, *W.MAPPINGS[a])
+        do = oracle_mod.Mapping(schema, ext, *W.MAPPINGS[b])
+        sb = sm.alloc()
+        llama.generate(sm, sb, 42, pad_byte=0xCD)
+        db = dm.alloc()
+        llama.copy(sm, sb, dm, db)
+        torch.cuda.synchronize()
+        for (r0, r1) in slabs:
+            slo, shi = _window(sm, so, r0, r1)
+            dlo, dhi = _window(dm, do, r0, r1)
+            swin = [_host(sb[j][slo[j]:shi[j]]).copy() for j in range(sm.blob_count)]
+            # the GPU source agrees with the oracle's generator on this slab
+            ref_src = [np.full(shi[j] - slo[j], 0xCD, np.uint8) for j in range(sm.blob_count)]
+            oracle_mod.generate(so, ref_src, 42, r0, r1, base=slo)
+            for j in range(sm.blob_count):
+                assert np.array_equal(swin[j], ref_src[j])
+            exp = [np.zeros(dhi[j] - dlo[j], np.uint8) for j in range(dm.blob_count)]
+            oracle_mod.copy_range(so, swin, slo, do, exp, dlo, r0, r1)
+            for j in range(dm.blob_count):
+                assert np.array_equal(_host(db[j][dlo[j]:dhi[j]]), exp[j]), (a, b, r0, j)
+        del sb, db
+        torch.cuda.empty_cache()
+
+
+def test_c4_full_size(llama, oracle_mod):
+    """C4: Listing-1 record, 8192 x 8192, AoSoA32 -> SoA SB, whole blob compared."""
+    cfg = W.C4
+    for a, b in cfg["pairs"]:
+        run_case(llama, oracle_mod, W.SCHEMAS[cfg["schema"]], list(cfg["extents"]), W.MAPPINGS[a],
+                 W.MAPPINGS[b], seed=42, paths=("auto",))
