@@ -110,12 +110,17 @@ __device__ __forceinline__ uint32_t tile_nrec(const PermParams& p, uint64_t t0) 
   return n < p.T ? (uint32_t)n : p.T;
 }
 
-// Issues the TMA loads of a tile's source segments into one stage (warp 0).
-__device__ __forceinline__ void issue_loads(const PermParams& p, uint64_t t0, uint8_t* img, uint64_t* bar,
-                                            int lane) {
+// Issues the TMA loads of a tile's source segments into one stage (warp 0):
+// lane 0 arms the stage's mbarrier with the byte count, the lanes issue one
+// cp.async.bulk per segment.
+__device__ __forceinline__ void issue_loads(const PermParams& p, uint64_t t0, bool full, uint8_t* img,
+                                            uint64_t* bar, int lane) {
   const int ns = n_segs(p, 0);
-  uint32_t total = 0;
-  for (int j = 0; j < ns; ++j) total += tile_seg(p, 0, t0, j).len & ~15u;
+  uint32_t total = p.src_tile_tma;
+  if (!full) {
+    total = 0;
+    for (int j = 0; j < ns; ++j) total += tile_seg(p, 0, t0, j).len & ~15u;
+  }
   if (lane == 0) mbar_arrive_expect_tx(bar, total);
   __syncwarp();
   for (int j = lane; j < ns; j += 32) {
@@ -144,11 +149,17 @@ __global__ void __launch_bounds__(kThreads) k_permute(const __grid_constant__ Pe
   }
   __syncthreads();
 
+  if (blockIdx.x == 0)
+    for (uint32_t g = 0; g < p.n_gaps; ++g)
+      for (uint32_t o = tid; o < p.gap_len[g]; o += kThreads) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
+
   const uint64_t first = blockIdx.x, stride = gridDim.x;
+  const uint64_t n_full = p.N / p.T;  // tiles [0, n_full) are full: no tails, no clipping
   if (kTma && warp == 0) {
     for (uint32_t s = 0; s < p.ns; ++s) {
       const uint64_t tile = first + s * stride;
-      if (tile < p.n_tiles) issue_loads(p, tile * p.T, sbuf + (size_t)s * p.src_stage, &bars[s], lane);
+      if (tile < p.n_tiles)
+        issue_loads(p, tile * p.T, tile < n_full, sbuf + (size_t)s * p.src_stage, &bars[s], lane);
     }
   }
 
@@ -158,17 +169,22 @@ __global__ void __launch_bounds__(kThreads) k_permute(const __grid_constant__ Pe
     uint8_t* simg = sbuf + (size_t)s * p.src_stage;
     uint8_t* dimg = dbuf + (size_t)d * p.dst_stage;
     const uint64_t t0 = tile * p.T;
-    const uint32_t nrec = tile_nrec(p, t0);
+    const bool full = tile < n_full;
+    const uint32_t nrec = full ? p.T : tile_nrec(p, t0);
 
     if (kTma) {
-      mbar_wait(&bars[s], (it / p.ns) & 1);
-      // sub-16-byte tails of segments (only in a partial last tile)
-      for (int j = 0; j < n_segs(p, 0); ++j) {
-        const Seg sg = tile_seg(p, 0, t0, j);
-        const uint32_t body = sg.len & ~15u;
-        for (uint32_t o = body + tid; o < sg.len; o += kThreads) simg[sg.soff + o] = sg.g[o];
+      if (warp == 0) {  // one warp waits; the others sleep in the barrier below
+        if (lane == 0) mbar_wait(&bars[s], (it / p.ns) & 1);
+        if (it >= 2) bulk_wait_read<1>();  // dst buffer d (tile it-2) has been read out
+        __syncwarp();
       }
-      if (warp == 0 && it >= 2) bulk_wait_read<1>();  // dst buffer d (tile it-2) drained
+      if (!full) {  // sub-16-byte tails of the last tile's segments
+        __syncthreads();
+        for (int j = 0; j < n_segs(p, 0); ++j) {
+          const Seg sg = tile_seg(p, 0, t0, j);
+          for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += kThreads) simg[sg.soff + o] = sg.g[o];
+        }
+      }
     } else {
       __syncthreads();
       for (int j = 0; j < n_segs(p, 0); ++j) {
@@ -178,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) k_permute(const __grid_constant__ Pe
     }
     __syncthreads();
 
-    if (nrec < p.T) {  // partial tile: records beyond N are padding in the dst image
+    if (!full) {  // records beyond N are padding in the dst image
       for (uint32_t o = 16 * tid; o < p.dst_stage; o += 16 * kThreads)
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       __syncthreads();
@@ -187,26 +203,27 @@ __global__ void __launch_bounds__(kThreads) k_permute(const __grid_constant__ Pe
     if (kTma) fence_proxy_async_smem();
     __syncthreads();
 
-    const int nd = n_segs(p, 1);
+    const int nds = n_segs(p, 1);
     if (kTma) {
       if (warp == 0) {
-        for (int j = lane; j < nd; j += 32) {
+        for (int j = lane; j < nds; j += 32) {
           const Seg sg = tile_seg(p, 1, t0, j);
           const uint32_t body = sg.len & ~15u;
           if (body) bulk_s2g(sg.g, dimg + sg.soff, body);
         }
         bulk_commit();
-        // the ring slot s is free again (all threads passed the barrier): prefetch
+        // ring slot s is free again (every thread passed the barrier): prefetch
         const uint64_t next = tile + (uint64_t)p.ns * stride;
-        if (next < p.n_tiles) issue_loads(p, next * p.T, simg, &bars[s], lane);
+        if (next < p.n_tiles) issue_loads(p, next * p.T, next < n_full, simg, &bars[s], lane);
       }
-      for (int j = 0; j < nd; ++j) {
-        const Seg sg = tile_seg(p, 1, t0, j);
-        const uint32_t body = sg.len & ~15u;
-        for (uint32_t o = body + tid; o < sg.len; o += kThreads) sg.g[o] = dimg[sg.soff + o];
+      if (!full) {
+        for (int j = 0; j < nds; ++j) {
+          const Seg sg = tile_seg(p, 1, t0, j);
+          for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += kThreads) sg.g[o] = dimg[sg.soff + o];
+        }
       }
     } else {
-      for (int j = 0; j < nd; ++j) {
+      for (int j = 0; j < nds; ++j) {
         const Seg sg = tile_seg(p, 1, t0, j);
         coop_copy(sg.g, dimg + sg.soff, sg.len, tid, kThreads);
       }

@@ -78,12 +78,14 @@ struct BlobCopyParams {
 // offsets are 16-byte aligned, so one 16-byte vector never straddles a run.
 struct RunParams {
   uint64_t N;
+  uint64_t C;        // records per chunk: a CTA moves every leaf of a chunk together
+  uint64_t n_chunks;
+  uint32_t chunk_vecs;  // 16-byte vectors in a full chunk (sum over leaves)
   int32_t K;
-  int32_t pad_;
   DevSide s, d;
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
-  uint64_t vstart[kMaxLeaves + 1];  // prefix of ceil(N*s_k/16) vectors per leaf
+  uint32_t cvstart[kMaxLeaves + 1];  // prefix of C*s_k/16 vectors per leaf in a chunk
   const uint8_t* sb[kMaxBlobs];
   uint8_t* db[kMaxBlobs];
 };
@@ -123,10 +125,18 @@ struct PermParams {
   uint32_t src_stage; // bytes of one src image buffer (16-B multiple)
   uint32_t dst_stage; // bytes of one dst image buffer
   uint32_t ns, nd;    // src stages, dst buffers
+  uint32_t src_tile_tma;  // TMA bytes of a full tile's source segments
+  uint32_t pad_;
   PermSide side[2];   // 0 = src, 1 = dst
   DevLeaf leaf[2][kMaxLeaves];
   uint32_t imgF[2][kMaxLeaves];
   Move moves[kMaxMoves];
+  // destination padding outside every tile segment (gaps between the leaf
+  // sub-arrays of an aligned SoA single blob): zeroed by CTA 0
+  uint32_t n_gaps;
+  uint32_t gap_blob[kMaxLeaves];
+  uint32_t gap_len[kMaxLeaves];
+  uint64_t gap_off[kMaxLeaves];
   uint8_t* blobs[2][kMaxBlobs];
 };
 

@@ -123,12 +123,20 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
   r.K = s.K();
   r.s = side_of(s);
   r.d = side_of(d);
-  r.vstart[0] = 0;
+  // chunk = C records, a multiple of 16 (every leaf's chunk part is whole
+  // 16-byte vectors) sized to ~32 KB of source bytes
+  uint64_t S = 0;
+  for (int k = 0; k < s.K(); ++k) S += s.sizes[k];
+  uint64_t C = std::max<uint64_t>(16, (32768 / S) / 16 * 16);
+  r.C = C;
+  r.n_chunks = ceil_div(s.N, C);
+  r.cvstart[0] = 0;
   for (int k = 0; k < s.K(); ++k) {
     r.sl[k] = s.dev_leaf(k);
     r.dl[k] = d.dev_leaf(k);
-    r.vstart[k + 1] = r.vstart[k] + ceil_div(s.N * s.sizes[k], 16);
+    r.cvstart[k + 1] = r.cvstart[k] + (uint32_t)(C * s.sizes[k] / 16);
   }
+  r.chunk_vecs = r.cvstart[s.K()];
   return true;
 }
 
@@ -215,6 +223,14 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     ps.img_bytes = (uint32_t)img;
   }
   pp.tma = tma ? 1 : 0;
+  {
+    uint64_t full_src = 0;  // every full-tile segment length is a 16-B multiple (T % 32 == 0)
+    if (soa_like[0])
+      for (int k = 0; k < s.K(); ++k) full_src += T * s.sizes[k];
+    else
+      full_src = T / s.L * s.B;
+    pp.src_tile_tma = (uint32_t)full_src;
+  }
   pp.src_stage = (uint32_t)align16(pp.side[0].img_bytes);
   pp.dst_stage = (uint32_t)align16(pp.side[1].img_bytes);
   pp.nd = 2;
@@ -248,6 +264,23 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     }
   }
   pp.n_moves = nm;
+
+  // destination padding no tile segment covers: the gaps between aligned
+  // SoA single-blob sub-arrays (reading #9); blocked SoA-like sides with
+  // gaps inside a block are left to the naive path
+  if (soa_like[1] && d.has_padding()) {
+    if (d.kind != LLAMA_SOA_SINGLE_BLOB) { *why = "padded large-block destination"; return false; }
+    uint64_t end = 0;
+    for (int k = 0; k < d.K(); ++k) {
+      if (d.base[k] > end) {
+        pp.gap_blob[pp.n_gaps] = d.blob[k];
+        pp.gap_off[pp.n_gaps] = end;
+        pp.gap_len[pp.n_gaps] = (uint32_t)(d.base[k] - end);
+        ++pp.n_gaps;
+      }
+      end = d.base[k] + d.N * d.sizes[k];
+    }
+  }
   p->path = LLAMA_PATH_PERMUTE;
   p->smem_bytes = (int)smem;
   return true;

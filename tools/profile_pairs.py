@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""Runs selected mapping pairs of a BASELINE config a few times (for ncu
+captures and quick timing).  Usage:
+    python tools/profile_pairs.py --config C2 --pairs aos:soa_mb,aosoa8:soa_mb --iters 3 [--path permute]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2106_04284_b200 as llama  # noqa: E402
+import workloads as W  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--pairs", default="aos:soa_mb")
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--path", default=None)
+ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--records", type=int, default=0)
+a = ap.parse_args()
+cfg = W.CONFIGS[a.config]
+schema = W.SCHEMAS[cfg["schema"]]
+ext = [a.records] if a.records else list(cfg["extents"])
+for pair in a.pairs.split(","):
+    s, d = pair.split(":")
+    sm = llama.Mapping(schema, ext, *W.MAPPINGS[s])
+    dm = llama.Mapping(schema, ext, *W.MAPPINGS[d])
+    sb, db = sm.alloc(), dm.alloc()
+    llama.generate(sm, sb, 42)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile)
+    e0.record()
+    for _ in range(a.iters):
+        llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.iters
+    nbytes = sm.footprint() + dm.footprint()
+    print(f"{s:>12} -> {d:<12} {llama.plan(sm, dm, path=a.path, tile_records=a.tile)} {ms:.3f} ms "
+          f"{nbytes / ms / 1e6:.0f} GB/s", flush=True)
+    del sb, db
