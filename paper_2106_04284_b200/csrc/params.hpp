@@ -100,11 +100,11 @@ struct PermSide {
   DevSide g;          // global normal form (segment addresses)
   uint64_t E;         // records the side's blobs cover (padded block extent / N)
   uint32_t soa_like;  // 1: per-leaf segments
+  uint32_t linear;    // 1: a full tile's segment addresses are linear in the tile index
   uint32_t Limg;      // image lanes (AoS-like: L; SoA-like: T)
   uint32_t limg_shift;
   uint32_t Bimg;      // image block stride
   uint32_t img_bytes; // image bytes of a full tile
-  uint32_t pad_;
 };
 
 struct Move {        // one unit move of the per-record permutation
@@ -126,7 +126,10 @@ struct PermParams {
   uint32_t dst_stage; // bytes of one dst image buffer
   uint32_t ns, nd;    // src stages, dst buffers
   uint32_t src_tile_tma;  // TMA bytes of a full tile's source segments
-  uint32_t pad_;
+  uint32_t debug;         // LLAMA_DEBUG_PERMUTE bits (experiments only): 1 skip permute, 2 skip stores
+  uint32_t unit_end[4];   // moves [0,unit_end[0]) are 8-B units, then 4-, 2-, 1-B units
+  uint32_t tab_moves;     // shared-memory bytes of the move table copy (16-B multiple)
+  uint32_t tab_bytes;     // shared-memory bytes of all table copies (16-B multiple)
   PermSide side[2];   // 0 = src, 1 = dst
   DevLeaf leaf[2][kMaxLeaves];
   uint32_t imgF[2][kMaxLeaves];

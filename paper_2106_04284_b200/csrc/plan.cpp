@@ -3,6 +3,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace llb {
@@ -10,9 +11,16 @@ namespace llb {
 namespace {
 
 constexpr uint64_t kAosLikeMaxBlock = 16384;  // larger AoSoA blocks are tiled inside a block
-constexpr uint64_t kTileTarget = 24 * 1024;   // src + dst image bytes per tile
 constexpr int kBarBytes = 128;
-constexpr int kSmemPerCtaBudget = 112 * 1024; // aim for >= 2 CTAs per SM
+
+// Tuning knobs (defaults measured on B200; env overrides for sweeps):
+//   LLAMA_TILE_BYTES  src + dst image bytes per tile
+//   LLAMA_SMEM_BUDGET shared memory per CTA the stage count may use
+//   LLAMA_STAGES      source stages (2..4); LLAMA_NO_TMA=1 forces LSU copies
+uint64_t env_u64(const char* name, uint64_t def) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::strtoull(v, nullptr, 10) : def;
+}
 
 uint64_t gcd64(uint64_t a, uint64_t b) {
   while (b) { uint64_t t = a % b; a = b; b = t; }
@@ -166,17 +174,21 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   uint64_t T;
   if (tile_records > 0) {
     T = (uint64_t)tile_records;
-    if (T % Tmult) { *why = "tile_records must be a multiple of 32 and of every AoS-like lane count"; return false; }
+    if (T % Tmult || (T > 256 && T % 256)) {
+      *why = "tile_records must be a multiple of 32 and of every AoS-like lane count, and <= 256 or a multiple of 256";
+      return false;
+    }
   } else {
     const uint64_t per = rec_img[0] + rec_img[1];
-    uint64_t c = std::max<uint64_t>(1, kTileTarget / (per * Tmult));
+    uint64_t c = std::max<uint64_t>(1, env_u64("LLAMA_TILE_BYTES", 32 * 1024) / (per * Tmult));
     const uint64_t cmax = std::max<uint64_t>(1, ceil_div(R, Tmult));
     c = std::min(c, cmax);
     T = 0;
     for (; c >= 1; --c) {
-      bool ok = true;
-      for (auto L : Tdiv) ok = ok && (L % (c * Tmult) == 0);
-      if (ok) { T = c * Tmult; break; }
+      const uint64_t t = c * Tmult;
+      bool ok = t <= 256 || t % 256 == 0;  // whole passes of 256 threads (kernel: R records per thread)
+      for (auto L : Tdiv) ok = ok && (L % t == 0);
+      if (ok) { T = t; break; }
     }
     if (!T) { *why = "no tile size divides the AoSoA lane count"; return false; }
   }
@@ -197,6 +209,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     ps.g = side_of(m);
     ps.E = m.E;
     ps.soa_like = soa_like[X] ? 1 : 0;
+    ps.linear = (!soa_like[X] || m.soa()) ? 1 : 0;  // AoS-like or SoA: segment start = a + tile * b
     for (int k = 0; k < m.K(); ++k) pp.leaf[X][k] = m.dev_leaf(k);
     uint64_t img;
     if (!soa_like[X]) {
@@ -222,6 +235,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     }
     ps.img_bytes = (uint32_t)img;
   }
+  if (env_u64("LLAMA_NO_TMA", 0)) tma = false;
   pp.tma = tma ? 1 : 0;
   {
     uint64_t full_src = 0;  // every full-tile segment length is a 16-B multiple (T % 32 == 0)
@@ -233,18 +247,10 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   }
   pp.src_stage = (uint32_t)align16(pp.side[0].img_bytes);
   pp.dst_stage = (uint32_t)align16(pp.side[1].img_bytes);
-  pp.nd = 2;
-  uint64_t smem = 0;
-  for (uint32_t ns = 4; ns >= 2; --ns) {
-    smem = kBarBytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
-    pp.ns = ns;
-    if (smem <= (uint64_t)kSmemPerCtaBudget) break;
-  }
-  if (smem > 227 * 1024) { *why = "tile images exceed shared memory"; return false; }
-
   // per-record move table: leaf k moves in units of the widest power of two
-  // that divides its size and both image offsets for every record
-  uint32_t nm = 0;
+  // that divides its size and both image offsets for every record; grouped by
+  // unit (8, 4, 2, 1 bytes) so the kernel runs one branch-free loop per unit
+  std::vector<Move> mv[4];
   for (int k = 0; k < s.K(); ++k) {
     uint64_t unit = std::min<uint64_t>(8, s.sizes[k]);
     for (int X = 0; X < 2; ++X) {
@@ -254,15 +260,39 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       if (T / ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(ps.Bimg));
       unit = std::min(unit, a);
     }
+    const int cls = unit == 8 ? 0 : unit == 4 ? 1 : unit == 2 ? 2 : 3;
     for (uint64_t j = 0; j < s.sizes[k] / unit; ++j) {
-      if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
-      Move& mv = pp.moves[nm++];
-      mv.soff = (uint32_t)(pp.imgF[0][k] + j * unit);
-      mv.doff = (uint32_t)(pp.imgF[1][k] + j * unit);
-      mv.size = (uint16_t)s.sizes[k];
-      mv.unit = (uint8_t)unit;
+      Move m;
+      m.soff = (uint32_t)(pp.imgF[0][k] + j * unit);
+      m.doff = (uint32_t)(pp.imgF[1][k] + j * unit);
+      m.size = (uint16_t)s.sizes[k];
+      m.unit = (uint8_t)unit;
+      m.pad_ = 0;
+      mv[cls].push_back(m);
     }
   }
+  uint32_t nm = 0;
+  for (int c = 0; c < 4; ++c) {
+    for (auto& m : mv[c]) {
+      if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
+      pp.moves[nm++] = m;
+    }
+    pp.unit_end[c] = nm;
+  }
+  pp.debug = (uint32_t)env_u64("LLAMA_DEBUG_PERMUTE", 0);
+  pp.tab_moves = (uint32_t)align16(12ull * nm);
+  pp.tab_bytes = (uint32_t)(pp.tab_moves + align16(2ull * 24 * s.K()));
+  pp.nd = 2;
+  uint64_t smem = 0;
+  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", 75 * 1000);
+  const uint32_t ns_max = (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_STAGES", 4)));
+  for (uint32_t ns = ns_max; ns >= 2; --ns) {
+    smem = kBarBytes + pp.tab_bytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
+    pp.ns = ns;
+    if (smem <= budget) break;
+  }
+  if (smem > 227 * 1024) { *why = "tile images exceed shared memory"; return false; }
+
   pp.n_moves = nm;
 
   // destination padding no tile segment covers: the gaps between aligned
