@@ -183,9 +183,49 @@ __device__ __forceinline__ void move_class_part(const SMove* __restrict__ mt, ui
   }
 }
 
+// Wide records (few records per tile, many moves): 32 x 32 blocks of
+// (record, move) pairs per warp; at step t lane j moves record rb+j's move
+// mb + ((j+t) & 31).  Lanes hit distinct records AND distinct moves, so both
+// images see spread banks (a record-parallel warp would hit one leaf of 32
+// records at the record stride: 8-way conflicts for 480-B aligned records).
+template <int W>
+__device__ __forceinline__ void diag_class(const PermParams& p, const SMove* __restrict__ mt, uint32_t c0, uint32_t c1,
+                                           uint32_t simg, uint32_t dimg, uint32_t nrec, int warp, int lane,
+                                           uint32_t& turn) {
+  using U = Unit<W>;
+  const uint32_t nrb = (nrec + 31) / 32;
+  const uint32_t nmb = (c1 - c0 + 31) / 32;
+  for (uint32_t b = 0; b < nrb * nmb; ++b, ++turn) {
+    if ((int)(turn % (kThreads / 32)) != warp) continue;
+    const uint32_t rb = (b / nmb) * 32, mb = c0 + (b % nmb) * 32;
+    const uint32_t r = rb + lane;
+    uint32_t sa, sm, da, dm;
+    rec_addr(p.side[0], simg, r, sa, sm);
+    rec_addr(p.side[1], dimg, r, da, dm);
+    const bool rok = r < nrec;
+#pragma unroll 4
+    for (uint32_t t = 0; t < 32; ++t) {
+      const uint32_t m = mb + ((lane + t) & 31);
+      if (rok && m < c1) {
+        const SMove mv = mt[m];
+        U::st(da + mv.doff + dm * mv.size, U::ld(sa + mv.soff + sm * mv.size));
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void permute_any(const PermParams& p, const SMove* mt, uint8_t* simg_p, uint8_t* dimg_p,
                                             uint32_t nrec, int tid) {
   const uint32_t simg = smem_u32(simg_p), dimg = smem_u32(dimg_p);
+  if (p.diag) {
+    const int warp = tid >> 5, lane = tid & 31;
+    uint32_t turn = 0;
+    diag_class<8>(p, mt, 0, p.unit_end[0], simg, dimg, nrec, warp, lane, turn);
+    diag_class<4>(p, mt, p.unit_end[0], p.unit_end[1], simg, dimg, nrec, warp, lane, turn);
+    diag_class<2>(p, mt, p.unit_end[1], p.unit_end[2], simg, dimg, nrec, warp, lane, turn);
+    diag_class<1>(p, mt, p.unit_end[2], p.unit_end[3], simg, dimg, nrec, warp, lane, turn);
+    return;
+  }
   if (nrec == p.T) {  // full tile: passes of 4, 2 or 1 x 256 records (T <= 256 or a multiple of 256)
     uint32_t r0 = 0;
     for (; r0 + 4 * kThreads <= p.T; r0 += 4 * kThreads) permute_full<4>(p, mt, simg, dimg, r0, tid);

@@ -9,6 +9,7 @@ int launch_naive(const NaiveParams& p, void* stream);
 int launch_gen(const GenParams& p, void* stream);
 int launch_fill(const FillParams& p, void* stream);
 int launch_blobcopy(const BlobCopyParams& p, void* stream);
+int launch_bulkcopy(const BulkCopyParams& p, void* stream);
 int launch_run(const RunParams& p, void* stream);
 int launch_permute(const PermParams& p, int smem_bytes, void* stream);
 

@@ -72,6 +72,20 @@ struct BlobCopyParams {
   uint8_t* dst[kMaxBlobs];
 };
 
+// Identity copy through TMA: each blob is cut into chunks of CH bytes that
+// one thread per CTA streams global -> shared -> global with a ring of NS
+// stages (cp.async.bulk load on an mbarrier, cp.async.bulk store).
+struct BulkCopyParams {
+  int32_t nb;
+  uint32_t CH;                       // chunk bytes (16-B multiple)
+  uint32_t NS;                       // ring stages
+  uint32_t pad_;
+  uint64_t cstart[kMaxBlobs + 1];    // prefix of chunks per blob
+  uint64_t bytes[kMaxBlobs];
+  const uint8_t* src[kMaxBlobs];
+  uint8_t* dst[kMaxBlobs];
+};
+
 // ------------------------------------------------------------------ run copy
 // Field-run copy: per leaf, records come in runs of
 // g = gcd(L_s, L_d) that are contiguous on both sides; g*s_k % 16 == 0 and all
@@ -130,6 +144,8 @@ struct PermParams {
   uint32_t unit_end[4];   // moves [0,unit_end[0]) are 8-B units, then 4-, 2-, 1-B units
   uint32_t tab_moves;     // shared-memory bytes of the move table copy (16-B multiple)
   uint32_t tab_bytes;     // shared-memory bytes of all table copies (16-B multiple)
+  uint32_t diag;          // 1: wide records -> diagonal (record, move) permute
+  uint32_t pad2_;
   PermSide side[2];   // 0 = src, 1 = dst
   DevLeaf leaf[2][kMaxLeaves];
   uint32_t imgF[2][kMaxLeaves];

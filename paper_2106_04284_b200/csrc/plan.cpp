@@ -92,13 +92,26 @@ bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why
   if (!same_layout(s, d)) { *why = "layouts differ"; return false; }
   if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
   p->path = LLAMA_PATH_BLOBCOPY;
-  p->blobcopy.reset(new BlobCopyParams);
-  BlobCopyParams& b = *p->blobcopy;
+  if (env_u64("LLAMA_BLOBCOPY_LSU", 0)) {  // thread (LDG/STG) variant, for comparison
+    p->blobcopy.reset(new BlobCopyParams);
+    BlobCopyParams& b = *p->blobcopy;
+    std::memset(&b, 0, sizeof(b));
+    b.nb = d.nblobs();
+    for (int j = 0; j < b.nb; ++j) {
+      b.bytes[j] = d.blob_sizes[j];
+      b.vstart[j + 1] = b.vstart[j] + ceil_div(d.blob_sizes[j], 16);
+    }
+    return true;
+  }
+  p->bulkcopy.reset(new BulkCopyParams);
+  BulkCopyParams& b = *p->bulkcopy;
   std::memset(&b, 0, sizeof(b));
   b.nb = d.nblobs();
+  b.CH = (uint32_t)env_u64("LLAMA_BULK_CHUNK", 65536) & ~15u;  // 64 KB x 3 stages: measured best on B200
+  b.NS = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, env_u64("LLAMA_BULK_STAGES", 3)));
   for (int j = 0; j < b.nb; ++j) {
     b.bytes[j] = d.blob_sizes[j];
-    b.vstart[j + 1] = b.vstart[j] + ceil_div(d.blob_sizes[j], 16);
+    b.cstart[j + 1] = b.cstart[j] + ceil_div(d.blob_sizes[j], b.CH);
   }
   return true;
 }
@@ -179,14 +192,21 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       return false;
     }
   } else {
+    // measured on B200: 32 KB tiles (3 CTAs/SM) when
+    // both sides are single segments; 64 KB (fewer, larger per-leaf TMA
+    // segments) when a side is SoA-like
     const uint64_t per = rec_img[0] + rec_img[1];
-    uint64_t c = std::max<uint64_t>(1, env_u64("LLAMA_TILE_BYTES", 32 * 1024) / (per * Tmult));
+    const uint64_t def_tile = (soa_like[0] || soa_like[1]) ? 64 * 1024 : 32 * 1024;
+    uint64_t c = std::max<uint64_t>(1, env_u64("LLAMA_TILE_BYTES", def_tile) / (per * Tmult));
     const uint64_t cmax = std::max<uint64_t>(1, ceil_div(R, Tmult));
     c = std::min(c, cmax);
     T = 0;
     for (; c >= 1; --c) {
       const uint64_t t = c * Tmult;
-      bool ok = t <= 256 || t % 256 == 0;  // whole passes of 256 threads (kernel: R records per thread)
+      // <= 256 records, or 512 / 1024 (whole passes of 256 threads, R = 2 / 4
+      // records per thread; measured: other multiples and > 116 KB of shared
+      // memory per CTA run markedly slower on B200)
+      bool ok = t <= 256 || t == 512 || t == 1024;
       for (auto L : Tdiv) ok = ok && (L % t == 0);
       if (ok) { T = t; break; }
     }
@@ -280,11 +300,13 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     pp.unit_end[c] = nm;
   }
   pp.debug = (uint32_t)env_u64("LLAMA_DEBUG_PERMUTE", 0);
+  // wide records: few records per tile, many moves -> diagonal permute
+  pp.diag = (uint32_t)env_u64("LLAMA_DIAG", (T < 256 && nm >= 32) ? 1 : 0);
   pp.tab_moves = (uint32_t)align16(12ull * nm);
   pp.tab_bytes = (uint32_t)(pp.tab_moves + align16(2ull * 24 * s.K()));
   pp.nd = 2;
   uint64_t smem = 0;
-  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", 75 * 1000);
+  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", (soa_like[0] || soa_like[1]) ? 120 * 1000 : 75 * 1000);
   const uint32_t ns_max = (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_STAGES", 4)));
   for (uint32_t ns = ns_max; ns >= 2; --ns) {
     smem = kBarBytes + pp.tab_bytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
@@ -331,8 +353,10 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   switch (path) {
     case LLAMA_PATH_AUTO:
       if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
-      if (plan_run(s, d, out, &why)) return LLAMA_OK;
+      // the TMA-staged permute also covers run pairs (SoA <-> AoSoA) and is
+      // faster there on B200 than the direct vector run copy
       if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
+      if (plan_run(s, d, out, &why)) return LLAMA_OK;
       plan_naive(s, d, out);
       return LLAMA_OK;
     case LLAMA_PATH_NAIVE:

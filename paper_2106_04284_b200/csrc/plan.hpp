@@ -20,6 +20,7 @@ struct Plan {
   std::unique_ptr<NaiveParams> naive;
   std::unique_ptr<FillParams> fill;
   std::unique_ptr<BlobCopyParams> blobcopy;
+  std::unique_ptr<BulkCopyParams> bulkcopy;  // TMA variant of the blob copy
   std::unique_ptr<RunParams> run;
   std::unique_ptr<PermParams> perm;
 };

@@ -133,17 +133,20 @@ def _plan(src_name, dst_name, schema=W.PARTICLE7, ext=(16_777_216,)):
 
 
 def test_planner_choices_c2():
-    """Identity -> blob copy; shared >=16 B runs -> run copy
-    (P:759-761); AoS <-> anything -> staged permute."""
+    """Identity -> blob copy; every other C2 pair -> the TMA-staged
+    permute, which on B200 also beats the direct run copy on pairs that share
+    >= 16 B runs; the run copy stays available as a forced path."""
     assert _plan("aos", "aos")["path"] == "blobcopy"
     assert _plan("soa_mb", "soa_mb")["path"] == "blobcopy"
-    assert _plan("aosoa8", "aosoa32")["path"] == "run"
-    assert _plan("soa_mb", "aosoa8")["path"] == "run"
-    assert _plan("aosoa32", "soa_mb")["path"] == "run"
-    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos")]:
+    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos"),
+                 ("aosoa8", "aosoa32"), ("soa_mb", "aosoa8"), ("aosoa32", "soa_mb")]:
         p = _plan(a, b)
         assert p["path"] == "permute" and p["tma"] and p["tile_records"] % 32 == 0
-    assert _plan("aosoa32", "soa_sb", W.LISTING1, (8192, 8192))["path"] == "run"  # C4
+    for a, b in [("aosoa8", "aosoa32"), ("soa_mb", "aosoa8"), ("aosoa32", "soa_mb")]:
+        s = llama.Mapping(W.PARTICLE7, (1024,), *W.MAPPINGS[a])
+        d = llama.Mapping(W.PARTICLE7, (1024,), *W.MAPPINGS[b])
+        assert llama.plan(s, d, path="run")["path"] == "run"
+    assert _plan("aosoa32", "soa_sb", W.LISTING1, (8192, 8192))["path"] == "permute"  # C4
     for a, b in W.C3["pairs"]:
         p = _plan(a, b, W.HEP100, (67_108_864,))
         assert p["path"] == "permute", (a, b, p)

@@ -1,5 +1,5 @@
 import re, sys
-cur = None
+cur = ""
 for line in open(sys.argv[1]):
     if line.startswith('=='):
         cur = line.strip()[3:]
