@@ -272,8 +272,14 @@ def run_ours(args, cfg):
     dom_ms_avg = share[dom][0] / share[dom][2]
     dom_bytes_avg = share[dom][1] / share[dom][2]
     achieved = dom_bytes_avg / (dom_ms_avg * 1e-3) / 1e9
+    traffic = None
+    try:  # dram read+write bytes per launch of this kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": f"k_permute (path {dom})" if dom == "permute" else f"path {dom}",
+                "traffic": traffic, "kernel": f"k_permute (path {dom})" if dom == "permute" else f"path {dom}",
                 "launches_per_step": share[dom][2], "algorithmic_bytes_per_launch": dom_bytes_avg,
                 "peak_source": peak_src, "share_of_step": share[dom][0] / sum(v[0] for v in share.values())}
 
