@@ -24,6 +24,10 @@ constexpr int kThreads = 256;
 constexpr int kBarBytes = 128;  // mbarrier area at the start of dynamic smem
 }  // namespace
 
+// Phase timers (debug bit 4, experiments only): cycles thread 0 spends per
+// phase of the tile loop, summed over CTAs.
+__device__ unsigned long long g_perm_prof[8];
+
 // Per-CTA shared copies of the tables the tile loop reads with a dynamic
 // index (kernel parameters live in the constant bank; dynamic-index reads of
 // a 20 KB parameter block miss the constant cache).
@@ -120,66 +124,68 @@ __device__ __forceinline__ void rec_addr(const PermSide& S, uint32_t img, uint32
   base = img + q * S.Bimg;
 }
 
-// Full tile: every record exists, so no guards.  A thread owns records
-// lane_r + j*Tp (j < R); M moves x R records of independent loads are
-// issued before their stores.
-template <int W, int R, int M>
-__device__ __forceinline__ void move_class_full(const SMove* __restrict__ mt, uint32_t m0, uint32_t m1, uint32_t G,
-                                                const uint32_t (&sa)[R], const uint32_t (&sm)[R],
-                                                const uint32_t (&da)[R], const uint32_t (&dm)[R]) {
-  using U = Unit<W>;
-  uint32_t m = m0;
-  for (; m + (M - 1) * G < m1; m += M * G) {
-    SMove mv[M];
+// One move class for the R records this thread owns.  The record-dependent
+// offsets (block base + (r % Limg) * size) are hoisted out of the move loop;
+// a move is then one load and one store at a warp-uniform offset (soff/doff
+// read from the parameter bank with a uniform index), so the compiler can use
+// [reg + ureg] addressing and batch the R independent loads.
+template <typename U, int R>
+__device__ __forceinline__ void move_class_fast(const PermParams& p, const MoveClass& mc, uint32_t G, uint32_t grp,
+                                                const uint8_t* __restrict__ simg, uint8_t* __restrict__ dimg,
+                                                const uint32_t (&sb)[R], const uint32_t (&sm)[R],
+                                                const uint32_t (&db)[R], const uint32_t (&dm)[R],
+                                                const bool (&ok)[R], bool all) {
+  uint32_t rs[R], rd[R];
 #pragma unroll
-    for (int i = 0; i < M; ++i) mv[i] = mt[m + i * G];
-    typename U::T v[M][R];
-#pragma unroll
-    for (int i = 0; i < M; ++i)
-#pragma unroll
-      for (int j = 0; j < R; ++j) v[i][j] = U::ld(sa[j] + mv[i].soff + sm[j] * mv[i].size);
-#pragma unroll
-    for (int i = 0; i < M; ++i)
-#pragma unroll
-      for (int j = 0; j < R; ++j) U::st(da[j] + mv[i].doff + dm[j] * mv[i].size, v[i][j]);
+  for (int j = 0; j < R; ++j) {
+    rs[j] = sb[j] + sm[j] * mc.size;
+    rd[j] = db[j] + dm[j] * mc.size;
   }
-  for (; m < m1; m += G) {
-    const SMove mv = mt[m];
-    typename U::T v[R];
+  if (all) {
+#pragma unroll 2
+    for (uint32_t m = mc.m0 + grp; m < mc.m1; m += G) {
+      const uint32_t so = p.moves[m].soff, dof = p.moves[m].doff;
+      U v[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) v[j] = U::ld(sa[j] + mv.soff + sm[j] * mv.size);
+      for (int j = 0; j < R; ++j) v[j] = *reinterpret_cast<const U*>(simg + rs[j] + so);
 #pragma unroll
-    for (int j = 0; j < R; ++j) U::st(da[j] + mv.doff + dm[j] * mv.size, v[j]);
+      for (int j = 0; j < R; ++j) *reinterpret_cast<U*>(dimg + rd[j] + dof) = v[j];
+    }
+  } else {
+    for (uint32_t m = mc.m0 + grp; m < mc.m1; m += G) {
+      const uint32_t so = p.moves[m].soff, dof = p.moves[m].doff;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (ok[j]) *reinterpret_cast<U*>(dimg + rd[j] + dof) = *reinterpret_cast<const U*>(simg + rs[j] + so);
+    }
   }
 }
 
 template <int R>
-__device__ __forceinline__ void permute_full(const PermParams& p, const SMove* __restrict__ mt, uint32_t simg,
-                                             uint32_t dimg, uint32_t r0, int tid) {
+__device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t* __restrict__ simg,
+                                             uint8_t* __restrict__ dimg, uint32_t nrec, uint32_t r0, int tid) {
   const uint32_t Tp = p.T < (uint32_t)kThreads ? p.T : (uint32_t)kThreads;  // records per pass
   const uint32_t G = (uint32_t)kThreads / Tp;                               // move groups
   const uint32_t lane_r = (uint32_t)tid % Tp, grp = (uint32_t)tid / Tp;
-  uint32_t sa[R], sm[R], da[R], dm[R];
+  uint32_t sb[R], sm[R], db[R], dm[R];
+  bool ok[R];
+  bool all = true;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const uint32_t r = r0 + lane_r + j * Tp;
-    rec_addr(p.side[0], simg, r, sa[j], sm[j]);
-    rec_addr(p.side[1], dimg, r, da[j], dm[j]);
+    ok[j] = r < nrec;
+    all = all && ok[j];
+    rec_addr(p.side[0], 0u, r, sb[j], sm[j]);
+    rec_addr(p.side[1], 0u, r, db[j], dm[j]);
   }
-  constexpr int M = R >= 4 ? 1 : 4 / R;  // <= 4 loads in flight per thread
-  move_class_full<8, R, M>(mt, grp, p.unit_end[0], G, sa, sm, da, dm);
-  move_class_full<4, R, M>(mt, p.unit_end[0] + grp, p.unit_end[1], G, sa, sm, da, dm);
-  move_class_full<2, R, M>(mt, p.unit_end[1] + grp, p.unit_end[2], G, sa, sm, da, dm);
-  move_class_full<1, R, M>(mt, p.unit_end[2] + grp, p.unit_end[3], G, sa, sm, da, dm);
-}
-
-// Partial (last) tile: records r < nrec only; simple guarded loops.
-template <int W>
-__device__ __forceinline__ void move_class_part(const SMove* __restrict__ mt, uint32_t m0, uint32_t m1, uint32_t G,
-                                                uint32_t sa, uint32_t sm, uint32_t da, uint32_t dm) {
-  for (uint32_t m = m0; m < m1; m += G) {
-    const SMove mv = mt[m];
-    Unit<W>::st(da + mv.doff + dm * mv.size, Unit<W>::ld(sa + mv.soff + sm * mv.size));
+  for (uint32_t c = 0; c < p.n_classes; ++c) {
+    const MoveClass mc = p.classes[c];
+    switch (mc.unit) {
+      case 8: move_class_fast<unsigned long long, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
+      case 4: move_class_fast<uint32_t, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
+      case 2: move_class_fast<unsigned short, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
+      default: move_class_fast<unsigned char, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
+    }
   }
 }
 
@@ -216,8 +222,8 @@ __device__ __forceinline__ void diag_class(const PermParams& p, const SMove* __r
 
 __device__ __forceinline__ void permute_any(const PermParams& p, const SMove* mt, uint8_t* simg_p, uint8_t* dimg_p,
                                             uint32_t nrec, int tid) {
-  const uint32_t simg = smem_u32(simg_p), dimg = smem_u32(dimg_p);
   if (p.diag) {
+    const uint32_t simg = smem_u32(simg_p), dimg = smem_u32(dimg_p);
     const int warp = tid >> 5, lane = tid & 31;
     uint32_t turn = 0;
     diag_class<8>(p, mt, 0, p.unit_end[0], simg, dimg, nrec, warp, lane, turn);
@@ -226,28 +232,14 @@ __device__ __forceinline__ void permute_any(const PermParams& p, const SMove* mt
     diag_class<1>(p, mt, p.unit_end[2], p.unit_end[3], simg, dimg, nrec, warp, lane, turn);
     return;
   }
-  if (nrec == p.T) {  // full tile: passes of 4, 2 or 1 x 256 records (T <= 256 or a multiple of 256)
-    uint32_t r0 = 0;
-    for (; r0 + 4 * kThreads <= p.T; r0 += 4 * kThreads) permute_full<4>(p, mt, simg, dimg, r0, tid);
-    if (r0 + 2 * kThreads <= p.T) {
-      permute_full<2>(p, mt, simg, dimg, r0, tid);
-      r0 += 2 * kThreads;
-    }
-    if (r0 < p.T) permute_full<1>(p, mt, simg, dimg, r0, tid);
-    return;
+  // passes of 4, 2 or 1 x 256 records (T <= 256 or a multiple of 256)
+  uint32_t r0 = 0;
+  for (; r0 + 4 * kThreads <= p.T; r0 += 4 * kThreads) permute_pass<4>(p, simg_p, dimg_p, nrec, r0, tid);
+  if (r0 + 2 * kThreads <= p.T) {
+    permute_pass<2>(p, simg_p, dimg_p, nrec, r0, tid);
+    r0 += 2 * kThreads;
   }
-  const uint32_t Tp = p.T < (uint32_t)kThreads ? p.T : (uint32_t)kThreads;
-  const uint32_t G = (uint32_t)kThreads / Tp;
-  const uint32_t grp = (uint32_t)tid / Tp;
-  for (uint32_t r = (uint32_t)tid % Tp; r < nrec; r += Tp) {
-    uint32_t sa, sm, da, dm;
-    rec_addr(p.side[0], simg, r, sa, sm);
-    rec_addr(p.side[1], dimg, r, da, dm);
-    move_class_part<8>(mt, grp, p.unit_end[0], G, sa, sm, da, dm);
-    move_class_part<4>(mt, p.unit_end[0] + grp, p.unit_end[1], G, sa, sm, da, dm);
-    move_class_part<2>(mt, p.unit_end[1] + grp, p.unit_end[2], G, sa, sm, da, dm);
-    move_class_part<1>(mt, p.unit_end[2] + grp, p.unit_end[3], G, sa, sm, da, dm);
-  }
+  if (r0 < p.T) permute_pass<1>(p, simg_p, dimg_p, nrec, r0, tid);
 }
 
 // Segment j of side X for a full tile, from the shared table (linear sides)
@@ -265,6 +257,60 @@ __device__ __forceinline__ uint32_t tile_nrec(const PermParams& p, uint64_t t0) 
   if (t0 >= p.N) return 0;
   const uint64_t n = p.N - t0;
   return n < p.T ? (uint32_t)n : p.T;
+}
+
+// ---- LSU transfers for sides with many small segments (SoA with many leaves):
+// every thread moves 16-byte chunks (cp.async for loads, arriving on the
+// stage mbarrier; LDS.128 + STG.128 for stores) instead of ~K tiny TMA ops.
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Chunk c of a full tile -> (segment j, byte offset), j advancing monotonically.
+__device__ __forceinline__ uint32_t chunk_seg(const uint32_t* __restrict__ cst, uint32_t c, int& j) {
+  while (c >= cst[j + 1]) ++j;
+  return (c - cst[j]) * 16;
+}
+
+__device__ __forceinline__ void issue_loads_lsu(const PermParams& p, const SSeg* sseg, const uint32_t* cst,
+                                                uint64_t tile, bool full, uint8_t* img, uint64_t* bar, int tid) {
+  const uint32_t simg = smem_u32(img);
+  if (full) {
+    int j = 0;
+    for (uint32_t c = tid; c < cst[n_segs(p, 0)]; c += kThreads) {
+      const uint32_t o = chunk_seg(cst, c, j);
+      cp_async16(simg + sseg[j].soff + o, sseg[j].g0 + tile * sseg[j].tstride + o);
+    }
+  } else {
+    for (int j = 0; j < n_segs(p, 0); ++j) {
+      const Seg sg = tile_seg(p, 0, tile * p.T, j);
+      for (uint32_t o = 16 * tid; o + 16 <= sg.len; o += 16 * kThreads) cp_async16(simg + sg.soff + o, sg.g + o);
+    }
+  }
+  cp_async_arrive_noinc(bar);  // every thread arrives once per phase (count = kThreads)
+}
+
+__device__ __forceinline__ void store_lsu(const PermParams& p, const SSeg* dseg, const uint32_t* cst, uint64_t tile,
+                                          bool full, const uint8_t* dimg, int tid) {
+  if (full) {
+    int j = 0;
+    for (uint32_t c = tid; c < cst[n_segs(p, 1)]; c += kThreads) {
+      const uint32_t o = chunk_seg(cst, c, j);
+      const uint4 v = *reinterpret_cast<const uint4*>(dimg + dseg[j].soff + o);
+      __stcs(reinterpret_cast<uint4*>(dseg[j].g0 + tile * dseg[j].tstride + o), v);
+    }
+  } else {
+    for (int j = 0; j < n_segs(p, 1); ++j) {
+      const Seg sg = tile_seg(p, 1, tile * p.T, j);
+      uint32_t o = 16 * tid;
+      for (; o + 16 <= sg.len; o += 16 * kThreads)
+        __stcs(reinterpret_cast<uint4*>(sg.g + o), *reinterpret_cast<const uint4*>(dimg + sg.soff + o));
+      for (uint32_t q = (sg.len & ~15u) + tid; q < sg.len; q += kThreads) sg.g[q] = dimg[sg.soff + q];
+    }
+  }
 }
 
 // Issues the TMA loads of a tile's source segments into one stage (warp 0):
@@ -290,16 +336,20 @@ __device__ __forceinline__ void issue_loads(const PermParams& p, const SSeg* sse
 
 template <bool kTma>
 __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__ PermParams p) {
-  // dynamic smem: [mbarriers | move table | src seg table | dst seg table | src ring | dst buffers]
+  // dynamic smem: [mbarriers | move table | src seg table | dst seg table |
+  //                src chunk prefix | dst chunk prefix | src ring | dst buffers]
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   SMove* mt = reinterpret_cast<SMove*>(smem + kBarBytes);
   SSeg* sseg = reinterpret_cast<SSeg*>(smem + kBarBytes + p.tab_moves);
   SSeg* dseg = sseg + p.K;
+  uint32_t* scst = reinterpret_cast<uint32_t*>(dseg + p.K);
+  uint32_t* dcst = scst + (p.K + 1);
   uint8_t* sbuf = smem + kBarBytes + p.tab_bytes;
   uint8_t* dbuf = sbuf + (size_t)p.ns * p.src_stage;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const bool lsu_s = kTma && p.lsu[0], lsu_d = kTma && p.lsu[1];
 
   // Zero both destination images once: padding positions are never written
   // by a move, so they stay 0 for every tile.
@@ -314,8 +364,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
       (X == 0 ? sseg : dseg)[k] = SSeg{s0.g, (uint64_t)(s1.g - s0.g), s0.soff, s0.len};
     }
   }
+  if (tid == 0) {  // 16-byte chunk prefixes of the full-tile segments (LSU sides)
+    uint32_t a = 0, b = 0;
+    scst[0] = dcst[0] = 0;
+    for (uint32_t k = 0; k < p.K; ++k) {
+      if (p.lsu[0] && (int)k < n_segs(p, 0)) a += tile_seg(p, 0, 0, (int)k).len / 16;
+      if (p.lsu[1] && (int)k < n_segs(p, 1)) b += tile_seg(p, 1, 0, (int)k).len / 16;
+      scst[k + 1] = a;
+      dcst[k + 1] = b;
+    }
+  }
   if (kTma && tid == 0) {
-    for (uint32_t s = 0; s < p.ns; ++s) mbar_init(&bars[s], 1);
+    for (uint32_t s = 0; s < p.ns; ++s) mbar_init(&bars[s], lsu_s ? kThreads : 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -326,10 +386,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
 
   const uint64_t first = blockIdx.x, stride = gridDim.x;
   const uint64_t n_full = p.N / p.T;  // tiles [0, n_full) are full: no tails, no clipping
-  if (kTma && warp == 0) {
+  const bool only_permute = p.debug & 16;
+  if (kTma && !only_permute) {
     for (uint32_t s = 0; s < p.ns; ++s) {
       const uint64_t tile = first + s * stride;
-      if (tile < p.n_tiles) issue_loads(p, sseg, tile, tile < n_full, sbuf + (size_t)s * p.src_stage, &bars[s], lane);
+      if (tile >= p.n_tiles) break;
+      uint8_t* img = sbuf + (size_t)s * p.src_stage;
+      if (lsu_s) issue_loads_lsu(p, sseg, scst, tile, tile < n_full, img, &bars[s], tid);
+      else if (warp == 0) issue_loads(p, sseg, tile, tile < n_full, img, &bars[s], lane);
     }
   }
 
@@ -342,10 +406,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
     const bool full = tile < n_full;
     const uint32_t nrec = full ? p.T : tile_nrec(p, t0);
 
-    if (kTma) {
+    const bool prof = (p.debug & 4) && tid == 0;
+    long long c0 = prof ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    if (only_permute) {
+      // experiment: permute the stage's stale bytes, no memory traffic
+    } else if (kTma) {
       if (warp == 0) {  // one warp waits; the others sleep in the barrier below
         if (lane == 0) mbar_wait(&bars[s], (it / p.ns) & 1);
-        if (it >= 2) bulk_wait_read<1>();  // dst buffer d (tile it-2) has been read out
+        if (prof) c1 = clock64();
+        if (!lsu_d && it >= 2) bulk_wait_read<1>();  // dst buffer d (tile it-2) has been read out
         __syncwarp();
       }
       if (!full) {  // sub-16-byte tails of the last tile's segments
@@ -369,28 +438,48 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
+    if (prof) c2 = clock64();
     if (!(p.debug & 1)) permute_any(p, mt, simg, dimg, nrec, tid);
-    if (kTma) fence_proxy_async_smem();
+    long long cf = prof ? clock64() : 0;
+    if (kTma && !lsu_d) fence_proxy_async_smem();
+    if (prof) c3 = clock64();
     __syncthreads();
+    if (prof) c4 = clock64();
 
     const int nds = n_segs(p, 1);
-    if (kTma) {
-      if (warp == 0) {
+    if (only_permute) {
+    } else if (kTma) {
+      const uint64_t next = tile + (uint64_t)p.ns * stride;
+      if (lsu_d) {
+        if (!(p.debug & 2)) store_lsu(p, dseg, dcst, tile, full, dimg, tid);
+      } else if (warp == 0) {
         for (int j = lane; j < nds; j += 32) {
           const Seg sg = full ? full_seg(p, dseg, 1, tile, j) : tile_seg(p, 1, t0, j);
           const uint32_t body = sg.len & ~15u;
           if (body && !(p.debug & 2)) bulk_s2g(sg.g, dimg + sg.soff, body);
         }
         bulk_commit();
-        // ring slot s is free again (every thread passed the barrier): prefetch
-        const uint64_t next = tile + (uint64_t)p.ns * stride;
-        if (next < p.n_tiles) issue_loads(p, sseg, next, next < n_full, simg, &bars[s], lane);
       }
-      if (!full) {
+      // ring slot s is free again (every thread passed the barrier): prefetch
+      if (next < p.n_tiles) {
+        if (lsu_s) issue_loads_lsu(p, sseg, scst, next, next < n_full, simg, &bars[s], tid);
+        else if (warp == 0) issue_loads(p, sseg, next, next < n_full, simg, &bars[s], lane);
+      }
+      if (!full && !lsu_d) {
         for (int j = 0; j < nds; ++j) {
           const Seg sg = tile_seg(p, 1, t0, j);
           for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += kThreads) sg.g[o] = dimg[sg.soff + o];
         }
+      }
+      if (prof) {
+        const long long c5 = clock64();
+        atomicAdd(&g_perm_prof[0], (unsigned long long)(c1 - c0));  // mbarrier wait (TMA load)
+        atomicAdd(&g_perm_prof[1], (unsigned long long)(c2 - c1));  // store drain + barrier A
+        atomicAdd(&g_perm_prof[2], (unsigned long long)(c3 - c2));  // permute (thread 0) + fence
+        atomicAdd(&g_perm_prof[3], (unsigned long long)(c4 - c3));  // barrier B (slowest thread)
+        atomicAdd(&g_perm_prof[4], (unsigned long long)(c5 - c4));  // issue stores + next loads
+        atomicAdd(&g_perm_prof[5], 1ull);                           // tiles
+        atomicAdd(&g_perm_prof[6], (unsigned long long)(c3 - cf));  // fence.proxy.async alone
       }
     } else {
       for (int j = 0; j < nds; ++j) {
@@ -399,7 +488,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
       }
     }
   }
-  if (kTma && warp == 0) bulk_wait_all();
+  if (kTma && warp == 0 && !only_permute) bulk_wait_all();
+}
+
+// Debug hook (not in the public header): read and optionally reset the phase timers.
+extern "C" int llama_debug_permute_profile(unsigned long long* out8, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, g_perm_prof, sizeof(g_perm_prof));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0};
+    e = cudaMemcpyToSymbol(g_perm_prof, z, sizeof(z));
+  }
+  return (int)e;
 }
 
 int launch_permute(const PermParams& p, int smem_bytes, void* stream) {

@@ -270,7 +270,10 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   // per-record move table: leaf k moves in units of the widest power of two
   // that divides its size and both image offsets for every record; grouped by
   // unit (8, 4, 2, 1 bytes) so the kernel runs one branch-free loop per unit
-  std::vector<Move> mv[4];
+  // classes by (unit, leaf size): within a class the record-dependent part of
+  // an image offset is the same for every move, so the kernel hoists it
+  std::vector<Move> mv[4][4];  // [unit class][size class]
+  auto lg = [](uint64_t v) { return v == 8 ? 0 : v == 4 ? 1 : v == 2 ? 2 : 3; };
   for (int k = 0; k < s.K(); ++k) {
     uint64_t unit = std::min<uint64_t>(8, s.sizes[k]);
     for (int X = 0; X < 2; ++X) {
@@ -280,7 +283,6 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       if (T / ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(ps.Bimg));
       unit = std::min(unit, a);
     }
-    const int cls = unit == 8 ? 0 : unit == 4 ? 1 : unit == 2 ? 2 : 3;
     for (uint64_t j = 0; j < s.sizes[k] / unit; ++j) {
       Move m;
       m.soff = (uint32_t)(pp.imgF[0][k] + j * unit);
@@ -288,22 +290,39 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       m.size = (uint16_t)s.sizes[k];
       m.unit = (uint8_t)unit;
       m.pad_ = 0;
-      mv[cls].push_back(m);
+      mv[lg(unit)][lg(s.sizes[k])].push_back(m);
     }
   }
   uint32_t nm = 0;
+  pp.n_classes = 0;
   for (int c = 0; c < 4; ++c) {
-    for (auto& m : mv[c]) {
-      if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
-      pp.moves[nm++] = m;
+    for (int z = 0; z < 4; ++z) {
+      if (mv[c][z].empty()) continue;
+      MoveClass& mc = pp.classes[pp.n_classes++];
+      mc.m0 = nm;
+      for (auto& m : mv[c][z]) {
+        if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
+        pp.moves[nm++] = m;
+      }
+      mc.m1 = nm;
+      mc.unit = 8u >> c;
+      mc.size = 8u >> z;
     }
     pp.unit_end[c] = nm;
   }
   pp.debug = (uint32_t)env_u64("LLAMA_DEBUG_PERMUTE", 0);
-  // wide records: few records per tile, many moves -> diagonal permute
-  pp.diag = (uint32_t)env_u64("LLAMA_DIAG", (T < 256 && nm >= 32) ? 1 : 0);
+  // diagonal (record, move) permute for wide records
+  pp.diag = (uint32_t)env_u64("LLAMA_DIAG", 0);  // opt-in: measured slower than record-parallel
   pp.tab_moves = (uint32_t)align16(12ull * nm);
-  pp.tab_bytes = (uint32_t)(pp.tab_moves + align16(2ull * 24 * s.K()));
+  pp.tab_bytes = (uint32_t)(pp.tab_moves + align16(2ull * 24 * s.K()) + align16(2ull * 4 * (s.K() + 1)));
+  // sides with many small per-leaf segments move them with all threads (a TMA
+  // bulk op costs ~0.1 us; 100 leaves x 2 sides per tile starve the pipeline)
+  for (int X = 0; X < 2; ++X) {
+    const Mapping& m = *side[X];
+    const bool many = soa_like[X] && m.K() > 16;
+    // opt-in (LLAMA_LSU_SEGS=1): measured no faster than TMA segments on B200
+    pp.lsu[X] = (uint32_t)(pp.tma && soa_like[X] && pp.side[X].linear && env_u64("LLAMA_LSU_SEGS", 0) && many);
+  }
   pp.nd = 2;
   uint64_t smem = 0;
   const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", (soa_like[0] || soa_like[1]) ? 120 * 1000 : 75 * 1000);
