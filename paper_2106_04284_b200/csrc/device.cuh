@@ -56,6 +56,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -97,6 +101,29 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // async-proxy (TMA) reads of them.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Host side: per-device cache of the dynamic-smem attribute and occupancy of
+// a kernel for the last shared-memory size it was launched with (these driver
+// queries cost tens of microseconds; a copy should not pay them every launch).
+struct LaunchCache {
+  int smem = -1;
+  int per_sm = 1;
+};
+
+template <typename K>
+inline int prepare_kernel(K kernel, int threads, int smem_bytes, LaunchCache* cache, int* per_sm) {
+  if (cache->smem != smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (e != cudaSuccess) return (int)e;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem_bytes);
+    cache->per_sm = n < 1 ? 1 : n;
+    cache->smem = smem_bytes;
+  }
+  *per_sm = cache->per_sm;
+  return 0;
 }
 
 }  // namespace llb

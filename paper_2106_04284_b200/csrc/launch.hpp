@@ -11,7 +11,9 @@ int launch_fill(const FillParams& p, void* stream);
 int launch_blobcopy(const BlobCopyParams& p, void* stream);
 int launch_bulkcopy(const BulkCopyParams& p, void* stream);
 int launch_run(const RunParams& p, void* stream);
-int launch_permute(const PermParams& p, int smem_bytes, void* stream);
+int launch_permute(const PermParams& p, int smem_bytes, void* stream);     // chooses v1 / warp-specialised
+int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream);
+int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream);
 
 const char* cuda_error_string(int err);
 int current_device_sms(int* sms);   // SM count of the current device

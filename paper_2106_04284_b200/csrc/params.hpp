@@ -146,14 +146,10 @@ struct PermParams {
   uint32_t dst_stage; // bytes of one dst image buffer
   uint32_t ns, nd;    // src stages, dst buffers
   uint32_t src_tile_tma;  // TMA bytes of a full tile's source segments
-  uint32_t debug;         // LLAMA_DEBUG_PERMUTE bits (experiments only): 1 skip permute, 2 skip stores
   uint32_t unit_end[4];   // moves [0,unit_end[0]) are 8-B units, then 4-, 2-, 1-B units
   uint32_t n_classes;
   MoveClass classes[kMaxClasses];
-  uint32_t tab_moves;     // shared-memory bytes of the move table copy (16-B multiple)
-  uint32_t tab_bytes;     // shared-memory bytes of all table copies (16-B multiple)
-  uint32_t diag;          // 1: wide records -> diagonal (record, move) permute
-  uint32_t lsu[2];        // per side: move segments with all threads (cp.async / STG) instead of TMA
+  uint32_t tab_bytes;     // shared-memory bytes of the segment tables (16-B multiple)
   uint32_t pad2_;
   PermSide side[2];   // 0 = src, 1 = dst
   DevLeaf leaf[2][kMaxLeaves];

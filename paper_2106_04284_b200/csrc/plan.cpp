@@ -310,19 +310,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     }
     pp.unit_end[c] = nm;
   }
-  pp.debug = (uint32_t)env_u64("LLAMA_DEBUG_PERMUTE", 0);
-  // diagonal (record, move) permute for wide records
-  pp.diag = (uint32_t)env_u64("LLAMA_DIAG", 0);  // opt-in: measured slower than record-parallel
-  pp.tab_moves = (uint32_t)align16(12ull * nm);
-  pp.tab_bytes = (uint32_t)(pp.tab_moves + align16(2ull * 24 * s.K()) + align16(2ull * 4 * (s.K() + 1)));
-  // sides with many small per-leaf segments move them with all threads (a TMA
-  // bulk op costs ~0.1 us; 100 leaves x 2 sides per tile starve the pipeline)
-  for (int X = 0; X < 2; ++X) {
-    const Mapping& m = *side[X];
-    const bool many = soa_like[X] && m.K() > 16;
-    // opt-in (LLAMA_LSU_SEGS=1): measured no faster than TMA segments on B200
-    pp.lsu[X] = (uint32_t)(pp.tma && soa_like[X] && pp.side[X].linear && env_u64("LLAMA_LSU_SEGS", 0) && many);
-  }
+  pp.tab_bytes = (uint32_t)align16(2ull * 32 * s.K());  // SSeg tables (24 B each, padded)
   pp.nd = 2;
   uint64_t smem = 0;
   const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", (soa_like[0] || soa_like[1]) ? 120 * 1000 : 75 * 1000);

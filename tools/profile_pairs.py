@@ -8,6 +8,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("LLAMA_PKG_ROOT"):  # A/B against another build of the package
+    sys.path.insert(0, os.environ["LLAMA_PKG_ROOT"])
 import torch  # noqa: E402
 
 import paper_2106_04284_b200 as llama  # noqa: E402
