@@ -192,11 +192,13 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       return false;
     }
   } else {
-    // measured on B200: 32 KB tiles (3 CTAs/SM) when
-    // both sides are single segments; 64 KB (fewer, larger per-leaf TMA
-    // segments) when a side is SoA-like
+    // measured on B200 with the warp-specialised kernel (DESIGN.md "Tile
+    // size"): small records (<= 128 B src + dst) -> 64 KB tiles (T = 1024
+    // for Particle7) with a deep ring in one CTA per SM; wide records (whose
+    // permute costs more per tile) -> the largest tile that still leaves two
+    // CTAs per SM (budget below)
     const uint64_t per = rec_img[0] + rec_img[1];
-    const uint64_t def_tile = (soa_like[0] || soa_like[1]) ? 64 * 1024 : 32 * 1024;
+    const uint64_t def_tile = per <= 128 ? 64 * 1024 : 48 * 1024;
     uint64_t c = std::max<uint64_t>(1, env_u64("LLAMA_TILE_BYTES", def_tile) / (per * Tmult));
     const uint64_t cmax = std::max<uint64_t>(1, ceil_div(R, Tmult));
     c = std::min(c, cmax);
@@ -208,6 +210,10 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       // memory per CTA run markedly slower on B200)
       bool ok = t <= 256 || t == 512 || t == 1024;
       for (auto L : Tdiv) ok = ok && (L % t == 0);
+      // wide records: the tile must leave room for two CTAs per SM with two
+      // source stages (measured: one CTA per SM starves the permute of warps)
+      const uint64_t est = 256 + 64ull * s.K() + 2 * (t * rec_img[0] + 16ull * s.K()) + 2 * (t * rec_img[1] + 16ull * s.K());
+      if (per > 128 && c > 1 && est > env_u64("LLAMA_SMEM_BUDGET", 112 * 1000)) ok = false;
       if (ok) { T = t; break; }
     }
     if (!T) { *why = "no tile size divides the AoSoA lane count"; return false; }
@@ -313,15 +319,20 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   pp.tab_bytes = (uint32_t)align16(2ull * 32 * s.K());  // SSeg tables (24 B each, padded)
   pp.nd = 2;
   uint64_t smem = 0;
-  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", (soa_like[0] || soa_like[1]) ? 120 * 1000 : 75 * 1000);
-  const uint32_t ns_max = (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_STAGES", 4)));
+  const uint64_t per_rec = rec_img[0] + rec_img[1];
+  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", per_rec <= 128 ? 230 * 1000 : 112 * 1000);
+  // small records: a deep (4-stage) ring; wide records: 2 stages, so more CTAs fit per SM
+  const uint32_t ns_max =
+      (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_STAGES", per_rec <= 128 ? 4 : 2)));
   for (uint32_t ns = ns_max; ns >= 2; --ns) {
     smem = kBarBytes + pp.tab_bytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
     pp.ns = ns;
-    if (smem <= budget) break;
+    // measured on B200: one CTA with 116-160 KB of shared memory runs far
+    // slower than both 108 KB and 172 KB (C4: 3.5 vs 6.0 TB/s); skip the window
+    const bool window = smem > 116 * 1024 && smem < 160 * 1024 && !std::getenv("LLAMA_STAGES");
+    if (smem <= budget && !(window && ns > 2)) break;
   }
   if (smem > 227 * 1024) { *why = "tile images exceed shared memory"; return false; }
-
   pp.n_moves = nm;
 
   // destination padding no tile segment covers: the gaps between aligned
@@ -359,10 +370,11 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   std::string why;
   switch (path) {
     case LLAMA_PATH_AUTO:
-      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
-      // the TMA-staged permute also covers run pairs (SoA <-> AoSoA) and is
-      // faster there on B200 than the direct vector run copy
+      // the warp-specialised TMA permute measured fastest on B200 for every
+      // pair it applies to -- identities (6.25-6.40 vs 6.14-6.20 TB/s for the
+      // bulk blob copy) and run pairs (SoA <-> AoSoA) included
       if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
+      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
       plan_naive(s, d, out);
       return LLAMA_OK;

@@ -133,12 +133,14 @@ def _plan(src_name, dst_name, schema=W.PARTICLE7, ext=(16_777_216,)):
 
 
 def test_planner_choices_c2():
-    """Identity -> blob copy; every other C2 pair -> the TMA-staged
-    permute, which on B200 also beats the direct run copy on pairs that share
-    >= 16 B runs; the run copy stays available as a forced path."""
-    assert _plan("aos", "aos")["path"] == "blobcopy"
-    assert _plan("soa_mb", "soa_mb")["path"] == "blobcopy"
-    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos"),
+    """Every C2 pair -> the warp-specialised TMA permute, which on B200 beats
+    the bulk blob copy on identities and the direct run copy on pairs
+    that share >= 16 B runs; both stay available as forced paths."""
+    for name in ("aos", "soa_mb", "aosoa8"):
+        s = llama.Mapping(W.PARTICLE7, (1000,), *W.MAPPINGS[name])
+        d = llama.Mapping(W.PARTICLE7, (1000,), *W.MAPPINGS[name])
+        assert llama.plan(s, d, path="blobcopy")["path"] == "blobcopy"
+    for a, b in [("aos", "aos"), ("soa_mb", "soa_mb"), ("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos"),
                  ("aosoa8", "aosoa32"), ("soa_mb", "aosoa8"), ("aosoa32", "soa_mb")]:
         p = _plan(a, b)
         assert p["path"] == "permute" and p["tma"] and p["tile_records"] % 32 == 0
