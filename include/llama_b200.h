@@ -187,6 +187,36 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
 llama_status llama_generate(const llama_mapping* m, void* const* blobs, uint64_t seed,
                             uint8_t pad_byte, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Staged cross-address-space copy (§3.9: "use smaller intermediate
+ * views to shuffle a chunk from one mapping to the other and then perform a
+ * copy of that chunk into the other address space, potentially overlapping
+ * shuffles and copies in an asynchronous workflow").
+ *
+ * A stager owns device staging memory and three streams of the device that
+ * is current when it is created.  llama_copy_staged cuts the copy into slabs
+ * of records whose bytes are contiguous ranges of every blob; per slab it
+ * DMAs the source ranges into staging memory (cudaMemcpyAsync), relayouts
+ * the slab there with the copy kernels (llama_copy on 1-D views of the slab),
+ * and DMAs the destination ranges back, overlapping the three steps of
+ * consecutive slabs.  Source and destination blobs may be host memory
+ * (pinned for full PCIe speed; pageable works but serialises) or device
+ * memory.  Same result contract as llama_copy (destination padding := 0).
+ */
+typedef struct llama_stager llama_stager; /* opaque; not thread-safe: one copy at a time */
+
+/* Creates a stager with `slab_bytes` of staging memory per side and buffer
+ * (3 buffers x 2 sides are allocated with cudaMalloc).  0 = 64 MiB.
+ * Errors: INVALID_ARGUMENT, CUDA (no device / allocation failed). */
+llama_status llama_stager_create(uint64_t slab_bytes, llama_stager** out);
+void llama_stager_destroy(llama_stager* st); /* NULL-safe; synchronises its streams */
+
+/* Enqueues the staged copy after all work already enqueued on `stream`;
+ * `stream` waits for its completion.  Errors as llama_copy, plus UNSUPPORTED
+ * when one slab of whole AoSoA blocks does not fit the staging memory. */
+llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
+                               const llama_mapping* dst_map, void* const* dst_blobs, void* stream);
+
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t llama_launch_count(void);
 

@@ -33,7 +33,8 @@ STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_
 EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_mapping_destroy",
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
-           "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version"]
+           "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
+           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged"]
 
 
 class LlamaError(RuntimeError):
@@ -83,6 +84,10 @@ def _load():
     lib.llama_copy_ex.argtypes = [ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p, P(_Options)]
     lib.llama_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(_Options), P(_PlanInfo)]
     lib.llama_generate.argtypes = [ctypes.c_void_p, vpp, ctypes.c_uint64, ctypes.c_uint8, ctypes.c_void_p]
+    lib.llama_stager_create.argtypes = [ctypes.c_uint64, P(ctypes.c_void_p)]
+    lib.llama_stager_destroy.argtypes = [ctypes.c_void_p]
+    lib.llama_stager_destroy.restype = None
+    lib.llama_copy_staged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
     lib.llama_launch_count.restype = ctypes.c_uint64
     lib.llama_status_string.restype = ctypes.c_char_p
     lib.llama_status_string.argtypes = [ctypes.c_int]
@@ -177,7 +182,27 @@ class Mapping:
                 torch.empty(16, dtype=torch.uint8, device=device) for s in self.blob_sizes()]
 
 
-def _ptrs(blobs, sizes, what):
+class Stager:
+    """Device staging memory + streams for llama_copy_staged:
+    slab_bytes per side per buffer (3 buffers x 2 sides), 0 = 64 MiB."""
+
+    def __init__(self, slab_bytes=0):
+        h = ctypes.c_void_p()
+        _check(_lib.llama_stager_create(int(slab_bytes), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.llama_stager_destroy(h)
+            self._h = None
+
+
+def _ptrs(blobs, sizes, what, device_only=True):
     if len(blobs) < len(sizes):
         raise LlamaError(-1, f"{what}: {len(sizes)} blobs needed, {len(blobs)} given")
     arr = (ctypes.c_void_p * max(1, len(blobs)))()
@@ -187,7 +212,7 @@ def _ptrs(blobs, sizes, what):
             continue
         if j < len(sizes) and b.numel() * b.element_size() < sizes[j]:
             raise LlamaError(-1, f"{what}[{j}] holds {b.numel() * b.element_size()} bytes, needs {sizes[j]}")
-        if not b.is_cuda:
+        if device_only and not b.is_cuda:
             raise LlamaError(-1, f"{what}[{j}] is not a CUDA tensor")
         arr[j] = b.data_ptr()
     return arr
@@ -213,6 +238,14 @@ def copy(src_map, src_blobs, dst_map, dst_blobs, stream=None, path=None, tile_re
     d = _ptrs(dst_blobs, dst_map.blob_sizes(), "dst_blobs")
     opt = _options(path, tile_records)
     _check(_lib.llama_copy_ex(src_map.handle, s, dst_map.handle, d, _stream(stream), ctypes.byref(opt)))
+
+
+def copy_staged(stager, src_map, src_blobs, dst_map, dst_blobs, stream=None):
+    """Staged copy between host (pinned) and/or device blobs (llama_copy_staged):
+    slab DMA in, relayout on the device, DMA out, overlapped on three streams."""
+    s = _ptrs(src_blobs, src_map.blob_sizes(), "src_blobs", device_only=False)
+    d = _ptrs(dst_blobs, dst_map.blob_sizes(), "dst_blobs", device_only=False)
+    _check(_lib.llama_copy_staged(stager.handle, src_map.handle, s, dst_map.handle, d, _stream(stream)))
 
 
 def plan(src_map, dst_map, path=None, tile_records=0):

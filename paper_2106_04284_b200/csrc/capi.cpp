@@ -8,14 +8,9 @@
 #include <string>
 #include <tuple>
 
+#include "capi_internal.hpp"
 #include "launch.hpp"
-#include "llama_b200.h"
-#include "mapping.hpp"
 #include "plan.hpp"
-
-struct llama_mapping {
-  llb::Mapping m;
-};
 
 namespace {
 
@@ -65,6 +60,10 @@ llama_status check_blobs(const llb::Mapping& m, void* const* blobs, const char* 
 }
 
 }  // namespace
+
+namespace llb {
+llama_status set_error(llama_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace llb
 
 extern "C" {
 

@@ -1,0 +1,257 @@
+// staged.cpp -- llama_copy_staged: the staged cross-address-space copy the
+// paper proposes (§3.9: "use smaller intermediate views to shuffle
+// a chunk from one mapping to the other and then perform a copy of that chunk
+// into the other address space, potentially overlapping shuffles and copies
+// in an asynchronous workflow").
+//
+// The records are cut into slabs [a, b) whose bytes are contiguous ranges of
+// every blob (slab boundaries on whole AoSoA blocks).  A slab is a complete
+// 1-D view of its own (the normal form depends only on the flat index), so:
+//   h2d stream:  DMA the slab's source ranges into a staging buffer
+//   comp stream: llama_copy between the slab's 1-D views, in staging memory
+//   d2h stream:  DMA the slab's destination ranges back
+// with three buffers in rotation, consecutive slabs overlap the two DMA
+// directions and the relayout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "capi_internal.hpp"
+
+namespace {
+
+constexpr int kNB = 3;              // staging buffers in rotation
+constexpr uint64_t kAlignLocal = 16;  // blob bases in staging memory (TMA needs 16 B)
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+uint64_t gcd64(uint64_t a, uint64_t b) {
+  while (b) { uint64_t t = a % b; a = b; b = t; }
+  return a;
+}
+
+struct Range {       // one contiguous byte range of a slab
+  int gblob;         // blob of the global view
+  uint64_t goff;     // offset in the global blob
+  int lblob;         // blob of the slab's 1-D view
+  uint64_t loff;     // offset in the local blob
+  uint64_t len;
+};
+
+// The ranges of records [a, b) of mapping g, as laid out in the slab's 1-D
+// view l (same kind / lanes / alignment, extent b - a).  a is a multiple of
+// g's block size when g is blocked.
+void slab_ranges(const llb::Mapping& g, const llb::Mapping& l, uint64_t a, uint64_t b, std::vector<Range>* out) {
+  out->clear();
+  if (b <= a) return;
+  if (!g.soa()) {  // AoS / AoSoA: whole blocks, one range
+    const uint64_t blk0 = a / g.L, blk1 = (b + g.L - 1) / g.L;
+    out->push_back(Range{0, g.base[0] + blk0 * g.B, 0, 0, (blk1 - blk0) * g.B});
+    return;
+  }
+  for (int k = 0; k < g.K(); ++k)  // SoA: one range per leaf sub-array
+    out->push_back(Range{(int)g.blob[k], g.offset(a, k), (int)l.blob[k], l.offset(0, k), (b - a) * g.sizes[k]});
+}
+
+}  // namespace
+
+struct llama_stager {
+  int device = 0;
+  uint64_t cap = 0;  // bytes per side per buffer
+  uint8_t* buf[kNB][2] = {};
+  uint8_t* zero = nullptr;  // 4 KB of device zeros (gap fills)
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t e_in[kNB] = {}, e_comp[kNB] = {}, e_out[kNB] = {}, e_start = nullptr, e_done = nullptr;
+  std::map<std::tuple<uint64_t, uint64_t>, llama_mapping*> local;  // (parent id, records) -> 1-D view
+  ~llama_stager() {
+    if (h2d) cudaStreamSynchronize(h2d);
+    if (comp) cudaStreamSynchronize(comp);
+    if (d2h) cudaStreamSynchronize(d2h);
+    for (auto& kv : local) llama_mapping_destroy(kv.second);
+    for (int j = 0; j < kNB; ++j) {
+      cudaFree(buf[j][0]);
+      cudaFree(buf[j][1]);
+      if (e_in[j]) cudaEventDestroy(e_in[j]);
+      if (e_comp[j]) cudaEventDestroy(e_comp[j]);
+      if (e_out[j]) cudaEventDestroy(e_out[j]);
+    }
+    cudaFree(zero);
+    if (e_start) cudaEventDestroy(e_start);
+    if (e_done) cudaEventDestroy(e_done);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (comp) cudaStreamDestroy(comp);
+    if (d2h) cudaStreamDestroy(d2h);
+  }
+  llama_mapping* view(const llama_mapping* parent, uint64_t n) {
+    auto key = std::make_tuple(parent->m.id, n);
+    auto it = local.find(key);
+    if (it != local.end()) return it->second;
+    const llb::Mapping& p = parent->m;
+    const int64_t ext = (int64_t)n;
+    llama_mapping_desc d{p.types.data(), p.K(), &ext, 1, p.kind, p.lanes, p.aligned ? 1 : 0};
+    llama_mapping* m = nullptr;
+    if (llama_mapping_create(&d, &m) != LLAMA_OK) return nullptr;
+    local[key] = m;
+    return m;
+  }
+};
+
+namespace {
+
+llama_status cuda_err(cudaError_t e, const char* what) {
+  return llb::set_error(LLAMA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Local blob base offsets inside one staging buffer (each blob 16-B aligned);
+// returns the bytes used.
+uint64_t layout_local(const llb::Mapping& l, std::vector<uint64_t>* base) {
+  base->assign(l.nblobs(), 0);
+  uint64_t off = 0;
+  for (int b = 0; b < l.nblobs(); ++b) {
+    (*base)[b] = off;
+    off = round_up(off + l.blob_sizes[b], kAlignLocal);
+  }
+  return off;
+}
+
+}  // namespace
+
+extern "C" {
+
+llama_status llama_stager_create(uint64_t slab_bytes, llama_stager** out) {
+  if (!out) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL out");
+  auto* st = new (std::nothrow) llama_stager;
+  if (!st) return llb::set_error(LLAMA_ERR_OOM, "out of host memory");
+  st->cap = round_up(slab_bytes ? slab_bytes : (64ull << 20), kAlignLocal);
+  cudaError_t e = cudaGetDevice(&st->device);
+  for (int j = 0; j < kNB && e == cudaSuccess; ++j) {
+    e = cudaMalloc(&st->buf[j][0], st->cap);
+    if (e == cudaSuccess) e = cudaMalloc(&st->buf[j][1], st->cap);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->e_in[j], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->e_comp[j], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->e_out[j], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&st->zero, 4096);
+  if (e == cudaSuccess) e = cudaMemset(st->zero, 0, 4096);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->e_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->e_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st->h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st->comp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st->d2h, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete st;
+    return cuda_err(e, "stager setup");
+  }
+  *out = st;
+  return LLAMA_OK;
+}
+
+void llama_stager_destroy(llama_stager* st) { delete st; }
+
+llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
+                               const llama_mapping* dst_map, void* const* dst_blobs, void* stream) {
+  if (!st || !src_map || !dst_map || !src_blobs || !dst_blobs)
+    return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    const llb::Mapping& s = src_map->m;
+    const llb::Mapping& d = dst_map->m;
+    if (s.types != d.types) return llb::set_error(LLAMA_ERR_RECORD_MISMATCH, "record dimensions differ");
+    if (s.extents != d.extents) return llb::set_error(LLAMA_ERR_SHAPE_MISMATCH, "array extents differ");
+    for (int b = 0; b < s.nblobs(); ++b)
+      if (s.blob_sizes[b] && !src_blobs[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL src blob");
+    for (int b = 0; b < d.nblobs(); ++b)
+      if (d.blob_sizes[b] && !dst_blobs[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL dst blob");
+    const uint64_t N = s.N;
+    if (d.footprint_bytes() == 0) return LLAMA_OK;
+
+    // slab unit: whole blocks of every blocked side (lcm of the lane counts)
+    uint64_t unit = 1;
+    for (const llb::Mapping* m : {&s, &d})
+      if (!m->soa()) unit = unit / gcd64(unit, m->L) * m->L;
+    // slab size from the per-record footprint, then shrunk until both 1-D
+    // views fit one staging buffer
+    const uint64_t per = std::max<uint64_t>(1, std::max(s.footprint_bytes(), d.footprint_bytes()) / std::max<uint64_t>(N, 1));
+    uint64_t n = std::max<uint64_t>(unit, st->cap / per / unit * unit);
+    if (n > N) n = (N + unit - 1) / unit * unit;
+    std::vector<uint64_t> lbs, lbd;
+    for (;;) {
+      const uint64_t nn = std::min(n, N);
+      llama_mapping* ls = st->view(src_map, nn);
+      llama_mapping* ld = st->view(dst_map, nn);
+      if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
+      if (layout_local(ls->m, &lbs) <= st->cap && layout_local(ld->m, &lbd) <= st->cap) break;
+      if (n <= unit) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "one slab of whole AoSoA blocks exceeds the staging buffer");
+      n = std::max(unit, (n / 2) / unit * unit);
+    }
+
+    cudaError_t e = cudaEventRecord(st->e_start, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->h2d, st->e_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->comp, st->e_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->d2h, st->e_start, 0);
+    if (e != cudaSuccess) return cuda_err(e, "stream ordering");
+
+    // destination padding outside every slab range: gaps between aligned
+    // SoA single-blob sub-arrays (reading #9) -> zero them from the device
+    if (d.kind == LLAMA_SOA_SINGLE_BLOB && d.aligned) {
+      uint64_t end = 0;
+      for (int k = 0; k < d.K(); ++k) {
+        if (d.base[k] > end) {
+          e = cudaMemcpyAsync(static_cast<uint8_t*>(dst_blobs[0]) + end, st->zero, d.base[k] - end,
+                              cudaMemcpyDefault, st->d2h);
+          if (e != cudaSuccess) return cuda_err(e, "gap fill");
+        }
+        end = d.base[k] + d.N * d.sizes[k];
+      }
+    }
+
+    std::vector<Range> rs, rd;
+    uint64_t c = 0;
+    for (uint64_t a = 0; a < N; a += n, ++c) {
+      const uint64_t b = std::min(N, a + n);
+      const int j = (int)(c % kNB);
+      llama_mapping* ls = st->view(src_map, b - a);
+      llama_mapping* ld = st->view(dst_map, b - a);
+      if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
+      layout_local(ls->m, &lbs);
+      layout_local(ld->m, &lbd);
+      slab_ranges(s, ls->m, a, b, &rs);
+      slab_ranges(d, ld->m, a, b, &rd);
+      // h2d: buffer j is free once the slab that used it has gone back out
+      if (c >= (uint64_t)kNB && (e = cudaStreamWaitEvent(st->h2d, st->e_out[j], 0)) != cudaSuccess)
+        return cuda_err(e, "h2d wait");
+      for (const Range& r : rs) {
+        e = cudaMemcpyAsync(st->buf[j][0] + lbs[r.lblob] + r.loff,
+                            static_cast<const uint8_t*>(src_blobs[r.gblob]) + r.goff, r.len, cudaMemcpyDefault,
+                            st->h2d);
+        if (e != cudaSuccess) return cuda_err(e, "h2d copy");
+      }
+      if ((e = cudaEventRecord(st->e_in[j], st->h2d)) != cudaSuccess) return cuda_err(e, "h2d event");
+      // relayout of the slab's 1-D views in staging memory
+      if ((e = cudaStreamWaitEvent(st->comp, st->e_in[j], 0)) != cudaSuccess) return cuda_err(e, "comp wait");
+      std::vector<void*> ps(ls->m.nblobs()), pd(ld->m.nblobs());
+      for (int q = 0; q < ls->m.nblobs(); ++q) ps[q] = st->buf[j][0] + lbs[q];
+      for (int q = 0; q < ld->m.nblobs(); ++q) pd[q] = st->buf[j][1] + lbd[q];
+      llama_status cs = llama_copy(ls, ps.data(), ld, pd.data(), st->comp);
+      if (cs != LLAMA_OK) return cs;
+      if ((e = cudaEventRecord(st->e_comp[j], st->comp)) != cudaSuccess) return cuda_err(e, "comp event");
+      // d2h
+      if ((e = cudaStreamWaitEvent(st->d2h, st->e_comp[j], 0)) != cudaSuccess) return cuda_err(e, "d2h wait");
+      for (const Range& r : rd) {
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(dst_blobs[r.gblob]) + r.goff, st->buf[j][1] + lbd[r.lblob] + r.loff,
+                            r.len, cudaMemcpyDefault, st->d2h);
+        if (e != cudaSuccess) return cuda_err(e, "d2h copy");
+      }
+      if ((e = cudaEventRecord(st->e_out[j], st->d2h)) != cudaSuccess) return cuda_err(e, "d2h event");
+    }
+    if ((e = cudaEventRecord(st->e_done, st->d2h)) != cudaSuccess) return cuda_err(e, "done event");
+    if ((e = cudaStreamWaitEvent((cudaStream_t)stream, st->e_done, 0)) != cudaSuccess) return cuda_err(e, "join");
+    return LLAMA_OK;
+  } catch (...) {
+    return llb::set_error(LLAMA_ERR_OOM, "staged copy failed");
+  }
+}
+
+}  // extern "C"
