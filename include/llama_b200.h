@@ -175,6 +175,7 @@ typedef struct {
   int32_t tma;              /* PERMUTE: 1 if every segment is moved by TMA bulk copies */
   uint64_t src_bytes;       /* sum of source blob sizes */
   uint64_t dst_bytes;       /* sum of destination blob sizes */
+  int32_t word_moves;       /* PERMUTE: > 0 if AoS <-> AoS word mode is used (words per record) */
 } llama_plan_info;
 
 llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_map,

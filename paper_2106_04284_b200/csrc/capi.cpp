@@ -167,6 +167,7 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
       out->smem_bytes = plan->smem_bytes;
       out->moves = (int32_t)plan->perm->n_moves;
       out->tma = (int32_t)plan->perm->tma;
+      out->word_moves = (int32_t)plan->perm->n_wmoves;
     }
     return LLAMA_OK;
   } catch (...) {

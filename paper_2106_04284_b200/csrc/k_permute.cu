@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
   for (uint32_t o = 16 * tid; o < p.nd * p.dst_stage; o += 16 * kThreads)
     *reinterpret_cast<uint4*>(dbuf + o) = make_uint4(0, 0, 0, 0);
   build_seg_tables(p, sseg, dseg, tid, kThreads);
+  WordMove* wt = word_table(smem + kBarBytes, p);
+  copy_word_table(p, wt, tid, kThreads);
   if (kTma && tid == 0) {
     for (uint32_t s = 0; s < p.ns; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
-    permute_records(p, simg, dimg, nrec, tid);
+    permute_records(p, wt, simg, dimg, nrec, tid);
     if (kTma) fence_proxy_async_smem();
     __syncthreads();
 

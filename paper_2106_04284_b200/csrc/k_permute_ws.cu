@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
   for (uint32_t o = 16 * tid; o < p.nd * p.dst_stage; o += 16 * kThreadsWS)
     *reinterpret_cast<uint4*>(dbuf + o) = make_uint4(0, 0, 0, 0);
   build_seg_tables(p, sseg, dseg, tid, kThreadsWS);
+  WordMove* wt = word_table(smem + kBarBytes, p);
+  copy_word_table(p, wt, tid, kThreadsWS);
   if (tid == 0) {
     for (uint32_t s = 0; s < p.ns; ++s) {
       mbar_init(&full[s], 1);
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       named_sync_consumers();
     }
-    permute_records(p, simg, dimg, nrec, tid);
+    permute_records(p, wt, simg, dimg, nrec, tid);
     if (!fl) {  // destination tails (sub-16-byte) go out directly
       named_sync_consumers();
       for (int j = 0; j < n_segs(p, 1); ++j) {

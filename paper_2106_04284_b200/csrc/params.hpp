@@ -129,6 +129,16 @@ struct Move {        // one unit move of the per-record permutation
   uint8_t pad_;
 };
 
+// Word move (AoS <-> AoS word mode): destination word doff of a record is
+// built from the 12-byte source window at soff (4-aligned):
+//   t = prmt(w0, w1, sel1); v = prmt(t, w2, sel2) & mask   (w2 read only if sel2 != 0x3210)
+struct WordMove {
+  uint16_t doff, soff;
+  uint16_t sel1, sel2;
+  uint32_t mask;
+};
+constexpr int kMaxWordMoves = 128;  // 4 per lane
+
 struct MoveClass {    // moves [m0, m1) share unit and leaf size
   uint32_t m0, m1;
   uint32_t unit, size;
@@ -149,6 +159,8 @@ struct PermParams {
   uint32_t unit_end[4];   // moves [0,unit_end[0]) are 8-B units, then 4-, 2-, 1-B units
   uint32_t n_classes;
   MoveClass classes[kMaxClasses];
+  uint32_t n_wmoves;     // > 0: AoS <-> AoS word mode (move-parallel) instead of the move classes
+  WordMove wmoves[kMaxWordMoves];
   uint32_t tab_bytes;     // shared-memory bytes of the segment tables (16-B multiple)
   uint32_t pad2_;
   PermSide side[2];   // 0 = src, 1 = dst

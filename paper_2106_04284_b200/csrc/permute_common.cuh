@@ -178,10 +178,58 @@ __device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t*
   }
 }
 
+// AoS <-> AoS word mode: lane j owns destination words j, j+32, ... of a
+// record (table in registers); warps take records in turn.  Both images are
+// accessed as consecutive words within a record: no bank conflicts at any
+// record stride (the 480-B aligned HEP record gives 8-way conflicts in the
+// record-parallel mapping).
+// (table: the per-CTA shared copy, see word_table())
+__device__ __forceinline__ void permute_words(const PermParams& p, const WordMove* __restrict__ wt,
+                                              const uint8_t* __restrict__ simg, uint8_t* __restrict__ dimg,
+                                              uint32_t nrec, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  WordMove w[4];
+  bool has[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t m = lane + 32 * i;
+    has[i] = m < p.n_wmoves;
+    w[i] = has[i] ? wt[m] : WordMove{0, 0, 0x3210, 0x3210, 0};
+  }
+  const uint32_t Bs = p.side[0].Bimg, Bd = p.side[1].Bimg;
+  for (uint32_t r = warp; r < nrec; r += kPermThreads / 32) {
+    const uint8_t* sr = simg + r * Bs;
+    uint8_t* dr = dimg + r * Bd;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!has[i]) continue;
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(sr + w[i].soff);
+      const uint32_t b = *reinterpret_cast<const uint32_t*>(sr + w[i].soff + 4);
+      uint32_t v = __byte_perm(a, b, w[i].sel1);
+      if (w[i].sel2 != 0x3210) v = __byte_perm(v, *reinterpret_cast<const uint32_t*>(sr + w[i].soff + 8), w[i].sel2);
+      *reinterpret_cast<uint32_t*>(dr + w[i].doff) = v & w[i].mask;
+    }
+  }
+}
+
 // The whole tile, threads tid in [0, 256): T <= 256 or a multiple of 256
 // (planner), in passes of 4, 2 or 1 x 256 records.
-__device__ __forceinline__ void permute_records(const PermParams& p, const uint8_t* simg, uint8_t* dimg,
-                                                uint32_t nrec, int tid) {
+// Per-CTA shared copy of the word-move table: it lives after the segment
+// tables (lane-indexed reads of the parameter bank would serialise).
+__device__ __forceinline__ WordMove* word_table(uint8_t* tables, const PermParams& p) {
+  return reinterpret_cast<WordMove*>(tables + ((2u * 32u * p.K + 15u) & ~15u));
+}
+
+__device__ __forceinline__ void copy_word_table(const PermParams& p, WordMove* wt, int tid, int nt) {
+  for (uint32_t m = tid; m < p.n_wmoves; m += nt) wt[m] = p.wmoves[m];
+}
+
+__device__ __forceinline__ void permute_records(const PermParams& p, const WordMove* wt, const uint8_t* simg,
+                                                uint8_t* dimg, uint32_t nrec, int tid) {
+  if (p.n_wmoves) {
+    permute_words(p, wt, simg, dimg, nrec, tid);
+    return;
+  }
   uint32_t r0 = 0;
   for (; r0 + 4 * kPermThreads <= p.T; r0 += 4 * kPermThreads) permute_pass<4>(p, simg, dimg, nrec, r0, tid);
   if (r0 + 2 * kPermThreads <= p.T) {

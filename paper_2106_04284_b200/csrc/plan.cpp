@@ -316,7 +316,43 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     }
     pp.unit_end[c] = nm;
   }
-  pp.tab_bytes = (uint32_t)align16(2ull * 32 * s.K());  // SSeg tables (24 B each, padded)
+  // AoS <-> AoS word mode for wide records (both sides plain AoS, strides
+  // multiples of 4, >= 64 destination words per record): each destination
+  // word is built from a <= 12-byte source window; lanes own words, so both
+  // images are read/written contiguously (no bank conflicts at any stride).
+  pp.n_wmoves = 0;
+  if (!soa_like[0] && !soa_like[1] && s.L == 1 && d.L == 1 && s.B % 4 == 0 && d.B % 4 == 0 &&
+      env_u64("LLAMA_WORD_MODE", 1)) {
+    std::vector<int64_t> src_of(d.B, -1);
+    for (int k = 0; k < s.K(); ++k)
+      for (uint32_t b = 0; b < s.sizes[k]; ++b) src_of[d.F[k] + b] = (int64_t)(s.F[k] + b);
+    std::vector<WordMove> wm;
+    bool ok = true;
+    for (uint64_t w = 0; w < d.B / 4 && ok; ++w) {
+      int64_t lo = -1;
+      for (int b = 0; b < 4; ++b)
+        if (src_of[4 * w + b] >= 0 && (lo < 0 || src_of[4 * w + b] < lo)) lo = src_of[4 * w + b];
+      if (lo < 0) continue;  // all padding: the zeroed image already holds it
+      const int64_t ws = lo & ~3ll;
+      uint32_t sel1 = 0, sel2 = 0, mask = 0;
+      for (int b = 0; b < 4; ++b) {
+        const int64_t q = src_of[4 * w + b];
+        const int64_t idx = q < 0 ? 0 : q - ws;
+        if (idx > 11) { ok = false; break; }
+        if (q >= 0) mask |= 0xFFu << (8 * b);
+        sel1 |= (uint32_t)(idx < 8 ? idx : 0) << (4 * b);
+        sel2 |= (uint32_t)(idx < 8 ? b : 4 + (idx - 8)) << (4 * b);
+      }
+      wm.push_back(WordMove{(uint16_t)(4 * w), (uint16_t)ws, (uint16_t)sel1, (uint16_t)sel2, mask});
+    }
+    if (ok && wm.size() >= 64 && wm.size() <= (size_t)kMaxWordMoves && d.B < 65536 && s.B < 65536) {
+      pp.n_wmoves = (uint32_t)wm.size();
+      for (size_t j = 0; j < wm.size(); ++j) pp.wmoves[j] = wm[j];
+    }
+  }
+  // SSeg tables (24 B each, padded) + the word-move table copy
+  pp.tab_bytes = (uint32_t)(align16(2ull * 32 * s.K()) + align16(sizeof(WordMove) * pp.n_wmoves));
+  if (pp.n_wmoves) pp.src_stage += 16;  // word windows may read up to 8 B past a tile's last record
   pp.nd = 2;
   uint64_t smem = 0;
   const uint64_t per_rec = rec_img[0] + rec_img[1];
