@@ -58,6 +58,12 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
     fence_mbar_init();
   }
   __syncthreads();
+  // Programmatic dependent launch: everything above touched only shared
+  // memory and parameters, so it overlapped the previous grid's tail; global
+  // memory is used only after that grid has completed.  Dependents may be
+  // scheduled at once (they occupy SMs only as this grid's CTAs retire).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (blockIdx.x == 0 && warp < kConsumerWarps)
     for (uint32_t g = 0; g < p.n_gaps; ++g)
@@ -168,9 +174,23 @@ int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
   if (e) return e;
   uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
   if (grid > p.n_tiles) grid = p.n_tiles;
-  k_permute_ws<<<(unsigned)grid, kThreadsWS, smem_bytes, (cudaStream_t)stream>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreadsWS);
+  cfg.dynamicSmemBytes = (size_t)smem_bytes;
+  cfg.stream = (cudaStream_t)stream;
+  static const bool no_pdl = [] {
+    const char* e = std::getenv("LLAMA_NO_PDL");
+    return e && *e == '1';
+  }();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, k_permute_ws, p);
   count_launch();
-  return (int)cudaGetLastError();
+  return le != cudaSuccess ? (int)le : (int)cudaGetLastError();
 }
 
 int launch_permute(const PermParams& p, int smem_bytes, void* stream) {

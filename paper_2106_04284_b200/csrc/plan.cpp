@@ -409,9 +409,9 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       // the warp-specialised TMA permute measured fastest on B200 for every
       // pair it applies to -- identities (6.25-6.40 vs 6.14-6.20 TB/s for the
       // bulk blob copy) and run pairs (SoA <-> AoSoA) included
-      // identities of SoA layouts (many blobs / segments): the bulk blob copy
+      // identities of SoA layouts with many leaves (many blobs / segments): the bulk blob copy
       // (HEP SoA MB: 6.4 TB/s vs 1.8 for 200 TMA segment ops per tile)
-      if (s.soa() && plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
       if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
       if (plan_run(s, d, out, &why)) return LLAMA_OK;

@@ -140,8 +140,8 @@ def test_planner_choices_c2():
         s = llama.Mapping(W.PARTICLE7, (1000,), *W.MAPPINGS[name])
         d = llama.Mapping(W.PARTICLE7, (1000,), *W.MAPPINGS[name])
         assert llama.plan(s, d, path="blobcopy")["path"] == "blobcopy"
-    assert _plan("soa_mb", "soa_mb")["path"] == "blobcopy"  # SoA identity: bulk copy
-    for a, b in [("aos", "aos"), ("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos"),
+    assert _plan("soa_mb", "soa_mb", W.HEP100, (1 << 20,))["path"] == "blobcopy"  # many-leaf SoA identity
+    for a, b in [("aos", "aos"), ("soa_mb", "soa_mb"), ("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aosoa8"), ("aosoa32", "aos"),
                  ("aosoa8", "aosoa32"), ("soa_mb", "aosoa8"), ("aosoa32", "soa_mb")]:
         p = _plan(a, b)
         assert p["path"] == "permute" and p["tma"] and p["tile_records"] % 32 == 0
