@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3}
+KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3, "one": 4, "split": 5}
 
 
 def build(force=False):
@@ -36,7 +36,10 @@ def build(force=False):
 
 
 class _CMapping(ctypes.Structure):
-    _fields_ = [
+    pass
+
+
+_CMapping._fields_ = [
         ("n_leaves", ctypes.c_int32),
         ("leaf_size", ctypes.POINTER(ctypes.c_int32)),
         ("rank", ctypes.c_int32),
@@ -44,6 +47,10 @@ class _CMapping(ctypes.Structure):
         ("kind", ctypes.c_int32),
         ("lanes", ctypes.c_int64),
         ("aligned", ctypes.c_int32),
+        ("inner_a", ctypes.POINTER(_CMapping)),
+        ("inner_b", ctypes.POINTER(_CMapping)),
+        ("leaves_a", ctypes.POINTER(ctypes.c_int32)),
+        ("n_a", ctypes.c_int32),
     ]
 
 
@@ -116,7 +123,33 @@ class Mapping:
         if lib().oracle_validate(ctypes.byref(self.c)) != 0:
             raise ValueError(f"invalid oracle mapping {kind} {self.sizes} {self.extents}")
 
+    @classmethod
+    def split(cls, schema, leaves_a, a, b):
+        """Split: the leaves of the full record listed in
+        leaves_a (increasing) are mapped by a, the others by b; a and b are
+        mappings of those sub-records over the same extents."""
+        self = cls.__new__(cls)
+        self.schema = schema if isinstance(schema, str) else None
+        self.sizes = leaf_sizes(schema) if isinstance(schema, str) else [int(s) for s in schema]
+        self.extents = list(a.extents)
+        self.kind_name = "split"
+        self.lanes = 1
+        self.aligned = False
+        self.inner = (a, b)
+        self.leaves_a = [int(k) for k in leaves_a]
+        self._sizes_c = (ctypes.c_int32 * len(self.sizes))(*self.sizes)
+        self._ext_c = (ctypes.c_int64 * len(self.extents))(*self.extents)
+        self._la_c = (ctypes.c_int32 * max(1, len(self.leaves_a)))(*self.leaves_a)
+        self.c = _CMapping(len(self.sizes), self._sizes_c, len(self.extents), self._ext_c,
+                           KINDS["split"], 1, 0, ctypes.pointer(a.c), ctypes.pointer(b.c),
+                           self._la_c, len(self.leaves_a))
+        if lib().oracle_validate(ctypes.byref(self.c)) != 0:
+            raise ValueError(f"invalid oracle split {self.sizes} leaves_a={self.leaves_a}")
+        return self
+
     def __repr__(self):
+        if self.kind_name == "split":
+            return f"oracle.Split({self.leaves_a}: {self.inner[0]!r} | {self.inner[1]!r})"
         return f"oracle.Mapping({self.kind_name}, L={self.lanes}, aligned={self.aligned}, ext={self.extents})"
 
     @property
@@ -164,6 +197,21 @@ class Mapping:
 
     def alloc(self, fill=0):
         return [np.full(s, fill, dtype=np.uint8) for s in self.blob_sizes()]
+
+
+def mapping_from_spec(schema_or_sizes, extents, spec):
+    """A mapping from a workloads.MAPPINGS tuple (kind, lanes, aligned) or a
+    split tree (leaves_a, part_a, part_b) whose parts are such tuples or trees
+    (P:479-481); `resolve` names are looked up by the caller."""
+    sizes = leaf_sizes(schema_or_sizes) if isinstance(schema_or_sizes, str) else list(schema_or_sizes)
+    if len(spec) == 3 and isinstance(spec[0], str):
+        kind, lanes, aligned = spec
+        return Mapping(sizes, extents, kind, lanes, aligned)
+    leaves_a, spec_a, spec_b = spec
+    sel = set(leaves_a)
+    a = mapping_from_spec([sizes[k] for k in leaves_a], extents, spec_a)
+    b = mapping_from_spec([sizes[k] for k in range(len(sizes)) if k not in sel], extents, spec_b)
+    return Mapping.split(sizes, leaves_a, a, b)
 
 
 def splitmix64(x):

@@ -18,8 +18,44 @@ int oracle_validate(const oracle_mapping* m) {
   }
   for (int32_t d = 0; d < m->rank; ++d)
     if (m->extents[d] < 0) return -1;
-  if (m->kind < ORACLE_AOS || m->kind > ORACLE_AOSOA) return -1;
+  if (m->kind < ORACLE_AOS || m->kind > ORACLE_SPLIT) return -1;
   if (m->kind == ORACLE_AOSOA && m->lanes < 1) return -1; /* S:238-240 */
+  if (m->kind == ORACLE_SPLIT) {
+    /* S:296-300: inner_a maps the selected leaves, inner_b the rest; both
+     * over the same extents; neither part may be empty (S:303). */
+    const oracle_mapping* a = m->inner_a;
+    const oracle_mapping* b = m->inner_b;
+    if (!a || !b || !m->leaves_a || m->n_a < 1 || m->n_a >= m->n_leaves) return -1;
+    if (oracle_validate(a) || oracle_validate(b)) return -1;
+    if (a->n_leaves != m->n_a || b->n_leaves != m->n_leaves - m->n_a) return -1;
+    if (a->rank != m->rank || b->rank != m->rank) return -1;
+    for (int32_t d = 0; d < m->rank; ++d)
+      if (a->extents[d] != m->extents[d] || b->extents[d] != m->extents[d]) return -1;
+    int32_t ja = 0, jb = 0;
+    for (int32_t k = 0; k < m->n_leaves; ++k) {
+      if (ja < m->n_a && m->leaves_a[ja] == k) {
+        if (a->leaf_size[ja] != m->leaf_size[k]) return -1;
+        ++ja;
+      } else {
+        if (b->leaf_size[jb] != m->leaf_size[k]) return -1;
+        ++jb;
+      }
+    }
+    if (ja != m->n_a) return -1; /* leaves_a not increasing or out of range */
+  }
+  return 0;
+}
+
+/* Split (S:299): which part leaf k of a split belongs to (1 = inner_a) and
+ * its leaf index inside that part (the coordinate re-indexed into the part). */
+static int split_part(const oracle_mapping* m, int32_t k, int32_t* j) {
+  int32_t ja = 0, jb = 0;
+  for (int32_t q = 0; q < k; ++q) {
+    if (ja < m->n_a && m->leaves_a[ja] == q) ++ja;
+    else ++jb;
+  }
+  if (ja < m->n_a && m->leaves_a[ja] == k) { *j = ja; return 1; }
+  *j = jb;
   return 0;
 }
 
@@ -89,6 +125,8 @@ static uint64_t soa_sb_starts(const oracle_mapping* m, uint64_t* starts) {
 
 /* "a compile time blob count". */
 int32_t oracle_blob_count(const oracle_mapping* m) {
+  /* a split's blobs are inner_a's followed by inner_b's */
+  if (m->kind == ORACLE_SPLIT) return oracle_blob_count(m->inner_a) + oracle_blob_count(m->inner_b);
   return m->kind == ORACLE_SOA_MB ? m->n_leaves : 1; /* SoA MB blobCount = leafCount */
 }
 
@@ -112,6 +150,13 @@ void oracle_blob_sizes(const oracle_mapping* m, uint64_t* sizes) {
       sizes[0] = blocks * L * record_offsets(m, NULL);
       break;
     }
+    case ORACLE_ONE: /* blobSize(0) = sizeOfAligned(dim), whatever the extents */
+      sizes[0] = oracle_aligned_offsets(m, NULL);
+      break;
+    case ORACLE_SPLIT: /* inner_a's blob sizes, then inner_b's */
+      oracle_blob_sizes(m->inner_a, sizes);
+      oracle_blob_sizes(m->inner_b, sizes + oracle_blob_count(m->inner_a));
+      break;
   }
 }
 
@@ -121,6 +166,9 @@ void oracle_blob_sizes(const oracle_mapping* m, uint64_t* sizes) {
  *   SoA MB: blob k, off = i*s_k
  *   SoA SB:     blob 0, off = start_k + i*s_k
  *   AoSoA L: blob 0, off = (i/L)*L*S + offsetOf(k)*L + (i%L)*s_k
+ *   One: blob 0, off = offsetOf_aligned(k), for every i
+ *   Split: the part's own answer for the re-indexed
+ *             leaf, blob number + blobCount(inner_a) for the inner_b part
  * where S / offsetOf are the packed or aligned record layout. */
 int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
                               int32_t* blob, uint64_t* offset) {
@@ -159,6 +207,21 @@ int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
       free(offs);
       return 0;
     }
+    case ORACLE_ONE: {
+      uint64_t* offs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)m->n_leaves);
+      oracle_aligned_offsets(m, offs);
+      *blob = 0;
+      *offset = offs[k]; /* independent of i */
+      free(offs);
+      return 0;
+    }
+    case ORACLE_SPLIT: {
+      int32_t j;
+      if (split_part(m, k, &j)) return oracle_blob_nr_and_offset(m->inner_a, i, j, blob, offset);
+      int rc = oracle_blob_nr_and_offset(m->inner_b, i, j, blob, offset);
+      *blob += oracle_blob_count(m->inner_a);
+      return rc;
+    }
   }
   return -1;
 }
@@ -166,26 +229,64 @@ int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
 /* A faster, equivalent evaluation of oracle_blob_nr_and_offset for the copy
  * loops: the per-leaf record offsets / sub-array starts are computed once
  * instead of per call.  The arithmetic per kind is the same as above. */
-typedef struct {
+typedef struct addr_ctx {
   const oracle_mapping* m;
   uint64_t S;
-  uint64_t* offs;   /* record offsets (AoS/AoSoA) or sub-array starts (SoA SB) */
+  uint64_t* offs;   /* record offsets (AoS/AoSoA/One) or sub-array starts (SoA SB) */
+  /* split: per leaf its part (1 = inner_a) and index in the part */
+  struct addr_ctx* a;
+  struct addr_ctx* b;
+  int32_t* part;
+  int32_t* idx;
+  int32_t blobs_a;
 } addr_ctx;
 
 static void addr_ctx_init(addr_ctx* c, const oracle_mapping* m) {
   c->m = m;
   c->offs = (uint64_t*)calloc((size_t)m->n_leaves, sizeof(uint64_t));
   c->S = 0;
+  c->a = c->b = NULL;
+  c->part = c->idx = NULL;
+  c->blobs_a = 0;
   if (m->kind == ORACLE_AOS || m->kind == ORACLE_AOSOA) c->S = record_offsets(m, c->offs);
   if (m->kind == ORACLE_SOA_SB) soa_sb_starts(m, c->offs);
+  if (m->kind == ORACLE_ONE) c->S = oracle_aligned_offsets(m, c->offs);
+  if (m->kind == ORACLE_SPLIT) {
+    c->a = (addr_ctx*)malloc(sizeof(addr_ctx));
+    c->b = (addr_ctx*)malloc(sizeof(addr_ctx));
+    addr_ctx_init(c->a, m->inner_a);
+    addr_ctx_init(c->b, m->inner_b);
+    c->part = (int32_t*)malloc(sizeof(int32_t) * (size_t)m->n_leaves);
+    c->idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)m->n_leaves);
+    for (int32_t k = 0; k < m->n_leaves; ++k) c->part[k] = split_part(m, k, &c->idx[k]);
+    c->blobs_a = oracle_blob_count(m->inner_a);
+  }
 }
 
-static void addr_ctx_free(addr_ctx* c) { free(c->offs); }
+static void addr_ctx_free(addr_ctx* c) {
+  free(c->offs);
+  if (c->a) { addr_ctx_free(c->a); free(c->a); }
+  if (c->b) { addr_ctx_free(c->b); free(c->b); }
+  free(c->part);
+  free(c->idx);
+}
 
 static void addr_of(const addr_ctx* c, uint64_t i, int32_t k, int32_t* blob, uint64_t* offset) {
   const oracle_mapping* m = c->m;
   uint64_t s_k = (uint64_t)m->leaf_size[k];
   switch (m->kind) {
+    case ORACLE_ONE:
+      *blob = 0;
+      *offset = c->offs[k];
+      return;
+    case ORACLE_SPLIT:
+      if (c->part[k]) {
+        addr_of(c->a, i, c->idx[k], blob, offset);
+      } else {
+        addr_of(c->b, i, c->idx[k], blob, offset);
+        *blob += c->blobs_a;
+      }
+      return;
     case ORACLE_AOS:
       *blob = 0;
       *offset = i * c->S + c->offs[k];

@@ -14,7 +14,7 @@
  *   for every array index i (row-major) and every leaf k (DFS order,
  *   P:296-309): dst[blob_d(i,k)][off_d(i,k) .. +s_k) = src[blob_s(i,k)][off_s(i,k) .. +s_k)
  * where (blob, off) is the mapping's blobNrAndOffset (§3.7), written
- * out per mapping kind directly from the definitions (P:460-473, S:244-286);
+ * out per mapping kind directly from the definitions (P:460-481, S:244-304);
  * destination padding bytes are written as 0 (reading #12).
  *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py
@@ -29,13 +29,18 @@
 extern "C" {
 #endif
 
-/* Mapping kinds (P:459-473). */
-enum { ORACLE_AOS = 0, ORACLE_SOA_SB = 1, ORACLE_SOA_MB = 2, ORACLE_AOSOA = 3 };
+/* Mapping kinds (P:459-481). */
+enum { ORACLE_AOS = 0, ORACLE_SOA_SB = 1, ORACLE_SOA_MB = 2, ORACLE_AOSOA = 3, ORACLE_ONE = 4, ORACLE_SPLIT = 5 };
 
 /* A mapping as the oracle sees it: the flattened leaf sizes (DFS order; each
  * leaf's alignment equals its size), the array extents (row-major),
- * the kind, the AoSoA lane count L (ignored otherwise) and packed/aligned. */
-typedef struct {
+ * the kind, the AoSoA lane count L (ignored otherwise) and packed/aligned.
+ * ORACLE_ONE always uses the aligned record layout.
+ * ORACLE_SPLIT: the leaves listed in leaves_a[0..n_a)
+ * (increasing) are mapped by inner_a -- a mapping of just those leaves, in
+ * order -- and the others by inner_b; the other fields of a split describe
+ * the full record (leaf sizes, extents); lanes / aligned are ignored. */
+typedef struct oracle_mapping {
   int32_t n_leaves;
   const int32_t* leaf_size; /* bytes, each in {1,2,4,8} */
   int32_t rank;
@@ -43,6 +48,10 @@ typedef struct {
   int32_t kind;
   int64_t lanes;
   int32_t aligned; /* 0 = tightly packed, 1 = natural alignment */
+  const struct oracle_mapping* inner_a; /* ORACLE_SPLIT only */
+  const struct oracle_mapping* inner_b;
+  const int32_t* leaves_a;
+  int32_t n_a;
 } oracle_mapping;
 
 /* Returns 0 if the mapping is well formed, -1 otherwise. */

@@ -37,6 +37,22 @@ MAPPINGS = {
     "aosoa4": ("aosoa", 4, False),
     "aosoa8": ("aosoa", 8, False),
     "aosoa32": ("aosoa", 32, False),
+    "one": ("one", 1, True),             # One: always the aligned record
+}
+
+# Split mappings, per schema: (leaves_a, part_a, part_b), where a
+# part is a MAPPINGS name or a nested split of that part's leaves; leaves_a
+# index the (sub-)record's DFS leaf list.
+SPLITS = {
+    # Listing-1 Particle, Pos -> SoA MB, the rest packed AoS
+    "split_pos": ("listing1", ([1, 2], "soa_mb", "aos")),
+    # Listing P:499-509 (MappingC): Pos -> SoA MB; of the rest {Id, Mass,
+    # Flags[3]}, Mass -> One and {Id, Flags[3]} -> aligned AoS
+    "mapping_c": ("listing1", ([1, 2], "soa_mb", ([1], "one", "aos_aligned"))),
+    # Particle7: Pos -> SoA MB, {Vel, Mass} -> AoSoA8 (the hot/cold split of P:479)
+    "split_p7": ("particle7", ([0, 1, 2], "soa_mb", "aosoa8")),
+    # HEP100: the 4-momenta of all 10 objects -> SoA MB, the rest aligned AoS
+    "split_hep": ("hep100", ([g * 10 + j for g in range(10) for j in range(4)], "soa_mb", "aos_aligned")),
 }
 
 SEEDS = (42, 1, 2)  # seed 42 default
@@ -52,3 +68,16 @@ C3 = dict(name="C3", schema="hep100", extents=(67_108_864,),
 C4 = dict(name="C4", schema="listing1", extents=(8192, 8192), pairs=[("aosoa32", "soa_sb")])
 C5 = dict(name="C5", schema="particle7", extents=(1 << 27,), pairs=[("aos", "soa_mb")])
 CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5}
+
+
+def resolve_spec(spec):
+    """A MAPPINGS name / split tree with MAPPINGS names -> the same tree with
+    (kind, lanes, aligned) tuples at the leaves (no layout arithmetic)."""
+    if isinstance(spec, str):
+        if spec in SPLITS:
+            return resolve_spec(SPLITS[spec][1])
+        return MAPPINGS[spec]
+    if len(spec) == 3 and isinstance(spec[0], str):
+        return spec
+    leaves_a, a, b = spec
+    return (list(leaves_a), resolve_spec(a), resolve_spec(b))
