@@ -63,7 +63,9 @@ typedef enum {
   LLAMA_AOS = 0,             /* P:460-463 fields after each other, repeated per record */
   LLAMA_SOA_SINGLE_BLOB = 1, /* P:465-468 one sub-array per leaf, all in one blob */
   LLAMA_SOA_MULTI_BLOB = 2,  /* P:465-468 one blob per leaf ("SoA MB") */
-  LLAMA_AOSOA = 3            /* P:470-473 AoS of blocks that repeat each field L times */
+  LLAMA_AOSOA = 3,           /* P:470-473 AoS of blocks that repeat each field L times */
+  LLAMA_ONE = 4,             /* P:475-477 the whole array collapsed onto one (aligned) record */
+  LLAMA_SPLIT = 5            /* P:479-481 composite, from llama_mapping_create_split only */
 } llama_kind;
 
 /* A mapping description (a mapping is configured on the array and
@@ -108,6 +110,17 @@ llama_status llama_mapping_create_from_schema(const char* schema, const int64_t*
                                               int32_t rank, llama_kind kind, int64_t lanes,
                                               int32_t aligned, llama_mapping** out);
 
+/* Split mapping (Listing P:499-509): the leaves
+ * leaves_a[0..n_a) (strictly increasing indices into the full record's DFS
+ * leaf list) are mapped by `a`, the remaining leaves by `b`; a and b are
+ * mappings of those sub-records (in leaf order) over the same extents.  The
+ * split's blobs are a's blobs followed by b's.  a and b may themselves be
+ * splits; they are copied, so they may be destroyed afterwards.
+ * Errors: INVALID_ARGUMENT (NULL, bad leaf list, leaf count or extents that
+ * do not add up), UNSUPPORTED (more than LLAMA_MAX_BLOBS blobs). */
+llama_status llama_mapping_create_split(const llama_mapping* a, const llama_mapping* b, const int32_t* leaves_a,
+                                        int32_t n_a, llama_mapping** out);
+
 /* Destroys a mapping; NULL-safe.  Plans cached for pairs involving it are
  * released. */
 void llama_mapping_destroy(llama_mapping* m);
@@ -143,7 +156,9 @@ llama_status llama_blob_nr_and_offset(const llama_mapping* m, const int64_t* ind
  * (reading #12).  Source padding never influences the result.
  * Errors (synchronous, before any launch): RECORD_MISMATCH, SHAPE_MISMATCH,
  * INVALID_ARGUMENT (NULL mapping/pointer array/pointer), ALIGNMENT, OVERLAP,
- * UNSUPPORTED; CUDA on a launch failure. */
+ * UNSUPPORTED (also: a destination that maps several records onto one
+ * location, e.g. a One leaf with more than one record -- the result would
+ * depend on the order of the writes); CUDA on a launch failure. */
 llama_status llama_copy(const llama_mapping* src_map, void* const* src_blobs,
                         const llama_mapping* dst_map, void* const* dst_blobs, void* stream);
 

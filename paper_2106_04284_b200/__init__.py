@@ -22,7 +22,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libllama_b200.so")
 
-KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3}
+KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3, "one": 4}
 PATHS = {"auto": 0, "naive": 1, "blobcopy": 2, "run": 3, "permute": 4}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_MISMATCH",
@@ -30,7 +30,8 @@ STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_
           -6: "LLAMA_ERR_OVERLAP", -7: "LLAMA_ERR_CUDA", -8: "LLAMA_ERR_OOM"}
 
 # Symbols declared in include/llama_b200.h (checked by tests/test_capi_host.py).
-EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_mapping_destroy",
+EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_mapping_create_split",
+           "llama_mapping_destroy",
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
            "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
@@ -71,6 +72,8 @@ def _load():
     lib.llama_mapping_create_from_schema.argtypes = [ctypes.c_char_p, P(ctypes.c_int64), ctypes.c_int32,
                                                      ctypes.c_int, ctypes.c_int64, ctypes.c_int32,
                                                      P(ctypes.c_void_p)]
+    lib.llama_mapping_create_split.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(ctypes.c_int32),
+                                                ctypes.c_int32, P(ctypes.c_void_p)]
     lib.llama_mapping_destroy.argtypes = [ctypes.c_void_p]
     lib.llama_mapping_destroy.restype = None
     lib.llama_blob_count.argtypes = [ctypes.c_void_p]
@@ -109,8 +112,10 @@ def _check(status):
 
 
 class Mapping:
-    """A mapping of a record dimension (schema string)
-    over array extents.  kind: 'aos' | 'soa_sb' | 'soa_mb' | 'aosoa'."""
+    """A mapping of a record dimension (schema string, S:122-126,
+    or a list of llama_scalar leaf type codes) over array extents.
+    kind: 'aos' | 'soa_sb' | 'soa_mb' | 'aosoa' | 'one'; splits come from
+    Mapping.split / Mapping.from_spec."""
 
     def __init__(self, schema, extents, kind="aos", lanes=1, aligned=False):
         self.schema = schema
@@ -122,9 +127,46 @@ class Mapping:
             raise ValueError(f"unknown mapping kind {kind!r}")
         ext = (ctypes.c_int64 * len(self.extents))(*self.extents)
         h = ctypes.c_void_p()
-        _check(_lib.llama_mapping_create_from_schema(schema.encode(), ext, len(self.extents), KINDS[kind],
-                                                     self.lanes, int(self.aligned), ctypes.byref(h)))
+        if isinstance(schema, str):
+            _check(_lib.llama_mapping_create_from_schema(schema.encode(), ext, len(self.extents), KINDS[kind],
+                                                         self.lanes, int(self.aligned), ctypes.byref(h)))
+        else:
+            types = (ctypes.c_int * len(schema))(*[int(t) for t in schema])
+            d = _Desc(types, len(schema), ext, len(self.extents), KINDS[kind], self.lanes, int(self.aligned))
+            _check(_lib.llama_mapping_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
+
+    @classmethod
+    def split(cls, a, b, leaves_a):
+        """Split: leaves_a (increasing DFS leaf indices of the full
+        record) are mapped by `a`, the others by `b`; blobs are a's then b's."""
+        self = cls.__new__(cls)
+        la = (ctypes.c_int32 * max(1, len(leaves_a)))(*[int(k) for k in leaves_a])
+        h = ctypes.c_void_p()
+        _check(_lib.llama_mapping_create_split(a.handle, b.handle, la, len(leaves_a), ctypes.byref(h)))
+        self._h = h
+        self.schema = None
+        self.extents = list(a.extents)
+        self.kind = "split"
+        self.lanes = 1
+        self.aligned = False
+        self.parts = (a, b, [int(k) for k in leaves_a])
+        return self
+
+    @classmethod
+    def from_spec(cls, schema, extents, spec):
+        """A mapping from (kind, lanes, aligned) or a split tree
+        (leaves_a, spec_a, spec_b) (argument marshalling: the parts' leaf
+        type lists are selected from the full record's)."""
+        if len(spec) == 3 and isinstance(spec[0], str):
+            kind, lanes, aligned = spec
+            return cls(schema, extents, kind, lanes, aligned)
+        types = schema if not isinstance(schema, str) else cls(schema, [0]).leaf_types()
+        leaves_a, spec_a, spec_b = spec
+        sel = set(int(k) for k in leaves_a)
+        a = cls.from_spec([types[k] for k in sorted(sel)], extents, spec_a)
+        b = cls.from_spec([t for k, t in enumerate(types) if k not in sel], extents, spec_b)
+        return cls.split(a, b, sorted(sel))
 
     @property
     def handle(self):
@@ -137,6 +179,8 @@ class Mapping:
             self._h = None
 
     def __repr__(self):
+        if self.kind == "split":
+            return f"Mapping(split {self.parts[2]}: {self.parts[0]!r} | {self.parts[1]!r})"
         return f"Mapping({self.kind}, lanes={self.lanes}, aligned={self.aligned}, extents={self.extents})"
 
     @property

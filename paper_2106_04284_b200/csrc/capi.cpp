@@ -104,6 +104,26 @@ llama_status llama_mapping_create_from_schema(const char* schema, const int64_t*
   }
 }
 
+llama_status llama_mapping_create_split(const llama_mapping* a, const llama_mapping* b, const int32_t* leaves_a,
+                                        int32_t n_a, llama_mapping** out) {
+  if (!a || !b || !out || (n_a > 0 && !leaves_a)) return fail(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    auto* m = new llama_mapping;
+    std::string err;
+    llama_status st = llb::build_split(a->m, b->m, leaves_a, n_a, &m->m, &err);
+    if (st != LLAMA_OK) {
+      delete m;
+      return fail(st, err);
+    }
+    *out = m;
+    return LLAMA_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(LLAMA_ERR_OOM, "out of host memory");
+  } catch (...) {
+    return fail(LLAMA_ERR_INVALID_ARGUMENT, "unexpected error");
+  }
+}
+
 void llama_mapping_destroy(llama_mapping* m) {
   if (!m) return;
   {
@@ -293,8 +313,6 @@ llama_status llama_generate(const llama_mapping* m, void* const* blobs, uint64_t
     g->N = mm.N;
     g->seed = seed;
     g->K = mm.K();
-    g->d = mm.dev_side();
-    if (mm.soa()) g->d.lshift = 63;
     for (int k = 0; k < mm.K(); ++k) g->dl[k] = mm.dev_leaf(k);
     for (int b = 0; b < mm.nblobs(); ++b) g->db[b] = static_cast<uint8_t*>(blobs[b]);
     if ((e = llb::launch_gen(*g, stream))) return cuda_fail(e, "generate launch");

@@ -20,6 +20,12 @@ __device__ __forceinline__ uint64_t nf_offset(uint64_t i, const DevSide& s, cons
   return l.base + q * s.B + l.F + (i - q * s.L) * l.size;
 }
 
+// The same with the leaf's own L and B (composite Split / One mappings).
+__device__ __forceinline__ uint64_t leaf_offset(uint64_t i, const DevLeaf& l) {
+  const uint64_t q = l.lshift != kNoShift ? (i >> l.lshift) : (i / l.L);
+  return l.base + q * l.B + l.F + (i - q * l.L) * l.size;
+}
+
 // Copies n bytes between arbitrary addresses using the widest naturally
 // aligned access both pointers allow (never assumes alignment; packed
 // layouts put f64 at odd offsets).

@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(kThreads) k_run(const __grid_constant__ RunPar
           const uint32_t lg = 31 - __clz(sl.size);  // log2 s_k
           const uint64_t r = r0 + ((uint64_t)(v - p.cvstart[k]) << (4 - lg));
           if (r < p.N) {
-            const uint8_t* s = p.sb[sl.blob] + nf_offset(r, p.s, sl);
-            uint8_t* d = p.db[dl.blob] + nf_offset(r, p.d, dl);
+            const uint8_t* s = p.sb[sl.blob] + leaf_offset(r, sl);
+            uint8_t* d = p.db[dl.blob] + leaf_offset(r, dl);
             if (r + (16u >> lg) <= p.N) {
               val[j] = __ldcs(reinterpret_cast<const uint4*>(s));
               dp[j] = d;

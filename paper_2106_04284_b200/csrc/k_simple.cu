@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(kThreads) k_naive(const __grid_constant__ Naiv
     for (int k = 0; k < p.K; ++k) {
       const DevLeaf& sl = p.sl[k];
       const DevLeaf& dl = p.dl[k];
-      const uint8_t* s = p.sb[sl.blob] + nf_offset(i, p.s, sl);
-      uint8_t* d = p.db[dl.blob] + nf_offset(i, p.d, dl);
+      const uint8_t* s = p.sb[sl.blob] + leaf_offset(i, sl);
+      uint8_t* d = p.db[dl.blob] + leaf_offset(i, dl);
       copy_elem(d, s, sl.size);
     }
   }
@@ -79,8 +79,11 @@ __global__ void __launch_bounds__(kThreads) k_gen(const __grid_constant__ GenPar
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.N; i += stride) {
     for (int k = 0; k < p.K; ++k) {
       const DevLeaf& dl = p.dl[k];
+      // a leaf that maps several records onto one place (One, B = 0) keeps
+      // the last of them in index order, as a sequential generator would
+      if (dl.B == 0 && i + dl.L < p.N) continue;
       uint64_t v = splitmix64(p.seed ^ (i * (uint64_t)p.K + (uint64_t)k));
-      uint8_t* d = p.db[dl.blob] + nf_offset(i, p.d, dl);
+      uint8_t* d = p.db[dl.blob] + leaf_offset(i, dl);
       copy_elem(d, reinterpret_cast<const uint8_t*>(&v), dl.size);
     }
   }

@@ -159,14 +159,66 @@ DevSide Mapping::dev_side() const {
   return d;
 }
 
-DevLeaf Mapping::dev_leaf(int k) const { return DevLeaf{base[k], F[k], blob[k], sizes[k]}; }
+DevLeaf Mapping::dev_leaf(int k) const {
+  DevLeaf l{};
+  l.base = base[k];
+  l.F = F[k];
+  l.L = Lk[k];
+  l.B = Bk[k];
+  l.blob = blob[k];
+  l.size = sizes[k];
+  if (Bk[k] == 0 && Lk[k] >= N) l.lshift = 63;  // a single block: i / L == 0 for every valid i
+  else l.lshift = (Lk[k] & (Lk[k] - 1)) == 0 ? (uint32_t)__builtin_ctzll(Lk[k]) : kNoShift;
+  return l;
+}
+
+llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leaves_a, int32_t n_a, Mapping* m,
+                         std::string* err) {
+  const int K = a.K() + b.K();
+  if (n_a != a.K()) { *err = "leaves_a must list exactly a's leaves"; return LLAMA_ERR_INVALID_ARGUMENT; }
+  if (K > LLAMA_MAX_LEAVES) { *err = "more than LLAMA_MAX_LEAVES leaves"; return LLAMA_ERR_UNSUPPORTED; }
+  if (a.extents != b.extents) { *err = "a and b must have the same extents"; return LLAMA_ERR_INVALID_ARGUMENT; }
+  if (a.nblobs() + b.nblobs() > LLAMA_MAX_BLOBS) { *err = "more than LLAMA_MAX_BLOBS blobs"; return LLAMA_ERR_UNSUPPORTED; }
+  std::vector<int> in_a(K, -1);
+  for (int j = 0; j < n_a; ++j) {
+    if (leaves_a[j] < 0 || leaves_a[j] >= K || (j > 0 && leaves_a[j] <= leaves_a[j - 1])) {
+      *err = "leaves_a must be strictly increasing leaf indices";
+      return LLAMA_ERR_INVALID_ARGUMENT;
+    }
+    in_a[leaves_a[j]] = j;
+  }
+  *m = Mapping();
+  m->extents = a.extents;
+  m->N = a.N;
+  m->kind = LLAMA_SPLIT;
+  m->uniform = false;
+  m->E = a.N;
+  int ib = 0;
+  for (int k = 0; k < K; ++k) {
+    const bool A = in_a[k] >= 0;
+    const Mapping& s = A ? a : b;
+    const int j = A ? in_a[k] : ib++;
+    m->types.push_back(s.types[j]);
+    m->sizes.push_back(s.sizes[j]);
+    m->rec_off.push_back(0);
+    m->Lk.push_back(s.Lk[j]);
+    m->Bk.push_back(s.Bk[j]);
+    m->base.push_back(s.base[j]);
+    m->F.push_back(s.F[j]);
+    m->blob.push_back(s.blob[j] + (A ? 0u : (uint32_t)a.nblobs()));
+  }
+  m->blob_sizes = a.blob_sizes;
+  m->blob_sizes.insert(m->blob_sizes.end(), b.blob_sizes.begin(), b.blob_sizes.end());
+  m->id = g_next_id.fetch_add(1);
+  return LLAMA_OK;
+}
 
 llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string* err) {
   if (!d.leaf_types || !d.extents) { *err = "NULL leaf_types or extents"; return LLAMA_ERR_INVALID_ARGUMENT; }
   if (d.n_leaves < 1 || d.rank < 1) { *err = "n_leaves and rank must be >= 1"; return LLAMA_ERR_INVALID_ARGUMENT; }
   if (d.n_leaves > LLAMA_MAX_LEAVES) { *err = "more than LLAMA_MAX_LEAVES leaves"; return LLAMA_ERR_UNSUPPORTED; }
   if (d.rank > LLAMA_MAX_RANK) { *err = "rank above LLAMA_MAX_RANK"; return LLAMA_ERR_UNSUPPORTED; }
-  if (d.kind < LLAMA_AOS || d.kind > LLAMA_AOSOA) { *err = "bad kind"; return LLAMA_ERR_INVALID_ARGUMENT; }
+  if (d.kind < LLAMA_AOS || d.kind > LLAMA_ONE) { *err = "bad kind"; return LLAMA_ERR_INVALID_ARGUMENT; }
   if (d.kind == LLAMA_AOSOA && d.lanes < 1) { *err = "AoSoA lanes must be >= 1"; return LLAMA_ERR_INVALID_ARGUMENT; }
   m->types.assign(d.leaf_types, d.leaf_types + d.n_leaves);
   m->sizes.clear();
@@ -185,7 +237,7 @@ llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string*
   m->N = N;
   m->kind = d.kind;
   m->lanes = d.kind == LLAMA_AOSOA ? d.lanes : 1;
-  m->aligned = d.aligned != 0;
+  m->aligned = d.aligned != 0 || d.kind == LLAMA_ONE;  // One stores one aligned record
   const int K = d.n_leaves;
 
   // record offsets: packed or natural alignment
@@ -229,6 +281,13 @@ llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string*
       }
       if (K > LLAMA_MAX_BLOBS) { *err = "more than LLAMA_MAX_BLOBS blobs"; return LLAMA_ERR_UNSUPPORTED; }
       break;
+    case LLAMA_ONE:  // every record at the same place (L = 1, B = 0)
+      m->L = 1;
+      m->B = 0;
+      m->E = N;
+      for (int k = 0; k < K; ++k) m->F[k] = m->rec_off[k];
+      m->blob_sizes.push_back(m->record_bytes);
+      break;
     case LLAMA_SOA_SINGLE_BLOB: {
       m->L = N > 0 ? N : 1;
       m->B = 0;
@@ -244,6 +303,8 @@ llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string*
       break;
     }
   }
+  m->Lk.assign(K, m->L);
+  m->Bk.assign(K, m->B);
   m->id = g_next_id.fetch_add(1);
   return LLAMA_OK;
 }

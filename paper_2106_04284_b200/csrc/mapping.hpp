@@ -31,8 +31,12 @@ struct Mapping {
   uint64_t record_bytes = 0; // S (packed or aligned record size)
   std::vector<uint64_t> rec_off;  // leaf offsets inside one record
 
-  // normal form: off(i,k) = base_k + (i / L) * B + F_k + (i % L) * s_k
+  // normal form: off(i,k) = base_k + (i / L_k) * B_k + F_k + (i % L_k) * s_k.
+  // L / B are the mapping-wide values of the four uniform kinds; Lk / Bk
+  // hold them per leaf (they differ between the parts of a Split).
   uint64_t L = 1, B = 0;
+  bool uniform = true;  // every leaf shares L and B (not a Split)
+  std::vector<uint64_t> Lk, Bk;
   std::vector<uint64_t> base, F;
   std::vector<uint32_t> blob;
   std::vector<uint64_t> blob_sizes;
@@ -41,15 +45,25 @@ struct Mapping {
   int K() const { return (int)sizes.size(); }
   int nblobs() const { return (int)blob_sizes.size(); }
   bool soa() const { return kind == LLAMA_SOA_SINGLE_BLOB || kind == LLAMA_SOA_MULTI_BLOB; }
+  // a leaf maps several records onto one location (One, or a One part of a Split)
+  bool collides() const {
+    for (int k = 0; k < K(); ++k)
+      if (Bk[k] == 0 && Lk[k] < N && N > 1) return true;
+    return false;
+  }
   uint64_t payload_bytes() const;   // N * sum s_k
   uint64_t footprint_bytes() const; // sum of blob sizes
   bool has_padding() const { return footprint_bytes() != payload_bytes(); }
-  uint64_t offset(uint64_t i, int k) const { return base[k] + (i / L) * B + F[k] + (i % L) * sizes[k]; }
+  uint64_t offset(uint64_t i, int k) const { return base[k] + (i / Lk[k]) * Bk[k] + F[k] + (i % Lk[k]) * sizes[k]; }
   DevSide dev_side() const;
   DevLeaf dev_leaf(int k) const;
 };
 
 // Builds the descriptor; returns LLAMA_OK or an error with *err set.
 llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string* err);
+
+// Split: leaves_a of the full record go to a, the rest to b.
+llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leaves_a, int32_t n_a, Mapping* m,
+                         std::string* err);
 
 }  // namespace llb

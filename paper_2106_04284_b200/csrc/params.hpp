@@ -24,11 +24,17 @@ struct DevSide {
   uint32_t pad_;
 };
 
+// One leaf's normal form (per leaf, so composite Split mappings and One fit):
+//   off(i) = base + (i / L) * B + F + (i % L) * size     in blob `blob`
 struct DevLeaf {
   uint64_t base;
   uint64_t F;
+  uint64_t L;
+  uint64_t B;
   uint32_t blob;
   uint32_t size;
+  uint32_t lshift;  // log2(L) when L is a power of two (63 for a single-block SoA leaf), else kNoShift
+  uint32_t pad_;
 };
 
 // ---------------------------------------------------------------- naive / gen
@@ -36,7 +42,6 @@ struct NaiveParams {
   uint64_t N;
   int32_t K;
   int32_t pad_;
-  DevSide s, d;
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];
@@ -48,7 +53,6 @@ struct GenParams {
   uint64_t seed;
   int32_t K;
   int32_t pad_;
-  DevSide d;
   DevLeaf dl[kMaxLeaves];
   uint8_t* db[kMaxBlobs];
 };
@@ -96,7 +100,6 @@ struct RunParams {
   uint64_t n_chunks;
   uint32_t chunk_vecs;  // 16-byte vectors in a full chunk (sum over leaves)
   int32_t K;
-  DevSide s, d;
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   uint32_t cvstart[kMaxLeaves + 1];  // prefix of C*s_k/16 vectors per leaf in a chunk
@@ -176,4 +179,8 @@ struct PermParams {
   uint8_t* blobs[2][kMaxBlobs];
 };
 
+// kernel parameter blocks travel as __grid_constant__ arguments (<= 32764 B)
+static_assert(sizeof(PermParams) <= 32764, "PermParams exceeds the kernel parameter limit");
+static_assert(sizeof(NaiveParams) <= 32764, "NaiveParams exceeds the kernel parameter limit");
+static_assert(sizeof(RunParams) <= 32764, "RunParams exceeds the kernel parameter limit");
 }  // namespace llb

@@ -32,7 +32,7 @@ uint64_t align16(uint64_t x) { return (x + 15) & ~15ull; }
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 bool same_layout(const Mapping& s, const Mapping& d) {
-  if (s.L != d.L || s.B != d.B || s.blob_sizes != d.blob_sizes) return false;
+  if (s.Lk != d.Lk || s.Bk != d.Bk || s.blob_sizes != d.blob_sizes) return false;
   for (int k = 0; k < s.K(); ++k)
     if (s.base[k] != d.base[k] || s.F[k] != d.F[k] || s.blob[k] != d.blob[k]) return false;
   return true;
@@ -78,8 +78,6 @@ void plan_naive(const Mapping& s, const Mapping& d, Plan* p) {
   std::memset(&n, 0, sizeof(n));
   n.N = s.N;
   n.K = s.K();
-  n.s = side_of(s);
-  n.d = side_of(d);
   for (int k = 0; k < s.K(); ++k) {
     n.sl[k] = s.dev_leaf(k);
     n.dl[k] = d.dev_leaf(k);
@@ -124,7 +122,7 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
     // records per common run ("min(N,M)"; gcd for lane counts that do
     // not divide each other); a single block counts as L = N
     const uint64_t n1 = std::max<uint64_t>(s.N, 1);
-    const uint64_t g = gcd64(std::min(s.L, n1), std::min(d.L, n1));
+    const uint64_t g = gcd64(std::min(s.Lk[k], n1), std::min(d.Lk[k], n1));
     const bool single_run = g >= s.N;    // the whole leaf is one run on both sides
     if (!single_run && (g * sz) % 16 != 0) { *why = "common runs shorter than 16 B"; return false; }
     for (int X = 0; X < 2; ++X) {
@@ -133,7 +131,7 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
         *why = "run starts not 16-B aligned";
         return false;
       }
-      if (!single_run && m.E > m.L && m.B % 16 != 0) { *why = "block stride not 16-B aligned"; return false; }
+      if (!single_run && m.N > m.Lk[k] && m.Bk[k] % 16 != 0) { *why = "block stride not 16-B aligned"; return false; }
     }
   }
   p->path = LLAMA_PATH_RUN;
@@ -142,8 +140,6 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
   std::memset(&r, 0, sizeof(r));
   r.N = s.N;
   r.K = s.K();
-  r.s = side_of(s);
-  r.d = side_of(d);
   // chunk = C records, a multiple of 16 (every leaf's chunk part is whole
   // 16-byte vectors) sized to ~32 KB of source bytes
   uint64_t S = 0;
@@ -162,6 +158,10 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
 }
 
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
+  // tiles need one normal form per side (not a Split) with records spread
+  // over the blobs (not One)
+  for (const Mapping* m : {&s, &d})
+    if (!m->uniform || m->kind == LLAMA_ONE) { *why = "split or one mapping"; return false; }
   const Mapping* side[2] = {&s, &d};
   bool soa_like[2];
   uint64_t Tmult = 32;
@@ -396,6 +396,10 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
                        std::string* err) {
   llama_status st = check_compatible(s, d, err);
   if (st != LLAMA_OK) return st;
+  if (d.collides()) {  // the copy's result would depend on the order of the writes
+    *err = "destination maps several records onto one location (One / a One part of a Split)";
+    return LLAMA_ERR_UNSUPPORTED;
+  }
   out->src_bytes = s.footprint_bytes();
   out->dst_bytes = d.footprint_bytes();
   if (out->dst_bytes == 0) {

@@ -165,6 +165,10 @@ llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, v
     for (int b = 0; b < d.nblobs(); ++b)
       if (d.blob_sizes[b] && !dst_blobs[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL dst blob");
     const uint64_t N = s.N;
+    if (d.collides())
+      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "destination maps several records onto one location");
+    if (!s.uniform || !d.uniform || s.kind == LLAMA_ONE || d.kind == LLAMA_ONE)
+      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a split / one mapping (copy its blobs, then llama_copy)");
     if (d.footprint_bytes() == 0) return LLAMA_OK;
 
     // slab unit: whole blocks of every blocked side (lcm of the lane counts)

@@ -166,3 +166,49 @@ def test_planner_forced_paths():
     with pytest.raises(llama.LlamaError):
         llama.plan(s, d, path="permute", tile_records=48)
     assert llama.plan(s, d, path="permute", tile_records=64)["tile_records"] == 64
+
+
+# ------------------------------------------------------------ One / Split (f1)
+SPLIT_NAMES = sorted(W.SPLITS)
+
+
+@pytest.mark.parametrize("name", SPLIT_NAMES + ["one"])
+@pytest.mark.parametrize("ext", [[1], [5], [33], [4, 3]])
+def test_split_one_descriptor_matches_oracle(oracle_mod, name, ext):
+    schema = W.SCHEMAS[W.SPLITS[name][0]] if name in W.SPLITS else W.LISTING1
+    spec = W.resolve_spec(name)
+    m = llama.Mapping.from_spec(schema, ext, spec)
+    o = oracle_mod.mapping_from_spec(schema, ext, spec)
+    assert m.blob_sizes() == o.blob_sizes()
+    assert m.leaf_types() == llama.Mapping(schema, ext).leaf_types()
+    n = int(np.prod(ext))
+    for flat in range(n):
+        idx = [int(x) for x in np.unravel_index(flat, ext)]
+        for k in range(o.n_leaves):
+            assert m.blob_nr_and_offset(idx, k) == o.addr(flat, k)
+
+
+def test_split_errors_and_plans():
+    sizes = llama.Mapping(W.LISTING1, [4]).leaf_types()
+    a = llama.Mapping(sizes[:2], [4], "soa_mb")
+    b = llama.Mapping(sizes[2:], [4], "aos")
+    llama.Mapping.split(a, b, [0, 1])
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping.split(a, b, [1, 0])
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping.split(a, b, [0])
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping.split(a, llama.Mapping(sizes[2:], [5], "aos"), [0, 1])
+    aos = llama.Mapping(W.LISTING1, [4])
+    one = llama.Mapping(W.LISTING1, [4], "one")
+    mc = llama.Mapping.from_spec(W.LISTING1, [4], W.resolve_spec("mapping_c"))
+    # a destination that maps several records onto one place is rejected (reading #24)
+    for dst in (one, mc):
+        with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
+            llama.plan(aos, dst)
+    assert llama.plan(one, aos)["path"] == "naive"
+    assert llama.plan(mc, aos)["path"] == "naive"
+    one1 = llama.Mapping(W.LISTING1, [1], "one")
+    llama.plan(llama.Mapping(W.LISTING1, [1]), one1)  # one record: no collision
+    sp = llama.Mapping.from_spec(W.LISTING1, [4], W.resolve_spec("split_pos"))
+    assert llama.plan(sp, sp)["path"] == "blobcopy"

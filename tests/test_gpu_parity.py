@@ -285,3 +285,70 @@ def test_staged_copy_host_buffers(llama, oracle_mod, cap):
         torch.cuda.synchronize()
         for j, x in enumerate(hd2):
             assert np.array_equal(x.numpy(), exp[j])
+
+
+# ------------------------------------------------------------ One / Split (f1)
+def run_spec_case(llama, oracle, schema, ext, s_spec, d_spec, seed=7, pad=0xCD):
+    """run_case for workloads spec trees (MAPPINGS tuples or split trees)."""
+    sm = llama.Mapping.from_spec(schema, ext, s_spec)
+    dm = llama.Mapping.from_spec(schema, ext, d_spec)
+    so = oracle.mapping_from_spec(schema, ext, s_spec)
+    do = oracle.mapping_from_spec(schema, ext, d_spec)
+    sb = sm.alloc("cuda")
+    llama.generate(sm, sb, seed, pad_byte=pad)
+    src_host = oracle.make_view(so, seed, pad_fill=pad)
+    for j, t in enumerate(sb):
+        assert np.array_equal(_host(t), src_host[j]), f"generated source differs in blob {j}"
+    exp = oracle.copy(so, src_host, do)
+    for path in ALL_PATHS:
+        if path != "auto":
+            try:
+                llama.plan(sm, dm, path=path)
+            except llama.LlamaError:
+                continue
+        db = dm.alloc("cuda")
+        for t in db:
+            t.fill_(0x5A)
+        llama.copy(sm, sb, dm, db, path=path)
+        torch.cuda.synchronize()
+        for j, t in enumerate(db):
+            got = _host(t)
+            assert np.array_equal(got, exp[j]), (f"{sm!r}->{dm!r} ext={ext} path={path}: blob {j}: "
+                                                 f"{int((got != exp[j]).sum())} bytes differ")
+
+
+_SPLIT_SETS = {
+    "particle7": ["aos", "soa_mb", "aosoa8", "split_p7"],
+    "listing1": ["aos", "aos_aligned", "soa_sb", "split_pos"],
+    "hep100": ["aos", "soa_mb", "split_hep"],
+}
+
+
+@pytest.mark.parametrize("n", [1, 33, 4097, 100_003])
+@pytest.mark.parametrize("schema_name", sorted(_SPLIT_SETS))
+def test_split_pairs(llama, oracle_mod, schema_name, n):
+    names = _SPLIT_SETS[schema_name]
+    if schema_name == "hep100" and n > 5000:
+        n = 5000
+    schema = W.SCHEMAS[schema_name]
+    for a in names:
+        for b in names:
+            if "split" in a or "split" in b:
+                run_spec_case(llama, oracle_mod, schema, [n], W.resolve_spec(a), W.resolve_spec(b))
+
+
+@pytest.mark.parametrize("n", [1, 9, 1000])
+def test_one_and_mapping_c_sources(llama, oracle_mod, n):
+    """One / MappingC (Listing P:499-509) as sources broadcast their One
+    record; as destinations only a single record is allowed (reading #24)."""
+    for src in ("one", "mapping_c"):
+        for dst in ("aos", "soa_mb", "split_pos"):
+            run_spec_case(llama, oracle_mod, W.LISTING1, [n], W.resolve_spec(src), W.resolve_spec(dst))
+    if n == 1:
+        for dst in ("one", "mapping_c"):
+            run_spec_case(llama, oracle_mod, W.LISTING1, [1], W.resolve_spec("aos"), W.resolve_spec(dst))
+    else:
+        sm = llama.Mapping(W.LISTING1, [n])
+        with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
+            llama.copy(sm, sm.alloc("cuda"), llama.Mapping(W.LISTING1, [n], "one"),
+                       llama.Mapping(W.LISTING1, [n], "one").alloc("cuda"))

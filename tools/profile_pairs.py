@@ -28,8 +28,8 @@ schema = W.SCHEMAS[cfg["schema"]]
 ext = [a.records] if a.records else list(cfg["extents"])
 for pair in a.pairs.split(","):
     s, d = pair.split(":")
-    sm = llama.Mapping(schema, ext, *W.MAPPINGS[s])
-    dm = llama.Mapping(schema, ext, *W.MAPPINGS[d])
+    sm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(s))
+    dm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(d))
     sb, db = sm.alloc(), dm.alloc()
     llama.generate(sm, sb, 42)
     torch.cuda.synchronize()
