@@ -40,7 +40,7 @@ __device__ __forceinline__ void issue_loads_v1(const PermParams& p, const SSeg* 
   }
 }
 
-template <bool kTma>
+template <bool kTma, bool kParts>
 __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__ PermParams p) {
   // dynamic smem: [mbarriers | segment tables | src ring | dst buffers]
   extern __shared__ __align__(128) uint8_t smem[];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
-    permute_records(p, wt, simg, dimg, nrec, tid);
+    permute_records<kParts>(p, wt, simg, dimg, nrec, tid);
     if (kTma) fence_proxy_async_smem();
     __syncthreads();
 
@@ -149,19 +149,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_permute(const __grid_constant__
 }
 
 int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream) {
-  static LaunchCache cache[2][64];
+  static LaunchCache cache[4][64];
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   current_device_sms(&sms);
-  int e = p.tma ? prepare_kernel(k_permute<true>, kThreads, smem_bytes, &cache[1][dev & 63], &per_sm)
-                : prepare_kernel(k_permute<false>, kThreads, smem_bytes, &cache[0][dev & 63], &per_sm);
+  const int v = (p.tma ? 1 : 0) + (multi_geo(p) ? 2 : 0);
+  void (*const kern[4])(PermParams) = {k_permute<false, false>, k_permute<true, false>, k_permute<false, true>,
+                                       k_permute<true, true>};
+  int e = prepare_kernel(kern[v], kThreads, smem_bytes, &cache[v][dev & 63], &per_sm);
   if (e) return e;
   uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
   if (grid > p.n_tiles) grid = p.n_tiles;
-  if (p.tma)
-    k_permute<true><<<(unsigned)grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(p);
-  else
-    k_permute<false><<<(unsigned)grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(p);
+  kern[v]<<<(unsigned)grid, kThreads, smem_bytes, (cudaStream_t)stream>>>(p);
   count_launch();
   return (int)cudaGetLastError();
 }

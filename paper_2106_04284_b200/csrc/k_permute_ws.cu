@@ -27,6 +27,7 @@ __device__ __forceinline__ void named_sync_consumers() {
   asm volatile("bar.sync 1, %0;" ::"n"(kPermThreads) : "memory");
 }
 
+template <bool kParts>
 __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_constant__ PermParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
       named_sync_consumers();
     }
-    permute_records(p, wt, simg, dimg, nrec, tid);
+    permute_records<kParts>(p, wt, simg, dimg, nrec, tid);
     if (!fl) {  // destination tails (sub-16-byte) go out directly
       named_sync_consumers();
       for (int j = 0; j < n_segs(p, 1); ++j) {
@@ -166,11 +167,13 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
 }
 
 int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
-  static LaunchCache cache[64];
+  static LaunchCache cache[2][64];
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   current_device_sms(&sms);
-  int e = prepare_kernel(k_permute_ws, kThreadsWS, smem_bytes, &cache[dev & 63], &per_sm);
+  const bool parts = multi_geo(p);
+  auto kern = parts ? k_permute_ws<true> : k_permute_ws<false>;
+  int e = prepare_kernel(kern, kThreadsWS, smem_bytes, &cache[parts][dev & 63], &per_sm);
   if (e) return e;
   uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
   if (grid > p.n_tiles) grid = p.n_tiles;
@@ -188,7 +191,7 @@ int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 0 : 1;
-  cudaError_t le = cudaLaunchKernelEx(&cfg, k_permute_ws, p);
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, p);
   count_launch();
   return le != cudaSuccess ? (int)le : (int)cudaGetLastError();
 }

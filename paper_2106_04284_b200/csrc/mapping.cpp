@@ -1,6 +1,7 @@
 // mapping.cpp -- schema parser, record offsets and the AoSoA normal form.
 #include "mapping.hpp"
 
+#include <algorithm>
 #include <atomic>
 #include <cctype>
 
@@ -192,7 +193,7 @@ llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leav
   m->N = a.N;
   m->kind = LLAMA_SPLIT;
   m->uniform = false;
-  m->E = a.N;
+  m->E = std::max(a.E, b.E);  // records the blobs cover: the largest of the parts
   int ib = 0;
   for (int k = 0; k < K; ++k) {
     const bool A = in_a[k] >= 0;
@@ -209,6 +210,15 @@ llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leav
   }
   m->blob_sizes = a.blob_sizes;
   m->blob_sizes.insert(m->blob_sizes.end(), b.blob_sizes.begin(), b.blob_sizes.end());
+  std::vector<int> full_b;  // leaf j of b is leaf full_b[j] of the split
+  for (int k = 0; k < K; ++k)
+    if (in_a[k] < 0) full_b.push_back(k);
+  for (int X = 0; X < 2; ++X)
+    for (const Part& q : (X == 0 ? a : b).parts) {
+      Part r = q;
+      for (int& l : r.leaves) l = X == 0 ? leaves_a[l] : full_b[l];
+      m->parts.push_back(r);
+    }
   m->id = g_next_id.fetch_add(1);
   return LLAMA_OK;
 }
@@ -305,6 +315,15 @@ llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string*
   }
   m->Lk.assign(K, m->L);
   m->Bk.assign(K, m->B);
+  Part whole;
+  whole.kind = m->kind;
+  whole.aligned = m->aligned;
+  whole.L = m->L;
+  whole.B = m->B;
+  whole.E = m->E;
+  whole.record_bytes = m->record_bytes;
+  for (int k = 0; k < K; ++k) whole.leaves.push_back(k);
+  m->parts.assign(1, whole);
   m->id = g_next_id.fetch_add(1);
   return LLAMA_OK;
 }

@@ -18,6 +18,17 @@ uint32_t scalar_size(llama_scalar t);
 // Returns false with a message on a malformed schema.
 bool parse_schema(const std::string& schema, std::vector<llama_scalar>* leaves, std::string* err);
 
+// A part of a mapping: leaves that share one uniform normal form (the whole
+// mapping for the classic kinds; each inner mapping of a Split).
+struct Part {
+  llama_kind kind = LLAMA_AOS;
+  bool aligned = false;
+  uint64_t L = 1, B = 0, E = 0;
+  uint64_t record_bytes = 0;  // the part's record size S (AoS / AoSoA)
+  std::vector<int> leaves;    // leaf indices of the full record, increasing
+  bool soa() const { return kind == LLAMA_SOA_SINGLE_BLOB || kind == LLAMA_SOA_MULTI_BLOB; }
+};
+
 struct Mapping {
   uint64_t id = 0;  // unique per process, keys the plan cache
   std::vector<llama_scalar> types;
@@ -41,6 +52,7 @@ struct Mapping {
   std::vector<uint32_t> blob;
   std::vector<uint64_t> blob_sizes;
   uint64_t E = 0;            // records covered by the blobs (blocked: nblocks*L; SoA: N)
+  std::vector<Part> parts;   // one for the classic kinds; a split's parts in blob order
 
   int K() const { return (int)sizes.size(); }
   int nblobs() const { return (int)blob_sizes.size(); }

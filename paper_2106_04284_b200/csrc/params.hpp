@@ -109,18 +109,39 @@ struct RunParams {
 
 // ------------------------------------------------------------ tile permute
 // A tile is T consecutive records.  Each side keeps one shared-memory image
-// per tile: an "AoS-like" side (L divides T) as the single contiguous byte
-// range of its T/L blocks; a "SoA-like" side (T divides L, or SoA) as one
-// segment of T*s_k bytes per leaf.  Inside the image, leaf k of tile record r
-// sits at  (r / Limg) * Bimg + imgF_k + (r % Limg) * s_k.
-struct PermSide {
-  DevSide g;          // global normal form (segment addresses)
-  uint64_t E;         // records the side's blobs cover (padded block extent / N)
+// per tile, made of the images of its parts (one part for the classic kinds,
+// one per inner mapping of a Split): an "AoS-like" part (L divides T) as the
+// single contiguous byte range of its T/L blocks; a "SoA-like" part (T
+// divides L, or SoA) as one segment of T*s_k bytes per leaf.  Inside the
+// image, leaf k (of part P) of tile record r sits at
+//   (r / Limg_P) * Bimg_P + imgF_k + (r % Limg_P) * s_k.
+struct PermPart {
+  DevSide g;          // the part's global normal form (segment addresses)
+  uint64_t E;         // records the part's blobs cover (padded block extent / N)
   uint32_t soa_like;  // 1: per-leaf segments
-  uint32_t linear;    // 1: a full tile's segment addresses are linear in the tile index
+  uint32_t pad_;
+};
+
+struct PermGeo {      // image geometry shared by one or more parts of a side
   uint32_t Limg;      // image lanes (AoS-like: L; SoA-like: T)
   uint32_t limg_shift;
   uint32_t Bimg;      // image block stride
+  uint32_t pad_;
+};
+constexpr int kMaxParts = 8;
+
+struct PermSeg {      // segment j of a side: part, leaf (AoS-like: any leaf of the part), image offset
+  uint16_t part;
+  uint16_t leaf;
+  uint32_t soff;
+};
+
+struct PermSide {
+  uint64_t E;         // records the side's blobs cover (max over its parts)
+  uint32_t n_parts;
+  uint32_t n_geo;     // distinct image geometries (1: the permute hoists one record offset)
+  uint32_t n_segs;
+  uint32_t linear;    // 1: a full tile's segment addresses are linear in the tile index
   uint32_t img_bytes; // image bytes of a full tile
 };
 
@@ -142,11 +163,12 @@ struct WordMove {
 };
 constexpr int kMaxWordMoves = 128;  // 4 per lane
 
-struct MoveClass {    // moves [m0, m1) share unit and leaf size
+struct MoveClass {    // moves [m0, m1) share unit, leaf size and the parts on both sides
   uint32_t m0, m1;
-  uint32_t unit, size;
+  uint16_t unit, size;
+  uint16_t sp, dp;    // src / dst image geometry
 };
-constexpr int kMaxClasses = 16;
+constexpr int kMaxClasses = 32;
 
 struct PermParams {
   uint64_t N;         // records
@@ -159,7 +181,6 @@ struct PermParams {
   uint32_t dst_stage; // bytes of one dst image buffer
   uint32_t ns, nd;    // src stages, dst buffers
   uint32_t src_tile_tma;  // TMA bytes of a full tile's source segments
-  uint32_t unit_end[4];   // moves [0,unit_end[0]) are 8-B units, then 4-, 2-, 1-B units
   uint32_t n_classes;
   MoveClass classes[kMaxClasses];
   uint32_t n_wmoves;     // > 0: AoS <-> AoS word mode (move-parallel) instead of the move classes
@@ -167,8 +188,10 @@ struct PermParams {
   uint32_t tab_bytes;     // shared-memory bytes of the segment tables (16-B multiple)
   uint32_t pad2_;
   PermSide side[2];   // 0 = src, 1 = dst
+  PermPart part[2][kMaxParts];
+  PermGeo geo[2][kMaxParts];
+  PermSeg seg[2][kMaxLeaves];
   DevLeaf leaf[2][kMaxLeaves];
-  uint32_t imgF[2][kMaxLeaves];
   Move moves[kMaxMoves];
   // destination padding outside every tile segment (gaps between the leaf
   // sub-arrays of an aligned SoA single blob): zeroed by CTA 0

@@ -3,10 +3,12 @@
 // alignment; k_permute_ws.cu: warp-specialised TMA pipeline).
 //
 // A tile is T consecutive records.  Each side
-// keeps one shared-memory image per tile: an AoS-like side (L divides T) as the
-// single contiguous byte range of its T/L blocks, a SoA-like side as one
-// segment of T*s_k bytes per leaf.  Inside an image, leaf k of tile record r
-// sits at (r / Limg) * Bimg + imgF_k + (r % Limg) * s_k.
+// keeps one shared-memory image per tile, the images of its parts one after
+// another (a Split has one part per inner mapping): an AoS-like part (L
+// divides T) as the single contiguous byte range of its T/L blocks, a
+// SoA-like part as one segment of T*s_k bytes per leaf.  Inside an image,
+// leaf k of tile record r sits at (r / Limg) * Bimg + imgF_k + (r % Limg) * s_k
+// with its part's Limg / Bimg.
 #pragma once
 #include "device.cuh"
 
@@ -23,26 +25,25 @@ struct Seg {
 // Segment j of side X for the tile starting at record t0 (any tile, clipped
 // to the side's record extent E).
 __device__ __forceinline__ Seg tile_seg(const PermParams& p, int X, uint64_t t0, int j) {
-  const PermSide& S = p.side[X];
-  const uint64_t end = t0 + p.T < S.E ? t0 + p.T : S.E;
+  const PermSeg sg = p.seg[X][j];
+  const PermPart& P = p.part[X][sg.part];
+  const uint64_t end = t0 + p.T < P.E ? t0 + p.T : P.E;
   const uint64_t nrec = end > t0 ? end - t0 : 0;
+  const DevLeaf& l = p.leaf[X][sg.leaf];
   Seg s;
-  if (!S.soa_like) {  // AoS-like: the tile's T/L whole blocks are one range
-    const DevLeaf& l0 = p.leaf[X][0];
-    const uint64_t blk0 = block_of(t0, S.g);
-    s.g = p.blobs[X][l0.blob] + l0.base + blk0 * S.g.B;
-    s.soff = 0;
-    s.len = (uint32_t)(block_of(nrec, S.g) * S.g.B);
-  } else {            // SoA-like: leaf j's T consecutive elements
-    const DevLeaf& l = p.leaf[X][j];
-    s.g = p.blobs[X][l.blob] + nf_offset(t0, S.g, l);
-    s.soff = p.imgF[X][j];
+  s.soff = sg.soff;
+  if (!P.soa_like) {  // AoS-like: the tile's T/L whole blocks are one range
+    const uint64_t blk0 = block_of(t0, P.g);
+    s.g = p.blobs[X][l.blob] + l.base + blk0 * P.g.B;
+    s.len = (uint32_t)(block_of(nrec, P.g) * P.g.B);
+  } else {            // SoA-like: the leaf's T consecutive elements
+    s.g = p.blobs[X][l.blob] + nf_offset(t0, P.g, l);
     s.len = (uint32_t)(nrec * l.size);
   }
   return s;
 }
 
-__device__ __forceinline__ int n_segs(const PermParams& p, int X) { return p.side[X].soa_like ? (int)p.K : 1; }
+__device__ __forceinline__ int n_segs(const PermParams& p, int X) { return (int)p.side[X].n_segs; }
 
 __device__ __forceinline__ uint32_t tile_nrec(const PermParams& p, uint64_t t0) {
   if (t0 >= p.N) return 0;
@@ -106,7 +107,7 @@ __device__ inline void coop_copy(uint8_t* d, const uint8_t* s, uint32_t len, int
 // ------------------------------------------------------------ the permute
 // Record-dependent part of an image offset of record r on one side:
 // base = (r / Limg) * Bimg, mul = r % Limg (multiplies the leaf size).
-__device__ __forceinline__ void rec_addr(const PermSide& S, uint32_t r, uint32_t& base, uint32_t& mul) {
+__device__ __forceinline__ void rec_addr(const PermGeo& S, uint32_t r, uint32_t& base, uint32_t& mul) {
   const uint32_t q = S.limg_shift != kNoShift ? (r >> S.limg_shift) : r / S.Limg;
   mul = r - q * S.Limg;
   base = q * S.Bimg;
@@ -150,7 +151,10 @@ __device__ __forceinline__ void move_class(const PermParams& p, const MoveClass&
 
 // Records r0 + lane_r + j*Tp (j < R) of the tile; for T < 256 the thread
 // groups beyond the first Tp threads split the move table instead (G groups).
-template <int R>
+// kParts: a side has several image geometries (Split parts of different
+// kinds), so the record-dependent offsets are recomputed when the class's
+// geometries differ from the previous class's (classes are ordered by them).
+template <int R, bool kParts>
 __device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t* __restrict__ simg,
                                              uint8_t* __restrict__ dimg, uint32_t nrec, uint32_t r0, int tid) {
   const uint32_t Tp = p.T < (uint32_t)kPermThreads ? p.T : (uint32_t)kPermThreads;
@@ -164,11 +168,22 @@ __device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t*
     const uint32_t r = r0 + lane_r + j * Tp;
     ok[j] = r < nrec;
     all = all && ok[j];
-    rec_addr(p.side[0], r, sb[j], sm[j]);
-    rec_addr(p.side[1], r, db[j], dm[j]);
+    rec_addr(p.geo[0][0], r, sb[j], sm[j]);
+    rec_addr(p.geo[1][0], r, db[j], dm[j]);
   }
+  uint32_t cur_sp = 0, cur_dp = 0;
   for (uint32_t c = 0; c < p.n_classes; ++c) {
     const MoveClass mc = p.classes[c];
+    if (kParts && mc.sp != cur_sp) {
+      cur_sp = mc.sp;
+#pragma unroll
+      for (int j = 0; j < R; ++j) rec_addr(p.geo[0][cur_sp], r0 + lane_r + j * Tp, sb[j], sm[j]);
+    }
+    if (kParts && mc.dp != cur_dp) {
+      cur_dp = mc.dp;
+#pragma unroll
+      for (int j = 0; j < R; ++j) rec_addr(p.geo[1][cur_dp], r0 + lane_r + j * Tp, db[j], dm[j]);
+    }
     switch (mc.unit) {
       case 8: move_class<unsigned long long, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
       case 4: move_class<uint32_t, R>(p, mc, G, grp, simg, dimg, sb, sm, db, dm, ok, all); break;
@@ -196,7 +211,7 @@ __device__ __forceinline__ void permute_words(const PermParams& p, const WordMov
     has[i] = m < p.n_wmoves;
     w[i] = has[i] ? wt[m] : WordMove{0, 0, 0x3210, 0x3210, 0};
   }
-  const uint32_t Bs = p.side[0].Bimg, Bd = p.side[1].Bimg;
+  const uint32_t Bs = p.geo[0][0].Bimg, Bd = p.geo[1][0].Bimg;
   for (uint32_t r = warp; r < nrec; r += kPermThreads / 32) {
     const uint8_t* sr = simg + r * Bs;
     uint8_t* dr = dimg + r * Bd;
@@ -224,19 +239,28 @@ __device__ __forceinline__ void copy_word_table(const PermParams& p, WordMove* w
   for (uint32_t m = tid; m < p.n_wmoves; m += nt) wt[m] = p.wmoves[m];
 }
 
+// kParts: instantiated separately (its own kernel), so the single-geometry
+// kernel keeps its register allocation and code size (measured: a shared
+// kernel with both paths ran 4.5% slower on the C2 pairs).
+template <bool kParts>
 __device__ __forceinline__ void permute_records(const PermParams& p, const WordMove* wt, const uint8_t* simg,
                                                 uint8_t* dimg, uint32_t nrec, int tid) {
-  if (p.n_wmoves) {
+  if (!kParts && p.n_wmoves) {
     permute_words(p, wt, simg, dimg, nrec, tid);
     return;
   }
   uint32_t r0 = 0;
-  for (; r0 + 4 * kPermThreads <= p.T; r0 += 4 * kPermThreads) permute_pass<4>(p, simg, dimg, nrec, r0, tid);
+  for (; r0 + 4 * kPermThreads <= p.T; r0 += 4 * kPermThreads) permute_pass<4, kParts>(p, simg, dimg, nrec, r0, tid);
   if (r0 + 2 * kPermThreads <= p.T) {
-    permute_pass<2>(p, simg, dimg, nrec, r0, tid);
+    permute_pass<2, kParts>(p, simg, dimg, nrec, r0, tid);
     r0 += 2 * kPermThreads;
   }
-  if (r0 < p.T) permute_pass<1>(p, simg, dimg, nrec, r0, tid);
+  if (r0 < p.T) permute_pass<1, kParts>(p, simg, dimg, nrec, r0, tid);
+}
+
+// Several image geometries on a side (planner: n_geo > 1)?
+__host__ __device__ __forceinline__ bool multi_geo(const PermParams& p) {
+  return p.side[0].n_geo > 1 || p.side[1].n_geo > 1;
 }
 
 }  // namespace llb

@@ -38,12 +38,6 @@ bool same_layout(const Mapping& s, const Mapping& d) {
   return true;
 }
 
-DevSide side_of(const Mapping& m) {
-  DevSide ds = m.dev_side();
-  if (m.soa()) ds.lshift = 63;  // one block: i / L == 0 for every valid i
-  return ds;
-}
-
 }  // namespace
 
 llama_status check_compatible(const Mapping& s, const Mapping& d, std::string* err) {
@@ -158,29 +152,35 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
 }
 
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
-  // tiles need one normal form per side (not a Split) with records spread
-  // over the blobs (not One)
-  for (const Mapping* m : {&s, &d})
-    if (!m->uniform || m->kind == LLAMA_ONE) { *why = "split or one mapping"; return false; }
+  // every part must spread its records over its blobs (not One)
+  for (const Mapping* m : {&s, &d}) {
+    if ((int)m->parts.size() > kMaxParts) { *why = "too many split parts"; return false; }
+    for (const Part& q : m->parts)
+      if (q.kind == LLAMA_ONE) { *why = "one mapping"; return false; }
+  }
   const Mapping* side[2] = {&s, &d};
-  bool soa_like[2];
+  std::vector<bool> soa_like[2];  // per part
   uint64_t Tmult = 32;
   std::vector<uint64_t> Tdiv;
-  uint64_t rec_img[2];
+  uint64_t rec_img[2] = {0, 0};
   for (int X = 0; X < 2; ++X) {
     const Mapping& m = *side[X];
-    if (m.soa()) {
-      soa_like[X] = true;
-    } else if (m.B <= kAosLikeMaxBlock) {
-      soa_like[X] = false;
-      Tmult = lcm64(Tmult, m.L);
-    } else {
-      soa_like[X] = true;  // huge AoSoA blocks: a tile stays inside one block
-      Tdiv.push_back(m.L);
+    for (const Part& q : m.parts) {
+      bool sl;
+      if (q.soa()) {
+        sl = true;
+      } else if (q.B <= kAosLikeMaxBlock) {
+        sl = false;
+        Tmult = lcm64(Tmult, q.L);
+      } else {
+        sl = true;  // huge AoSoA blocks: a tile stays inside one block
+        Tdiv.push_back(q.L);
+      }
+      soa_like[X].push_back(sl);
+      uint64_t sum = 0;
+      for (int k : q.leaves) sum += m.sizes[k];
+      rec_img[X] += sl ? sum : q.record_bytes;
     }
-    uint64_t sum = 0;
-    for (auto v : m.sizes) sum += v;
-    rec_img[X] = soa_like[X] ? sum : m.record_bytes;
   }
   if (Tmult > 8192) { *why = "lane counts need tiles above 8192 records"; return false; }
   const uint64_t R = d.E;  // records the destination blobs cover
@@ -229,99 +229,127 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   pp.K = (uint32_t)s.K();
   pp.n_tiles = ceil_div(R, T);
   bool tma = true;
+  std::vector<uint32_t> imgF[2] = {std::vector<uint32_t>(s.K()), std::vector<uint32_t>(s.K())};
+  std::vector<int> part_of[2] = {std::vector<int>(s.K()), std::vector<int>(s.K())};
+  std::vector<int> geo_of[2] = {std::vector<int>(s.K()), std::vector<int>(s.K())};
+  uint64_t full_src = 0;  // TMA bytes of a full tile's source segments (16-B multiples: T % 32 == 0)
   for (int X = 0; X < 2; ++X) {
     const Mapping& m = *side[X];
     PermSide& ps = pp.side[X];
-    ps.g = side_of(m);
     ps.E = m.E;
-    ps.soa_like = soa_like[X] ? 1 : 0;
-    ps.linear = (!soa_like[X] || m.soa()) ? 1 : 0;  // AoS-like or SoA: segment start = a + tile * b
+    ps.n_parts = (uint32_t)m.parts.size();
+    ps.linear = 1;
     for (int k = 0; k < m.K(); ++k) pp.leaf[X][k] = m.dev_leaf(k);
-    uint64_t img;
-    if (!soa_like[X]) {
-      ps.Limg = (uint32_t)m.L;
-      ps.limg_shift = (m.L & (m.L - 1)) == 0 ? (uint32_t)__builtin_ctzll(m.L) : kNoShift;
-      ps.Bimg = (uint32_t)m.B;
-      img = T / m.L * m.B;
-      for (int k = 0; k < m.K(); ++k) pp.imgF[X][k] = (uint32_t)m.F[k];
-      if (m.base[0] % 16 || img % 16) tma = false;
-    } else {
-      ps.Limg = (uint32_t)T;
-      ps.limg_shift = 31;  // r < T: one image block
-      ps.Bimg = 0;
-      uint64_t off = 0;
-      for (int k = 0; k < m.K(); ++k) {
-        off = align16(off);
-        pp.imgF[X][k] = (uint32_t)off;
-        off += T * m.sizes[k];
-        if (m.base[k] % 16) tma = false;
-        if (!m.soa() && (m.F[k] % 16 || m.B % 16)) tma = false;
+    uint64_t off = 0;  // the side image: its parts' images one after another
+    uint32_t ns = 0;
+    for (size_t j = 0; j < m.parts.size(); ++j) {
+      const Part& q = m.parts[j];
+      PermPart& pq = pp.part[X][j];
+      pq.g.L = q.L;
+      pq.g.B = q.B;
+      pq.g.lshift = q.soa() ? 63u : (q.L & (q.L - 1)) == 0 ? (uint32_t)__builtin_ctzll(q.L) : kNoShift;
+      pq.E = q.E;
+      pq.soa_like = soa_like[X][j] ? 1 : 0;
+      if (soa_like[X][j] && !q.soa()) ps.linear = 0;  // large AoSoA blocks: segment starts jump per block
+      // the part's image geometry; parts with equal geometry share one entry
+      PermGeo g{};
+      if (!soa_like[X][j]) {
+        g.Limg = (uint32_t)q.L;
+        g.limg_shift = (q.L & (q.L - 1)) == 0 ? (uint32_t)__builtin_ctzll(q.L) : kNoShift;
+        g.Bimg = (uint32_t)q.B;
+      } else {
+        g.Limg = (uint32_t)T;
+        g.limg_shift = 31;  // r < T: one image block
+        g.Bimg = 0;
       }
-      img = align16(off);
+      uint32_t gi = 0;
+      while (gi < ps.n_geo && !(pp.geo[X][gi].Limg == g.Limg && pp.geo[X][gi].Bimg == g.Bimg)) ++gi;
+      if (gi == ps.n_geo) pp.geo[X][ps.n_geo++] = g;
+      for (int k : q.leaves) {
+        part_of[X][k] = (int)j;
+        geo_of[X][k] = (int)gi;
+      }
+      off = align16(off);
+      if (!soa_like[X][j]) {
+        const uint64_t img = T / q.L * q.B;
+        for (int k : q.leaves) imgF[X][k] = (uint32_t)(off + m.F[k]);
+        pp.seg[X][ns++] = PermSeg{(uint16_t)j, (uint16_t)q.leaves[0], (uint32_t)off};
+        if (m.base[q.leaves[0]] % 16 || img % 16) tma = false;
+        if (X == 0) full_src += img;
+        off += img;
+      } else {
+        for (int k : q.leaves) {
+          off = align16(off);
+          imgF[X][k] = (uint32_t)off;
+          pp.seg[X][ns++] = PermSeg{(uint16_t)j, (uint16_t)k, (uint32_t)off};
+          off += T * m.sizes[k];
+          if (m.base[k] % 16) tma = false;
+          if (!q.soa() && (m.F[k] % 16 || q.B % 16)) tma = false;
+          if (X == 0) full_src += T * m.sizes[k];
+        }
+      }
     }
-    ps.img_bytes = (uint32_t)img;
+    ps.n_segs = ns;
+    ps.img_bytes = (uint32_t)align16(off);
   }
   if (env_u64("LLAMA_NO_TMA", 0)) tma = false;
   pp.tma = tma ? 1 : 0;
-  {
-    uint64_t full_src = 0;  // every full-tile segment length is a 16-B multiple (T % 32 == 0)
-    if (soa_like[0])
-      for (int k = 0; k < s.K(); ++k) full_src += T * s.sizes[k];
-    else
-      full_src = T / s.L * s.B;
-    pp.src_tile_tma = (uint32_t)full_src;
-  }
+  pp.src_tile_tma = (uint32_t)full_src;
   pp.src_stage = (uint32_t)align16(pp.side[0].img_bytes);
   pp.dst_stage = (uint32_t)align16(pp.side[1].img_bytes);
   // per-record move table: leaf k moves in units of the widest power of two
-  // that divides its size and both image offsets for every record; grouped by
-  // unit (8, 4, 2, 1 bytes) so the kernel runs one branch-free loop per unit
-  // classes by (unit, leaf size): within a class the record-dependent part of
-  // an image offset is the same for every move, so the kernel hoists it
-  std::vector<Move> mv[4][4];  // [unit class][size class]
+  // that divides its size and both image offsets for every record; classes
+  // by (src geometry, dst geometry, unit, leaf size): within a class the
+  // record-dependent part of an image offset is the same for every move, so
+  // the kernel hoists it, and recomputes it only when the geometries change
+  std::vector<Move> mv[kMaxParts][kMaxParts][4][4];  // [src geo][dst geo][unit][size]
   auto lg = [](uint64_t v) { return v == 8 ? 0 : v == 4 ? 1 : v == 2 ? 2 : 3; };
   for (int k = 0; k < s.K(); ++k) {
     uint64_t unit = std::min<uint64_t>(8, s.sizes[k]);
     for (int X = 0; X < 2; ++X) {
-      const PermSide& ps = pp.side[X];
-      uint64_t a = std::min<uint64_t>(16, lowbit(pp.imgF[X][k]));
-      if (ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(s.sizes[k]));
-      if (T / ps.Limg > 1) a = std::min<uint64_t>(a, lowbit(ps.Bimg));
+      const PermGeo& pq = pp.geo[X][geo_of[X][k]];
+      uint64_t a = std::min<uint64_t>(16, lowbit(imgF[X][k]));
+      if (pq.Limg > 1) a = std::min<uint64_t>(a, lowbit(s.sizes[k]));
+      if (T / pq.Limg > 1) a = std::min<uint64_t>(a, lowbit(pq.Bimg));
       unit = std::min(unit, a);
     }
     for (uint64_t j = 0; j < s.sizes[k] / unit; ++j) {
       Move m;
-      m.soff = (uint32_t)(pp.imgF[0][k] + j * unit);
-      m.doff = (uint32_t)(pp.imgF[1][k] + j * unit);
+      m.soff = (uint32_t)(imgF[0][k] + j * unit);
+      m.doff = (uint32_t)(imgF[1][k] + j * unit);
       m.size = (uint16_t)s.sizes[k];
       m.unit = (uint8_t)unit;
       m.pad_ = 0;
-      mv[lg(unit)][lg(s.sizes[k])].push_back(m);
+      mv[geo_of[0][k]][geo_of[1][k]][lg(unit)][lg(s.sizes[k])].push_back(m);
     }
   }
   uint32_t nm = 0;
   pp.n_classes = 0;
-  for (int c = 0; c < 4; ++c) {
-    for (int z = 0; z < 4; ++z) {
-      if (mv[c][z].empty()) continue;
-      MoveClass& mc = pp.classes[pp.n_classes++];
-      mc.m0 = nm;
-      for (auto& m : mv[c][z]) {
-        if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
-        pp.moves[nm++] = m;
-      }
-      mc.m1 = nm;
-      mc.unit = 8u >> c;
-      mc.size = 8u >> z;
-    }
-    pp.unit_end[c] = nm;
-  }
+  for (int a = 0; a < kMaxParts; ++a)
+    for (int b = 0; b < kMaxParts; ++b)
+      for (int c = 0; c < 4; ++c)
+        for (int z = 0; z < 4; ++z) {
+          if (mv[a][b][c][z].empty()) continue;
+          if (pp.n_classes >= (uint32_t)kMaxClasses) { *why = "too many move classes"; return false; }
+          MoveClass& mc = pp.classes[pp.n_classes++];
+          mc.m0 = nm;
+          for (auto& m : mv[a][b][c][z]) {
+            if (nm >= (uint32_t)kMaxMoves) { *why = "move table too long"; return false; }
+            pp.moves[nm++] = m;
+          }
+          mc.m1 = nm;
+          mc.unit = (uint16_t)(8u >> c);
+          mc.size = (uint16_t)(8u >> z);
+          mc.sp = (uint16_t)a;
+          mc.dp = (uint16_t)b;
+        }
   // AoS <-> AoS word mode for wide records (both sides plain AoS, strides
   // multiples of 4, >= 64 destination words per record): each destination
   // word is built from a <= 12-byte source window; lanes own words, so both
   // images are read/written contiguously (no bank conflicts at any stride).
   pp.n_wmoves = 0;
-  if (!soa_like[0] && !soa_like[1] && s.L == 1 && d.L == 1 && s.B % 4 == 0 && d.B % 4 == 0 &&
+  if (s.parts.size() == 1 && d.parts.size() == 1 && !soa_like[0][0] && !soa_like[1][0] && s.L == 1 &&
+      d.L == 1 && s.B % 4 == 0 && d.B % 4 == 0 &&
       env_u64("LLAMA_WORD_MODE", 1)) {
     std::vector<int64_t> src_of(d.B, -1);
     for (int k = 0; k < s.K(); ++k)
@@ -372,12 +400,19 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   pp.n_moves = nm;
 
   // destination padding no tile segment covers: the gaps between aligned
-  // SoA single-blob sub-arrays (reading #9); blocked SoA-like sides with
-  // gaps inside a block are left to the naive path
-  if (soa_like[1] && d.has_padding()) {
-    if (d.kind != LLAMA_SOA_SINGLE_BLOB) { *why = "padded large-block destination"; return false; }
+  // SoA single-blob sub-arrays (reading #9); blocked SoA-like parts with
+  // padding (tail block, aligned records) are left to the naive path
+  for (size_t j = 0; j < d.parts.size(); ++j) {
+    const Part& q = d.parts[j];
+    if (!soa_like[1][j] || q.kind == LLAMA_SOA_MULTI_BLOB) continue;
+    if (q.kind != LLAMA_SOA_SINGLE_BLOB) {
+      uint64_t sum = 0;
+      for (int k : q.leaves) sum += d.sizes[k];
+      if (q.E != d.N || q.record_bytes != sum) { *why = "padded large-block destination"; return false; }
+      continue;
+    }
     uint64_t end = 0;
-    for (int k = 0; k < d.K(); ++k) {
+    for (int k : q.leaves) {
       if (d.base[k] > end) {
         pp.gap_blob[pp.n_gaps] = d.blob[k];
         pp.gap_off[pp.n_gaps] = end;

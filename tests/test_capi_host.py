@@ -211,4 +211,13 @@ def test_split_errors_and_plans():
     one1 = llama.Mapping(W.LISTING1, [1], "one")
     llama.plan(llama.Mapping(W.LISTING1, [1]), one1)  # one record: no collision
     sp = llama.Mapping.from_spec(W.LISTING1, [4], W.resolve_spec("split_pos"))
-    assert llama.plan(sp, sp)["path"] == "blobcopy"
+    assert llama.plan(sp, sp, path="blobcopy")["path"] == "blobcopy"
+    # splits whose parts all spread records over blobs take the tile permute (parts per side)
+    big = [1 << 20]
+    for name, other in (("split_p7", "aos"), ("split_p7", "soa_mb"), ("split_pos", "aos_aligned"),
+                        ("split_hep", "aos")):
+        schema = W.SCHEMAS[W.SPLITS[name][0]]
+        a = llama.Mapping.from_spec(schema, big, W.resolve_spec(name))
+        b = llama.Mapping(schema, big, *W.MAPPINGS[other])
+        assert llama.plan(a, b)["path"] == "permute", (name, other)
+        assert llama.plan(b, a)["path"] == "permute", (other, name)

@@ -1,0 +1,10 @@
+#!/bin/bash
+# A/B over the 16 C2 pairs: old build (tools/ab_old) vs current, alternating, same box.
+P=aos:aos,aos:soa_mb,aos:aosoa8,aos:aosoa32,soa_mb:aos,soa_mb:soa_mb,soa_mb:aosoa8,soa_mb:aosoa32,aosoa8:aos,aosoa8:soa_mb,aosoa8:aosoa8,aosoa8:aosoa32,aosoa32:aos,aosoa32:soa_mb,aosoa32:aosoa8,aosoa32:aosoa32
+for rep in 1 2; do  # VARIANTS='old exp new' adds tools/ab_exp
+ for v in ${VARIANTS:-old new}; do
+  case $v in old) R=tools/ab_old;; exp) R=tools/ab_exp;; *) R=;; esac
+  echo "== $v rep$rep"
+  LLAMA_PKG_ROOT=$R python tools/profile_pairs.py --pairs $P --iters 10 | awk '{print $1, $3, $(NF-3), $(NF-1)}'
+ done
+done
