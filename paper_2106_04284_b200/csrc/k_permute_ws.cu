@@ -1,14 +1,18 @@
 // k_permute_ws.cu -- the warp-specialised TMA tile permute (the hot kernel).
 //
 // 8 consumer warps permute tiles back to back; 1 producer warp drives the TMA
-// (cp.async.bulk loads into an ns-stage source ring, bulk stores out of two
-// destination buffers).  Four mbarrier rings replace block-wide barriers:
+// (cp.async.bulk loads into an ns-stage source ring, bulk stores out of nd =
+// 2 or 3 destination buffers).  Four mbarrier rings replace block-wide barriers:
 //   full[s]   TMA bytes of a tile landed in source stage s   (producer -> consumers)
 //   empty[s]  consumers finished reading source stage s      (consumers -> producer)
 //   dfull[d]  consumers finished writing destination buffer d (consumers -> producer)
 //   dempty[d] the bulk store out of buffer d has read it out  (producer -> consumers)
 // so the permute of tile i overlaps the stores of tile i-1 and the loads of
 // tiles i+1 .. i+ns-1, and no warp waits for another's issue work.
+// Producer order per tile (p.order, measured on B200): 2 = refill
+// load of stage s first, then the stores of tile i (default; C2 +3-5% over
+// stores-first); with nd >= 3 the buffer of tile i-1 is handed back once its
+// store has been read out, keeping one store in flight.
 // Requires 16-byte aligned segment starts (planner: tma = 1).
 #include <cstdlib>
 
@@ -18,22 +22,24 @@
 namespace llb {
 
 namespace {
-constexpr int kConsumerWarps = kPermThreads / 32;        // 8
-constexpr int kThreadsWS = kPermThreads + 32;            // + 1 producer warp
-constexpr int kBarBytes = 128;                           // 4 rings x <= 4 x 8 B
+constexpr int kBarBytes = 128;  // 4 rings x <= 4 x 8 B
 }  // namespace
 
+// NC consumer threads (8 or 16 warps) + 1 producer warp
+template <int NC>
 __device__ __forceinline__ void named_sync_consumers() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kPermThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
 }
 
-template <bool kParts>
-__global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_constant__ PermParams p) {
+template <bool kParts, int NC>
+__global__ void __launch_bounds__(NC + 32, NC == 256 ? 3 : 1) k_permute_ws(const __grid_constant__ PermParams p) {
+  constexpr int kConsumerWarps = NC / 32;
+  constexpr int kThreadsWS = NC + 32;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 4;
-  uint64_t* dfull = full + 8;
-  uint64_t* dempty = full + 10;
+  uint64_t* dfull = full + 8;  // ns <= 4 source stages, nd <= 4 destination buffers
+  uint64_t* dempty = full + 12;
   SSeg* sseg = reinterpret_cast<SSeg*>(smem + kBarBytes);
   SSeg* dseg = sseg + p.K;
   uint8_t* sbuf = smem + kBarBytes + p.tab_bytes;
@@ -52,7 +58,7 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int d = 0; d < 2; ++d) {
+    for (uint32_t d = 0; d < p.nd; ++d) {
       mbar_init(&dfull[d], 1);
       mbar_init(&dempty[d], 1);
     }
@@ -68,7 +74,7 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
 
   if (blockIdx.x == 0 && warp < kConsumerWarps)
     for (uint32_t g = 0; g < p.n_gaps; ++g)
-      for (uint32_t o = tid; o < p.gap_len[g]; o += kPermThreads) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
+      for (uint32_t o = tid; o < p.gap_len[g]; o += NC) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
 
   const uint64_t first = blockIdx.x, stride = gridDim.x;
   const uint64_t n_full = p.N / p.T;
@@ -76,10 +82,11 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer
-    auto load = [&](uint32_t i) {
+    // ring positions advance incrementally (no division by the runtime ns / nd
+    // on the producer's per-tile critical path)
+    auto load = [&](uint32_t i, uint32_t s) {
       const uint64_t tile = first + (uint64_t)i * stride;
       const bool fl = tile < n_full;
-      const uint32_t s = i % p.ns;
       uint8_t* img = sbuf + (size_t)s * p.src_stage;
       const int ns = n_segs(p, 0);
       uint32_t total = p.src_tile_tma;
@@ -95,13 +102,21 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
         if (body) bulk_g2s(img + sg.soff, sg.g, body, &full[s]);
       }
     };
-    for (uint32_t i = 0; i < p.ns && i < n_my; ++i) load(i);
+    for (uint32_t i = 0; i < p.ns && i < n_my; ++i) load(i, i);
     const int nds = n_segs(p, 1);
+    uint32_t s = 0, sph = 0, d = 0, dph = 0, dprev = p.nd - 1;
     for (uint32_t i = 0; i < n_my; ++i) {
       const uint64_t tile = first + (uint64_t)i * stride;
       const bool fl = tile < n_full;
-      const uint32_t d = i & 1;
-      if (lane == 0) mbar_wait(&dfull[d], (i >> 1) & 1);
+      auto refill = [&]() {  // refill the source stage tile i used
+        if (i + p.ns < n_my) {
+          if (lane == 0) mbar_wait(&empty[s], sph);
+          __syncwarp();
+          load(i + p.ns, s);
+        }
+      };
+      if (p.order == 2) refill();
+      if (lane == 0) mbar_wait(&dfull[d], dph);
       __syncwarp();
       uint8_t* dimg = dbuf + (size_t)d * p.dst_stage;
       for (int j = lane; j < nds; j += 32) {
@@ -110,70 +125,88 @@ __global__ void __launch_bounds__(kThreadsWS, 3) k_permute_ws(const __grid_const
         if (body) bulk_s2g(sg.g, dimg + sg.soff, body);
       }
       bulk_commit();
-      if (i + p.ns < n_my) {  // refill the source stage tile i used
-        if (lane == 0) mbar_wait(&empty[i % p.ns], (i / p.ns) & 1);
+      if (p.order == 1 && p.nd == 2) {  // release buffer d before refilling
+        bulk_wait_read<0>();
         __syncwarp();
-        load(i + p.ns);
+        if (lane == 0) mbar_arrive(&dempty[d]);
       }
-      // hand buffer d back as soon as the store has read it out (the
-      // consumers meanwhile fill the other buffer)
-      bulk_wait_read<0>();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dempty[d]);
+      if (p.order != 2) refill();
+      if (p.order == 1 && p.nd == 2) {
+      } else if (p.nd == 2) {
+        // hand buffer d back as soon as the store has read it out (the
+        // consumers meanwhile fill the other buffer)
+        bulk_wait_read<0>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[d]);
+      } else if (i > 0) {
+        // >= 3 buffers: keep this tile's store in flight, hand back the previous one's
+        bulk_wait_read<1>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[dprev]);
+      }
+      dprev = d;
+      if (++s == p.ns) { s = 0; sph ^= 1; }
+      if (++d == p.nd) { d = 0; dph ^= 1; }
     }
     bulk_wait_all();
     return;
   }
 
   // ------------------------------------------------------------- consumers
+  uint32_t s = 0, sph = 0, d = 0, dph = 0;
   for (uint32_t i = 0; i < n_my; ++i) {
     const uint64_t tile = first + (uint64_t)i * stride;
     const uint64_t t0 = tile * p.T;
     const bool fl = tile < n_full;
-    const uint32_t s = i % p.ns, d = i & 1;
     uint8_t* simg = sbuf + (size_t)s * p.src_stage;
     uint8_t* dimg = dbuf + (size_t)d * p.dst_stage;
     if (tid == 0) {  // one consumer thread waits, the others sleep in the named barrier
-      mbar_wait(&full[s], (i / p.ns) & 1);
-      mbar_wait(&dempty[d], ((i >> 1) & 1) ^ 1);  // first use of each buffer passes
+      mbar_wait(&full[s], sph);
+      mbar_wait(&dempty[d], dph ^ 1);  // first use of each buffer passes
     }
-    named_sync_consumers();
+    named_sync_consumers<NC>();
     uint32_t nrec = p.T;
     if (!fl) {  // last, partial tile: source tails, zeroed destination image
       nrec = tile_nrec(p, t0);
       for (int j = 0; j < n_segs(p, 0); ++j) {
         const Seg sg = tile_seg(p, 0, t0, j);
-        for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += kPermThreads) simg[sg.soff + o] = sg.g[o];
+        for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += NC) simg[sg.soff + o] = sg.g[o];
       }
-      for (uint32_t o = 16 * tid; o < p.dst_stage; o += 16 * kPermThreads)
+      for (uint32_t o = 16 * tid; o < p.dst_stage; o += 16 * NC)
         *reinterpret_cast<uint4*>(dimg + o) = make_uint4(0, 0, 0, 0);
-      named_sync_consumers();
+      named_sync_consumers<NC>();
     }
-    permute_records<kParts>(p, wt, simg, dimg, nrec, tid);
+    permute_records<kParts, NC>(p, wt, simg, dimg, nrec, tid);
     if (!fl) {  // destination tails (sub-16-byte) go out directly
-      named_sync_consumers();
+      named_sync_consumers<NC>();
       for (int j = 0; j < n_segs(p, 1); ++j) {
         const Seg sg = tile_seg(p, 1, t0, j);
-        for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += kPermThreads) sg.g[o] = dimg[sg.soff + o];
+        for (uint32_t o = (sg.len & ~15u) + tid; o < sg.len; o += NC) sg.g[o] = dimg[sg.soff + o];
       }
     }
     fence_proxy_async_smem();  // generic-proxy image writes -> TMA store reads
-    named_sync_consumers();
+    named_sync_consumers<NC>();
     if (tid == 0) {
       mbar_arrive(&empty[s]);
       mbar_arrive(&dfull[d]);
     }
+    if (++s == p.ns) { s = 0; sph ^= 1; }
+    if (++d == p.nd) { d = 0; dph ^= 1; }
   }
 }
 
 int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
+  // 8 consumer warps (measured: 16 in one CTA are no faster for small
+  // records and halve the speed of wide ones, which lose their 2 CTAs per SM)
   static LaunchCache cache[2][64];
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   current_device_sms(&sms);
-  const bool parts = multi_geo(p);
-  auto kern = parts ? k_permute_ws<true> : k_permute_ws<false>;
-  int e = prepare_kernel(kern, kThreadsWS, smem_bytes, &cache[parts][dev & 63], &per_sm);
+  const int v = multi_geo(p) ? 1 : 0;
+  void (*const kerns[2])(PermParams) = {k_permute_ws<false, kPermThreads>, k_permute_ws<true, kPermThreads>};
+  auto kern = kerns[v];
+  const int kThreadsWS = kPermThreads + 32;
+  int e = prepare_kernel(kern, kThreadsWS, smem_bytes, &cache[v][dev & 63], &per_sm);
   if (e) return e;
   uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
   if (grid > p.n_tiles) grid = p.n_tiles;

@@ -180,6 +180,7 @@ struct PermParams {
   uint32_t src_stage; // bytes of one src image buffer (16-B multiple)
   uint32_t dst_stage; // bytes of one dst image buffer
   uint32_t ns, nd;    // src stages, dst buffers
+  uint32_t order;     // producer: 1 = release the dst buffer before the refill load
   uint32_t src_tile_tma;  // TMA bytes of a full tile's source segments
   uint32_t n_classes;
   MoveClass classes[kMaxClasses];

@@ -154,11 +154,11 @@ __device__ __forceinline__ void move_class(const PermParams& p, const MoveClass&
 // kParts: a side has several image geometries (Split parts of different
 // kinds), so the record-dependent offsets are recomputed when the class's
 // geometries differ from the previous class's (classes are ordered by them).
-template <int R, bool kParts>
+template <int R, bool kParts, int NT>
 __device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t* __restrict__ simg,
                                              uint8_t* __restrict__ dimg, uint32_t nrec, uint32_t r0, int tid) {
-  const uint32_t Tp = p.T < (uint32_t)kPermThreads ? p.T : (uint32_t)kPermThreads;
-  const uint32_t G = (uint32_t)kPermThreads / Tp;
+  const uint32_t Tp = p.T < (uint32_t)NT ? p.T : (uint32_t)NT;
+  const uint32_t G = (uint32_t)NT / Tp;
   const uint32_t lane_r = (uint32_t)tid % Tp, grp = (uint32_t)tid / Tp;
   uint32_t sb[R], sm[R], db[R], dm[R];
   bool ok[R];
@@ -199,6 +199,7 @@ __device__ __forceinline__ void permute_pass(const PermParams& p, const uint8_t*
 // record stride (the 480-B aligned HEP record gives 8-way conflicts in the
 // record-parallel mapping).
 // (table: the per-CTA shared copy, see word_table())
+template <int NT>
 __device__ __forceinline__ void permute_words(const PermParams& p, const WordMove* __restrict__ wt,
                                               const uint8_t* __restrict__ simg, uint8_t* __restrict__ dimg,
                                               uint32_t nrec, int tid) {
@@ -212,7 +213,7 @@ __device__ __forceinline__ void permute_words(const PermParams& p, const WordMov
     w[i] = has[i] ? wt[m] : WordMove{0, 0, 0x3210, 0x3210, 0};
   }
   const uint32_t Bs = p.geo[0][0].Bimg, Bd = p.geo[1][0].Bimg;
-  for (uint32_t r = warp; r < nrec; r += kPermThreads / 32) {
+  for (uint32_t r = warp; r < nrec; r += NT / 32) {
     const uint8_t* sr = simg + r * Bs;
     uint8_t* dr = dimg + r * Bd;
 #pragma unroll
@@ -242,20 +243,20 @@ __device__ __forceinline__ void copy_word_table(const PermParams& p, WordMove* w
 // kParts: instantiated separately (its own kernel), so the single-geometry
 // kernel keeps its register allocation and code size (measured: a shared
 // kernel with both paths ran 4.5% slower on the C2 pairs).
-template <bool kParts>
+template <bool kParts, int NT = kPermThreads>
 __device__ __forceinline__ void permute_records(const PermParams& p, const WordMove* wt, const uint8_t* simg,
                                                 uint8_t* dimg, uint32_t nrec, int tid) {
   if (!kParts && p.n_wmoves) {
-    permute_words(p, wt, simg, dimg, nrec, tid);
+    permute_words<NT>(p, wt, simg, dimg, nrec, tid);
     return;
   }
   uint32_t r0 = 0;
-  for (; r0 + 4 * kPermThreads <= p.T; r0 += 4 * kPermThreads) permute_pass<4, kParts>(p, simg, dimg, nrec, r0, tid);
-  if (r0 + 2 * kPermThreads <= p.T) {
-    permute_pass<2, kParts>(p, simg, dimg, nrec, r0, tid);
-    r0 += 2 * kPermThreads;
+  for (; r0 + 4 * NT <= p.T; r0 += 4 * NT) permute_pass<4, kParts, NT>(p, simg, dimg, nrec, r0, tid);
+  if (r0 + 2 * NT <= p.T) {
+    permute_pass<2, kParts, NT>(p, simg, dimg, nrec, r0, tid);
+    r0 += 2 * NT;
   }
-  if (r0 < p.T) permute_pass<1, kParts>(p, simg, dimg, nrec, r0, tid);
+  if (r0 < p.T) permute_pass<1, kParts, NT>(p, simg, dimg, nrec, r0, tid);
 }
 
 // Several image geometries on a side (planner: n_geo > 1)?

@@ -5,6 +5,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("LLAMA_PKG_ROOT"):  # A/B against another build of the package
+    sys.path.insert(0, os.environ["LLAMA_PKG_ROOT"])
 import torch  # noqa: E402
 
 import paper_2106_04284_b200 as llama  # noqa: E402
@@ -13,7 +15,7 @@ import workloads as W  # noqa: E402
 N = 1 << 24
 S = W.PARTICLE7
 SPECS = {
-    "aos": ("aos", 1, False), "soa_mb": ("soa_mb", 1, False), "aosoa8": ("aosoa", 8, False),
+    "aos": ("aos", 1, False), "soa_mb": ("soa_mb", 1, False), "aosoa8": ("aosoa", 8, False), "aosoa32": ("aosoa", 32, False),
     "split_mb_mb": ([0, 1, 2], ("soa_mb", 1, False), ("soa_mb", 1, False)),
     "split_mb_aos": ([0, 1, 2], ("soa_mb", 1, False), ("aos", 1, False)),
     "split_mb_a8": ([0, 1, 2], ("soa_mb", 1, False), ("aosoa", 8, False)),
