@@ -29,7 +29,7 @@ def build(force=False):
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
         return _LIB
     tmp = _LIB + f".tmp{os.getpid()}"
-    subprocess.check_call(["gcc", "-O3", "-std=c11", "-fopenmp", "-fPIC", "-shared",
+    subprocess.check_call(["gcc", "-O3", "-std=c11", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
                            "-Wall", "-Wextra", "-o", tmp, _SRC])
     os.replace(tmp, _LIB)
     return _LIB
@@ -84,6 +84,8 @@ def lib():
         _lib.oracle_copy_range.argtypes = [M, u8pp, P(ctypes.c_uint64), M, u8pp,
                                            P(ctypes.c_uint64), ctypes.c_int64, ctypes.c_int64]
         _lib.oracle_copy.argtypes = [M, u8pp, M, u8pp, ctypes.c_int32]
+        _lib.oracle_nbody_move.argtypes = [M, u8pp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
+                                           ctypes.c_int64, ctypes.c_int64]
     return _lib
 
 
@@ -248,3 +250,16 @@ def copy_range(src, src_blobs, src_base, dst, dst_blobs, dst_base, i0, i1):
     if rc != 0:
         raise ValueError(f"oracle_copy_range failed rc={rc}")
     return rc
+
+
+def nbody_move(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), i0=0, i1=None):
+    """n-body move (Listing P:643-645) in place on m's blobs: Pos += Vel * dt
+    in f32 (two roundings).  Default leaves: Particle7's Pos.X..Z, Vel.X..Z."""
+    if i1 is None:
+        i1 = m.record_count
+    p3 = (ctypes.c_int32 * 3)(*pos)
+    v3 = (ctypes.c_int32 * 3)(*vel)
+    rc = lib().oracle_nbody_move(m.ref, _u8pp(blobs), p3, v3, ctypes.c_float(dt), int(i0), int(i1))
+    if rc != 0:
+        raise ValueError(f"oracle_nbody_move failed rc={rc}")
+    return blobs

@@ -416,3 +416,36 @@ int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
   addr_ctx_free(&cd);
   return 0;
 }
+
+/* Listing P:643-645: particles(i)(Pos{}) += particles(i)(Vel{}) * TIMESTEP, per
+ * component, FP = float.  Two roundings: t = v * dt, then p + t
+ * (reading #25; the library builds this file with -ffp-contract=off so the
+ * compiler cannot fuse them). */
+int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos, const int32_t* vel,
+                      float dt, int64_t i0, int64_t i1) {
+  if (oracle_validate(m)) return -1;
+  int64_t n = oracle_record_count(m);
+  if (i0 < 0 || i1 > n || i0 > i1) return -1;
+  for (int c = 0; c < 3; ++c) {
+    if (pos[c] < 0 || pos[c] >= m->n_leaves || vel[c] < 0 || vel[c] >= m->n_leaves) return -1;
+    if (m->leaf_size[pos[c]] != 4 || m->leaf_size[vel[c]] != 4) return -1;
+  }
+  addr_ctx c;
+  addr_ctx_init(&c, m);
+  for (int64_t i = i0; i < i1; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      int32_t bp, bv;
+      uint64_t op, ov;
+      addr_of(&c, (uint64_t)i, pos[k], &bp, &op);
+      addr_of(&c, (uint64_t)i, vel[k], &bv, &ov);
+      float p, v;
+      memcpy(&p, blobs[bp] + op, 4);
+      memcpy(&v, blobs[bv] + ov, 4);
+      float t = v * dt;
+      p = p + t;
+      memcpy(blobs[bp] + op, &p, 4);
+    }
+  }
+  addr_ctx_free(&c);
+  return 0;
+}

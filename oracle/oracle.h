@@ -104,6 +104,17 @@ int oracle_copy_range(const oracle_mapping* src, const uint8_t* const* src_blobs
 int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
                 const oracle_mapping* dst, uint8_t* const* dst_blobs, int32_t nthreads);
 
+/* n-body move (Listing P:643-645, §4.1), FP = float
+ * (P:618): for every particle i in [i0, i1) and c in {X, Y, Z}
+ *   Pos_c(i) = Pos_c(i) + Vel_c(i) * dt
+ * in f32 with two roundings (the product, then the sum; DESIGN.md reading
+ * #25), reading and writing through the oracle's own address function.
+ * pos[3] / vel[3] are the leaf indices of Pos.{X,Y,Z} / Vel.{X,Y,Z}; those
+ * leaves must be 4 bytes.  Every other byte is left as it is.
+ * Returns 0, or -1 for an invalid mapping / leaf / range. */
+int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos, const int32_t* vel,
+                      float dt, int64_t i0, int64_t i1);
+
 #ifdef __cplusplus
 }
 #endif

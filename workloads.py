@@ -81,3 +81,32 @@ def resolve_spec(spec):
         return spec
     leaves_a, a, b = spec
     return (list(leaves_a), resolve_spec(a), resolve_spec(b))
+
+
+# ------------------------------------------------------------- n-body (f3)
+# Listing P:617-619: FP = float, TIMESTEP = 0.0001f.  Initial state (S:685,
+# the paper gives none): Pos, Vel uniform in [-1, 1), Mass in (0, 1], drawn
+# from splitmix64 hashes as u = (h >> 40) * 2^-24, exact in f32.
+NBODY_TIMESTEP = 0.0001
+NBODY_MOVE_N = 1 << 28  # "Move with 256Mi particles"
+
+
+def _splitmix64_np(x):
+    import numpy as np
+    z = (x + np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+    z = ((z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)).astype(np.uint64)
+    z = ((z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)).astype(np.uint64)
+    return z ^ (z >> np.uint64(31))
+
+
+def particle_values(n, seed=42, i0=0):
+    """(n, 7) float32: Pos.X..Z, Vel.X..Z, Mass of particles i0 .. i0+n-1 (Particle7 leaf order)."""
+    import numpy as np
+    with np.errstate(over="ignore"):
+        i = np.arange(i0, i0 + n, dtype=np.uint64)[:, None] * np.uint64(7) + np.arange(7, dtype=np.uint64)[None, :]
+        h = _splitmix64_np(i ^ np.uint64(seed))
+    u = (h >> np.uint64(40)).astype(np.float64) * 2.0 ** -24
+    out = np.empty((n, 7), dtype=np.float32)
+    out[:, :6] = (2.0 * u[:, :6] - 1.0).astype(np.float32)
+    out[:, 6] = (1.0 - u[:, 6]).astype(np.float32)
+    return out
