@@ -233,6 +233,33 @@ void llama_stager_destroy(llama_stager* st); /* NULL-safe; synchronises its stre
 llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
                                const llama_mapping* dst_map, void* const* dst_blobs, void* stream);
 
+/* ------------------------------------------------------------------------
+ * n-body move (Listing P:643-645, §4.1, §4.2
+ * P:698-743): in place on one view, for every particle i and c in {X,Y,Z}
+ *     Pos_c(i) = Pos_c(i) + Vel_c(i) * dt
+ * in f32 with two roundings (product, then sum; reading #25).
+ * pos_leaves[3] / vel_leaves[3]: leaf indices (DFS order) of Pos.{X,Y,Z} and
+ * Vel.{X,Y,Z}; all six must be 4-byte leaves (f32).  Only Pos bytes change
+ * value (the AoS kernel rewrites whole records with their own bytes).
+ * Paths (llama_move_path): GENERIC = thread per particle through the
+ * mapping's address function (any mapping); RUNS = 4 consecutive particles
+ * per thread as 16-byte vectors of each leaf (every Pos/Vel leaf laid out in
+ * 16-byte aligned runs of >= 4 records: SoA, AoSoA with L % 4 == 0, splits of
+ * those); AOS = records of one packed/aligned AoS part staged through shared
+ * memory with coalesced 16-byte accesses (record size a multiple of 4).
+ * Blobs: device memory, 16-byte aligned (as llama_copy).
+ * Errors: INVALID_ARGUMENT (NULL, bad leaf index, non-4-byte leaf, a leaf
+ * listed twice), UNSUPPORTED (forced path not applicable; a mapping that maps
+ * several particles onto one place), ALIGNMENT, CUDA. */
+typedef enum { LLAMA_MOVE_AUTO = 0, LLAMA_MOVE_GENERIC = 1, LLAMA_MOVE_RUNS = 2, LLAMA_MOVE_AOS = 3 } llama_move_path;
+llama_status llama_nbody_move(const llama_mapping* m, void* const* blobs, const int32_t* pos_leaves,
+                              const int32_t* vel_leaves, float dt, void* stream);
+/* The same with a forced path (AUTO = planner's choice); *path_used (may be
+ * NULL) receives the path that ran. */
+llama_status llama_nbody_move_ex(const llama_mapping* m, void* const* blobs, const int32_t* pos_leaves,
+                                 const int32_t* vel_leaves, float dt, llama_move_path path,
+                                 llama_move_path* path_used, void* stream);
+
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t llama_launch_count(void);
 

@@ -35,7 +35,10 @@ EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_ma
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
            "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
-           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged"]
+           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_nbody_move",
+           "llama_nbody_move_ex"]
+MOVE_PATHS = {"auto": 0, "generic": 1, "runs": 2, "aos": 3}
+MOVE_PATH_NAMES = {v: k for k, v in MOVE_PATHS.items()}
 
 
 class LlamaError(RuntimeError):
@@ -93,6 +96,10 @@ def _load():
     lib.llama_copy_staged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
     lib.llama_launch_count.restype = ctypes.c_uint64
     lib.llama_status_string.restype = ctypes.c_char_p
+    lib.llama_nbody_move.argtypes = [ctypes.c_void_p, vpp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
+                                     ctypes.c_void_p]
+    lib.llama_nbody_move_ex.argtypes = [ctypes.c_void_p, vpp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
+                                        ctypes.c_int, P(ctypes.c_int), ctypes.c_void_p]
     lib.llama_status_string.argtypes = [ctypes.c_int]
     lib.llama_last_error_message.restype = ctypes.c_char_p
     lib.llama_version.restype = ctypes.c_char_p
@@ -317,3 +324,16 @@ def launch_count():
 
 def version():
     return _lib.llama_version().decode()
+
+
+def nbody_move(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), path="auto", stream=None):
+    """n-body move in place (llama_nbody_move_ex; Listing P:643-645):
+    Pos += Vel * dt in f32 on device blobs.  Default leaves: Particle7's
+    Pos.X..Z and Vel.X..Z.  Returns the path that ran."""
+    ptrs = _ptrs(blobs, m.blob_sizes(), "blobs")
+    p3 = (ctypes.c_int32 * 3)(*pos)
+    v3 = (ctypes.c_int32 * 3)(*vel)
+    used = ctypes.c_int(0)
+    _check(_lib.llama_nbody_move_ex(m.handle, ptrs, p3, v3, ctypes.c_float(dt), MOVE_PATHS[path],
+                                    ctypes.byref(used), _stream(stream)))
+    return MOVE_PATH_NAMES[used.value]

@@ -15,6 +15,10 @@ int launch_permute(const PermParams& p, int smem_bytes, void* stream);     // ch
 int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream);
 int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream);
 
+int launch_move_generic(const MoveParams& p, void* stream);
+int launch_move_runs(const MoveParams& p, void* stream);
+int launch_move_aos(const MoveParams& p, void* stream);
+
 const char* cuda_error_string(int err);
 int current_device_sms(int* sms);   // SM count of the current device
 int max_optin_smem(int* bytes);     // max dynamic shared memory per CTA (opt-in)

@@ -203,6 +203,21 @@ struct PermParams {
   uint8_t* blobs[2][kMaxBlobs];
 };
 
+// ---------------------------------------------------------- n-body move
+// Listing P:643-645: Pos_c += Vel_c * dt for c in X, Y, Z (f32, two roundings).
+struct MoveParams {
+  uint64_t N;
+  float dt;
+  uint32_t S;          // AOS path: record stride in bytes
+  uint32_t g;          // AOS path: records per thread (g * S % 16 == 0)
+  uint32_t aligned;    // GENERIC path: every Pos/Vel access is 4-byte aligned
+  uint64_t base;       // AOS path: byte offset of record 0 in blob `blob`
+  uint32_t blob;       // AOS path
+  uint32_t fpos[3], fvel[3];  // AOS path: leaf offsets inside a record
+  DevLeaf pos[3], vel[3];     // GENERIC / RUNS paths
+  uint8_t* blobs[kMaxBlobs];
+};
+
 // kernel parameter blocks travel as __grid_constant__ arguments (<= 32764 B)
 static_assert(sizeof(PermParams) <= 32764, "PermParams exceeds the kernel parameter limit");
 static_assert(sizeof(NaiveParams) <= 32764, "NaiveParams exceeds the kernel parameter limit");
