@@ -13,6 +13,11 @@ its own 16M records; no data-path collective).
 
 --impl reference times the CPU oracle (oracle/, plain C naive copy) on a
 bounded sample of the same workload; it needs no GPU.
+
+--config MOVE: the n-body move (Listing P:643-645) on 256Mi
+Particle7 particles per GPU in four layouts {packed AoS, SoA MB,
+AoSoA32, Split(Pos -> SoA MB | rest -> AoSoA8)}; one step = one move per layout;
+value = algorithmic bytes (24 read + 12 written per particle) / step time.
 """
 import argparse
 import json
@@ -39,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5", "MOVE"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -482,8 +487,217 @@ def run_c5(args, cfg):
     return 0
 
 
+# ------------------------------------------------------ n-body move (f3)
+MOVE_METRIC = "n-body move GB/s (24 B read + 12 B written per particle), 256Mi Particle7 per GPU"
+MOVE_LAYOUTS = ["aos", "soa_mb", "aosoa32", "split_p7"]
+MOVE_USEFUL = 36  # bytes per particle: Pos + Vel read (24), Pos written (12)
+
+
+def move_workload(world):
+    return {"workload": "MOVE: n-body move (Listing P:643-645) on 268,435,456 Particle7 particles per GPU in "
+                        "{packed AoS, SoA MB, AoSoA32, Split(Pos->SoA MB | Vel,Mass->AoSoA8)}",
+            "particles_per_gpu": W.NBODY_MOVE_N, "layouts": MOVE_LAYOUTS, "dt": W.NBODY_TIMESTEP,
+            "l2": "inputs larger than L2 (7.5 GB per layout; L2 is 126 MB)",
+            "parallelism": f"dp{world} (independent particles per GPU, weak scaling)"}
+
+
+def move_cpu_sample(target_s=10.0):
+    """The oracle's move (1 thread) on a bounded prefix, all four layouts."""
+    import numpy as np
+
+    import oracle
+    n = 1 << 18
+    while True:
+        aos = oracle.Mapping(W.PARTICLE7, [n], "aos")
+        src = [np.frombuffer(W.particle_values(n, seed=42).tobytes(), np.uint8).copy()]
+        views = {}
+        for name in MOVE_LAYOUTS:
+            m = oracle.mapping_from_spec(W.PARTICLE7, [n], W.resolve_spec(name))
+            views[name] = (m, oracle.copy(aos, src, m))
+        t0 = time.perf_counter()
+        for name in MOVE_LAYOUTS:
+            oracle.nbody_move(views[name][0], views[name][1], W.NBODY_TIMESTEP)
+        dt = time.perf_counter() - t0
+        if dt * 4 >= target_s or n >= W.NBODY_MOVE_N:
+            return n, dt, MOVE_USEFUL * n * len(MOVE_LAYOUTS) / dt / 1e9
+        n = min(W.NBODY_MOVE_N, max(n * 2, int(n * target_s / max(dt, 1e-3))))
+
+
+def run_move_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    if args.warmup:
+        move_cpu_sample(target_s=1.0)
+    n, dt, value = move_cpu_sample(target_s=10.0)
+    line = {"metric": MOVE_METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": 1,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic particles (S:685 recipe, seed 42)",
+            "config": dict(move_workload(1), sample_particles=n), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"oracle move on {n} particles x {len(MOVE_LAYOUTS)} layouts"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_move(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_04284_b200 as llama
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = W.NBODY_MOVE_N
+    dt = float(np.float32(W.NBODY_TIMESTEP))
+    stream = torch.cuda.current_stream()
+    # initial particles (S:685 recipe; rank r holds particles r*n ..) as packed
+    # AoS, relayouted into each layout with llama.copy
+    aos = llama.Mapping(W.PARTICLE7, [n], "aos")
+    a0 = aos.alloc("cuda")
+    chunk = 1 << 24
+    for i0 in range(0, n, chunk):
+        v = W.particle_values(chunk, seed=42, i0=rank * n + i0)
+        a0[0][i0 * 28:(i0 + chunk) * 28].copy_(torch.from_numpy(np.frombuffer(v.tobytes(), np.uint8).copy()))
+    maps = {k: llama.Mapping.from_spec(W.PARTICLE7, [n], W.resolve_spec(k)) for k in MOVE_LAYOUTS}
+    blobs = {}
+    for k in MOVE_LAYOUTS:
+        blobs[k] = maps[k].alloc("cuda")
+        llama.copy(aos, a0, maps[k], blobs[k], stream=stream)
+    del a0
+    torch.cuda.synchronize()
+    paths = {k: llama.nbody_move(maps[k], blobs[k], 0.0, stream=stream) for k in MOVE_LAYOUTS}
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        for k in MOVE_LAYOUTS:
+            llama.nbody_move(maps[k], blobs[k], dt, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = llama.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = llama.launch_count() - l0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    step_bytes = MOVE_USEFUL * n * len(MOVE_LAYOUTS)
+    value = step_bytes * world / (ms * 1e-3) / 1e9
+    # per layout (separate event-bracketed pass)
+    per = {}
+    for k in MOVE_LAYOUTS:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            llama.nbody_move(maps[k], blobs[k], dt, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1) / args.steps
+        dram = (28 + 28) * n if k == "aos" else MOVE_USEFUL * n  # AoS moves whole records (P:690)
+        per[k] = {"path": paths[k], "ms": kms, "useful_gbs": MOVE_USEFUL * n / (kms * 1e-3) / 1e9,
+                  "dram_gbs_expected": dram / (kms * 1e-3) / 1e9}
+    peak, peak_src = hbm_peak()
+    dom = "runs"
+    runs_ms = [per[k]["ms"] for k in MOVE_LAYOUTS if per[k]["path"] == "runs"]
+    achieved = MOVE_USEFUL * n / (statistics.mean(runs_ms) * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get("move_runs", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_move_runs", "launches_per_step": len(runs_ms),
+                "algorithmic_bytes_per_launch": MOVE_USEFUL * n, "peak_source": peak_src,
+                "share_of_step": sum(runs_ms) / sum(p["ms"] for p in per.values()),
+                "duration_from": "per-layout CUDA events (separate pass)"}
+    e2e = None
+    if not args.no_e2e:
+        # through the public API with host buffers: H2D of the step's particles
+        # (every layout's blobs), the moves, D2H of the results
+        host = {k: [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in blobs[k]]
+                for k in MOVE_LAYOUTS}
+        for k in MOVE_LAYOUTS:
+            for h, t in zip(host[k], blobs[k]):
+                h.copy_(t)
+        nbytes = sum(maps[k].footprint() for k in MOVE_LAYOUTS)
+
+        def e2e_step():
+            for k in MOVE_LAYOUTS:
+                for h, t in zip(host[k], blobs[k]):
+                    t.copy_(h, non_blocking=True)
+                llama.nbody_move(maps[k], blobs[k], dt, stream=stream)
+                for h, t in zip(host[k], blobs[k]):
+                    h.copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(max(1, args.e2e_steps)):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / max(1, args.e2e_steps)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": step_bytes * world / (ems * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": ems,
+               "method": "pinned host blobs -> device (cudaMemcpyAsync), llama_nbody_move, device -> host"}
+        del host
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cn, cdt, cval = move_cpu_sample()
+            cpu = {"value": cval, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                   "sample": f"oracle move on a prefix of {cn} particles x {len(MOVE_LAYOUTS)} layouts, {cdt:.1f} s"}
+        except Exception as ex:
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+    if rank == 0:
+        ratio = per["soa_mb"]["ms"] / per["aos"]["ms"]
+        line = {"metric": MOVE_METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic particles (S:685 recipe, seed 42)",
+                "config": move_workload(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk, "per_layout": per,
+                "soa_over_aos_runtime": ratio,
+                "paper_soa_over_aos_runtime": {"gpu": [0.55, 0.60, 0.62], "cpu": 0.646, "cite": "P:734, P:691",
+                                               "aos_useful_fraction": 1 - (1 + 4) / (7 + 7)}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if args.config == "MOVE":
+        return run_move_reference(args) if args.impl == "reference" else run_move(args)
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
