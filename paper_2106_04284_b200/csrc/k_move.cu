@@ -2,12 +2,14 @@
 //   Pos_c(i) = Pos_c(i) + Vel_c(i) * dt,  c in {X, Y, Z}, f32, two roundings
 // (reading #25: __fmul_rn / __fadd_rn keep nvcc from fusing them).
 //
-// Three kernels, one per layout family:
+// Kernels, one per layout family:
 //   k_move_generic  thread per particle through the per-leaf normal form (any mapping)
 //   k_move_runs     4 consecutive particles per thread, one 16-byte vector per leaf
 //                   (SoA, AoSoA with L % 4 == 0, splits of those): 6 loads, 3 stores
-//   k_move_aos      packed / aligned AoS: a warp moves 32*g whole records through
-//                   shared memory with coalesced 16-byte loads and stores
+//   k_move_aos_tma  packed / aligned AoS: tiles of whole records through a TMA
+//                   ring in shared memory, Pos updated in place (default)
+//   k_move_aos      the same with warp-staged coalesced 16-byte LSU accesses
+//                   (LLAMA_MOVE_AOS_LSU=1; measured 17% slower)
 // All are HBM-bound: algorithmic traffic 24 B read + 12 B written per particle;
 // an AoS layout moves whole records (S read + S written).
 #include "device.cuh"
@@ -171,7 +173,109 @@ __global__ void __launch_bounds__(kThreads) k_move_aos(const __grid_constant__ M
   }
 }
 
+// TMA variant (the default for AoS): tiles of T whole records move in and out
+// of an NS-stage shared-memory ring with cp.async.bulk; the 8 consumer warps
+// update Pos in place, the producer warp (one lane) stores the tile from the
+// same stage and refills the stage once the store has read it out.
+//   full[s]  the tile's bytes landed in stage s   (TMA -> consumers)
+//   done[s]  consumers updated stage s            (consumers -> producer)
+constexpr int kMoveConsumers = 256;
+
+__global__ void __launch_bounds__(kMoveConsumers + 32, 1) k_move_aos_tma(const __grid_constant__ MoveParams p) {
+  extern __shared__ __align__(128) uint8_t smem_tma[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_tma);
+  uint64_t* done = full + 8;
+  uint8_t* ring = smem_tma + 128;
+  const uint32_t T = p.tile, NS = p.ns;
+  const uint32_t tile_bytes = T * p.S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (uint32_t s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t n_tiles = p.N / T;  // whole tiles; the rest goes to the generic kernel
+  const uint64_t first = blockIdx.x, stride = gridDim.x;
+  const uint32_t n_my = first < n_tiles ? (uint32_t)((n_tiles - first + stride - 1) / stride) : 0;
+  uint8_t* g0 = p.blobs[p.blob] + p.base;
+
+  if (warp == kMoveConsumers / 32) {  // ------------------------------ producer
+    if (lane == 0) {
+      auto load = [&](uint32_t i, uint32_t s) {
+        const uint64_t tile = first + (uint64_t)i * stride;
+        mbar_arrive_expect_tx(&full[s], tile_bytes);
+        bulk_g2s(ring + (size_t)s * tile_bytes, g0 + tile * tile_bytes, tile_bytes, &full[s]);
+      };
+      for (uint32_t i = 0; i < NS && i < n_my; ++i) load(i, i);
+      uint32_t s = 0, ph = 0, sprev = NS - 1;
+      for (uint32_t i = 0; i < n_my; ++i) {
+        const uint64_t tile = first + (uint64_t)i * stride;
+        mbar_wait(&done[s], ph);
+        bulk_s2g(g0 + tile * tile_bytes, ring + (size_t)s * tile_bytes, tile_bytes);
+        bulk_commit();
+        // keep this store in flight; the previous tile's stage is free once
+        // its store has been read out: refill it
+        if (i > 0 && i - 1 + NS < n_my) {
+          bulk_wait_read<1>();
+          load(i - 1 + NS, sprev);
+        }
+        sprev = s;
+        if (++s == NS) { s = 0; ph ^= 1; }
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+  // ------------------------------------------------------------- consumers
+  uint32_t s = 0, ph = 0;
+  for (uint32_t i = 0; i < n_my; ++i) {
+    if (tid == 0) mbar_wait(&full[s], ph);
+    asm volatile("bar.sync 1, %0;" ::"n"(kMoveConsumers) : "memory");
+    uint8_t* img = ring + (size_t)s * tile_bytes;
+    for (uint32_t r = tid; r < T; r += kMoveConsumers) {  // record stride S: conflict-free for odd S/4
+      uint8_t* rec = img + (size_t)r * p.S;
+      float x[3], v[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        x[k] = *reinterpret_cast<const float*>(rec + p.fpos[k]);
+        v[k] = *reinterpret_cast<const float*>(rec + p.fvel[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) *reinterpret_cast<float*>(rec + p.fpos[k]) = move1(x[k], v[k], p.dt);
+    }
+    fence_proxy_async_smem();  // generic-proxy writes -> the TMA store's reads
+    asm volatile("bar.sync 1, %0;" ::"n"(kMoveConsumers) : "memory");
+    if (tid == 0) mbar_arrive(&done[s]);
+    if (++s == NS) { s = 0; ph ^= 1; }
+  }
+}
+
+int launch_move_aos_tma(const MoveParams& p, void* stream) {
+  const uint64_t n_tiles = p.N / p.tile;
+  if (n_tiles) {
+    const int smem = 128 + (int)(p.ns * p.tile * p.S);
+    static LaunchCache cache[64];
+    int dev = 0, per_sm = 1;
+    cudaGetDevice(&dev);
+    int e = prepare_kernel(k_move_aos_tma, kMoveConsumers + 32, smem, &cache[dev & 63], &per_sm);
+    if (e) return e;
+    int sms = 148;
+    current_device_sms(&sms);
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (grid > n_tiles) grid = n_tiles;
+    k_move_aos_tma<<<(unsigned)grid, kMoveConsumers + 32, smem, (cudaStream_t)stream>>>(p);
+    count_launch();
+    e = (int)cudaGetLastError();
+    if (e) return e;
+  }
+  return launch_move_generic_range(p, n_tiles * p.tile, stream);  // the partial last tile
+}
+
 int launch_move_aos(const MoveParams& p, void* stream) {
+  if (p.tile) return launch_move_aos_tma(p, stream);
   if (p.N == 0) return 0;
   const uint64_t recs = 32ull * p.g;
   const uint64_t n_chunks = p.N / recs;

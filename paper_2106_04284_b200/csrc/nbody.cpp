@@ -1,6 +1,7 @@
 // nbody.cpp -- C ABI of the n-body move (Listing P:643-645)
 // and its path planner.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -93,6 +94,17 @@ llama_status llama_nbody_move_ex(const llama_mapping* mh, void* const* blobs, co
         for (int c = 0; c < 3; ++c) {
           p.fpos[c] = (uint32_t)m.F[leaves[c]];
           p.fvel[c] = (uint32_t)m.F[leaves[3 + c]];
+        }
+        // TMA ring: tiles of T records (a multiple of 256, ~32 KB, T*S a
+        // 16-byte multiple since S % 4 == 0 and T % 4 == 0), up to 8 stages
+        // in ~200 KB of shared memory; LLAMA_MOVE_AOS_LSU=1 selects the
+        // warp-staged LSU kernel instead
+        const char* lsu = std::getenv("LLAMA_MOVE_AOS_LSU");
+        const uint64_t T = std::max<uint64_t>(256, (32768 / S) / 256 * 256);
+        const uint64_t ns = std::min<uint64_t>(8, (200 * 1024) / (T * S));
+        if (!(lsu && *lsu == '1') && ns >= 2 && T * S <= 64 * 1024) {
+          p.tile = (uint32_t)T;
+          p.ns = (uint32_t)ns;
         }
       }
       break;

@@ -214,6 +214,7 @@ struct MoveParams {
   uint64_t base;       // AOS path: byte offset of record 0 in blob `blob`
   uint32_t blob;       // AOS path
   uint32_t fpos[3], fvel[3];  // AOS path: leaf offsets inside a record
+  uint32_t tile, ns;          // AOS path, TMA kernel: records per tile, ring stages (tile = 0: LSU kernel)
   DevLeaf pos[3], vel[3];     // GENERIC / RUNS paths
   uint8_t* blobs[kMaxBlobs];
 };
