@@ -20,6 +20,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3, "one": 4, "split": 5}
+LINS = {"row": 0, "col": 1, "morton": 2}
 
 
 def build(force=False):
@@ -51,6 +52,7 @@ _CMapping._fields_ = [
         ("inner_b", ctypes.POINTER(_CMapping)),
         ("leaves_a", ctypes.POINTER(ctypes.c_int32)),
         ("n_a", ctypes.c_int32),
+        ("lin", ctypes.c_int32),
     ]
 
 
@@ -86,6 +88,10 @@ def lib():
         _lib.oracle_copy.argtypes = [M, u8pp, M, u8pp, ctypes.c_int32]
         _lib.oracle_nbody_move.argtypes = [M, u8pp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
                                            ctypes.c_int64, ctypes.c_int64]
+        u32pp = P(P(ctypes.c_uint32))
+        _lib.oracle_copy_counted.argtypes = [M, u8pp, M, u8pp, P(ctypes.c_uint64), P(ctypes.c_uint64), u32pp, u32pp]
+        _lib.oracle_nbody_move_counted.argtypes = [M, u8pp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
+                                                   P(ctypes.c_uint64), u32pp]
     return _lib
 
 
@@ -107,7 +113,7 @@ class Mapping:
     """A mapping as the oracle sees it: flattened leaf sizes, extents, kind,
     AoSoA lanes and packed/aligned."""
 
-    def __init__(self, schema, extents, kind, lanes=1, aligned=False):
+    def __init__(self, schema, extents, kind, lanes=1, aligned=False, lin="row"):
         if isinstance(schema, str):
             self.schema = schema
             self.sizes = leaf_sizes(schema)
@@ -118,10 +124,11 @@ class Mapping:
         self.kind_name = kind
         self.lanes = int(lanes)
         self.aligned = bool(aligned)
+        self.lin = lin
         self._sizes_c = (ctypes.c_int32 * len(self.sizes))(*self.sizes)
         self._ext_c = (ctypes.c_int64 * len(self.extents))(*self.extents)
         self.c = _CMapping(len(self.sizes), self._sizes_c, len(self.extents), self._ext_c,
-                           KINDS[kind], self.lanes, int(self.aligned))
+                           KINDS[kind], self.lanes, int(self.aligned), None, None, None, 0, LINS[lin])
         if lib().oracle_validate(ctypes.byref(self.c)) != 0:
             raise ValueError(f"invalid oracle mapping {kind} {self.sizes} {self.extents}")
 
@@ -137,6 +144,7 @@ class Mapping:
         self.kind_name = "split"
         self.lanes = 1
         self.aligned = False
+        self.lin = "row"
         self.inner = (a, b)
         self.leaves_a = [int(k) for k in leaves_a]
         self._sizes_c = (ctypes.c_int32 * len(self.sizes))(*self.sizes)
@@ -144,7 +152,7 @@ class Mapping:
         self._la_c = (ctypes.c_int32 * max(1, len(self.leaves_a)))(*self.leaves_a)
         self.c = _CMapping(len(self.sizes), self._sizes_c, len(self.extents), self._ext_c,
                            KINDS["split"], 1, 0, ctypes.pointer(a.c), ctypes.pointer(b.c),
-                           self._la_c, len(self.leaves_a))
+                           self._la_c, len(self.leaves_a), 0)
         if lib().oracle_validate(ctypes.byref(self.c)) != 0:
             raise ValueError(f"invalid oracle split {self.sizes} leaves_a={self.leaves_a}")
         return self
@@ -201,18 +209,18 @@ class Mapping:
         return [np.full(s, fill, dtype=np.uint8) for s in self.blob_sizes()]
 
 
-def mapping_from_spec(schema_or_sizes, extents, spec):
+def mapping_from_spec(schema_or_sizes, extents, spec, lin="row"):
     """A mapping from a workloads.MAPPINGS tuple (kind, lanes, aligned) or a
     split tree (leaves_a, part_a, part_b) whose parts are such tuples or trees
     (P:479-481); `resolve` names are looked up by the caller."""
     sizes = leaf_sizes(schema_or_sizes) if isinstance(schema_or_sizes, str) else list(schema_or_sizes)
     if len(spec) == 3 and isinstance(spec[0], str):
         kind, lanes, aligned = spec
-        return Mapping(sizes, extents, kind, lanes, aligned)
+        return Mapping(sizes, extents, kind, lanes, aligned, lin)
     leaves_a, spec_a, spec_b = spec
     sel = set(leaves_a)
-    a = mapping_from_spec([sizes[k] for k in leaves_a], extents, spec_a)
-    b = mapping_from_spec([sizes[k] for k in range(len(sizes)) if k not in sel], extents, spec_b)
+    a = mapping_from_spec([sizes[k] for k in leaves_a], extents, spec_a, lin)
+    b = mapping_from_spec([sizes[k] for k in range(len(sizes)) if k not in sel], extents, spec_b, lin)
     return Mapping.split(sizes, leaves_a, a, b)
 
 
@@ -263,3 +271,40 @@ def nbody_move(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), i0=0, i1=None):
     if rc != 0:
         raise ValueError(f"oracle_nbody_move failed rc={rc}")
     return blobs
+
+
+def _u32pp(arrays):
+    ptrs = (ctypes.POINTER(ctypes.c_uint32) * len(arrays))()
+    for j, a in enumerate(arrays):
+        assert a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]
+        ptrs[j] = a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+    return ptrs
+
+
+def copy_counted(src, src_blobs, dst):
+    """The copy with Trace / Heatmap counters on both sides:
+    returns (dst_blobs, src_hits, dst_hits, src_heat, dst_heat)."""
+    dst_blobs = dst.alloc()
+    sh = np.zeros(src.n_leaves, np.uint64)
+    dh = np.zeros(dst.n_leaves, np.uint64)
+    sheat = [np.zeros(max(1, s), np.uint32) for s in src.blob_sizes()]
+    dheat = [np.zeros(max(1, s), np.uint32) for s in dst.blob_sizes()]
+    u64 = ctypes.POINTER(ctypes.c_uint64)
+    rc = lib().oracle_copy_counted(src.ref, _u8pp(src_blobs), dst.ref, _u8pp(dst_blobs),
+                                   sh.ctypes.data_as(u64), dh.ctypes.data_as(u64), _u32pp(sheat), _u32pp(dheat))
+    if rc != 0:
+        raise ValueError(f"oracle_copy_counted failed rc={rc}")
+    return dst_blobs, sh, dh, sheat, dheat
+
+
+def nbody_move_counted(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5)):
+    """The move with Trace / Heatmap counters: returns (hits, heat)."""
+    hits = np.zeros(m.n_leaves, np.uint64)
+    heat = [np.zeros(max(1, s), np.uint32) for s in m.blob_sizes()]
+    p3 = (ctypes.c_int32 * 3)(*pos)
+    v3 = (ctypes.c_int32 * 3)(*vel)
+    rc = lib().oracle_nbody_move_counted(m.ref, _u8pp(blobs), p3, v3, ctypes.c_float(dt),
+                                         hits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _u32pp(heat))
+    if rc != 0:
+        raise ValueError(f"oracle_nbody_move_counted failed rc={rc}")
+    return hits, heat

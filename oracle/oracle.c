@@ -10,6 +10,13 @@
 #include <omp.h>
 #endif
 
+static int log2_exact(int64_t e) { /* -1 unless e is a power of two */
+  int b = 0;
+  if (e < 1) return -1;
+  while ((1ll << b) < e) ++b;
+  return (1ll << b) == e ? b : -1;
+}
+
 int oracle_validate(const oracle_mapping* m) {
   if (!m || m->n_leaves < 1 || !m->leaf_size || m->rank < 1 || !m->extents) return -1;
   for (int32_t k = 0; k < m->n_leaves; ++k) {
@@ -19,6 +26,10 @@ int oracle_validate(const oracle_mapping* m) {
   for (int32_t d = 0; d < m->rank; ++d)
     if (m->extents[d] < 0) return -1;
   if (m->kind < ORACLE_AOS || m->kind > ORACLE_SPLIT) return -1;
+  if (m->lin < ORACLE_ROW_MAJOR || m->lin > ORACLE_MORTON || m->rank > 16) return -1;
+  if (m->lin == ORACLE_MORTON) /* all extents equal and a power of two */
+    for (int32_t d = 0; d < m->rank; ++d)
+      if (m->extents[d] != m->extents[0] || log2_exact(m->extents[0]) < 0) return -1;
   if (m->kind == ORACLE_AOSOA && m->lanes < 1) return -1; /* S:238-240 */
   if (m->kind == ORACLE_SPLIT) {
     /* S:296-300: inner_a maps the selected leaves, inner_b the rest; both
@@ -66,14 +77,36 @@ int64_t oracle_record_count(const oracle_mapping* m) {
   return n;
 }
 
-/* P:414-416 (enumeration {0,0},{0,1},{0,2},{1,0}...): last index fastest. */
 int64_t oracle_linearize(const oracle_mapping* m, const int64_t* index) {
-  int64_t flat = 0;
-  for (int32_t d = 0; d < m->rank; ++d) {
+  for (int32_t d = 0; d < m->rank; ++d)
     if (index[d] < 0 || index[d] >= m->extents[d]) return -1;
-    flat = flat * m->extents[d] + index[d];
+  int64_t flat = 0;
+  if (m->lin == ORACLE_COL_MAJOR) { /* first index fastest */
+    for (int32_t d = m->rank - 1; d >= 0; --d) flat = flat * m->extents[d] + index[d];
+    return flat;
   }
+  if (m->lin == ORACLE_MORTON) { /* interleave the index bits */
+    int bits = log2_exact(m->extents[0]);
+    for (int b = 0; b < bits; ++b)
+      for (int32_t d = 0; d < m->rank; ++d)
+        flat |= ((index[d] >> b) & 1) << (b * m->rank + (m->rank - 1 - d));
+    return flat;
+  }
+  /* P:414-416 (enumeration {0,0},{0,1},{0,2},{1,0}...): last index fastest */
+  for (int32_t d = 0; d < m->rank; ++d) flat = flat * m->extents[d] + index[d];
   return flat;
+}
+
+/* Storage position of the record whose array index has row-major rank i. */
+static uint64_t storage_index(const oracle_mapping* m, uint64_t i) {
+  if (m->lin == ORACLE_ROW_MAJOR || m->kind == ORACLE_SPLIT) return i;
+  int64_t index[16];
+  uint64_t r = i;
+  for (int32_t d = m->rank - 1; d >= 0; --d) { /* row-major rank -> index */
+    index[d] = (int64_t)(r % (uint64_t)m->extents[d]);
+    r /= (uint64_t)m->extents[d];
+  }
+  return (uint64_t)oracle_linearize(m, index);
 }
 
 /* S:60-66 sizeOfPacked / offsetOf(packed): leaves one after another, no padding. */
@@ -175,7 +208,7 @@ int oracle_blob_nr_and_offset(const oracle_mapping* m, int64_t i, int32_t k,
   if (k < 0 || k >= m->n_leaves) return -1;
   if (i < 0 || i >= oracle_record_count(m)) return -1;
   uint64_t s_k = (uint64_t)m->leaf_size[k];
-  uint64_t ui = (uint64_t)i;
+  uint64_t ui = storage_index(m, (uint64_t)i);
   switch (m->kind) {
     case ORACLE_AOS: {
       uint64_t* offs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)m->n_leaves);
@@ -274,6 +307,7 @@ static void addr_ctx_free(addr_ctx* c) {
 static void addr_of(const addr_ctx* c, uint64_t i, int32_t k, int32_t* blob, uint64_t* offset) {
   const oracle_mapping* m = c->m;
   uint64_t s_k = (uint64_t)m->leaf_size[k];
+  i = storage_index(m, i); /* i: row-major rank of the array index */
   switch (m->kind) {
     case ORACLE_ONE:
       *blob = 0;
@@ -446,6 +480,52 @@ int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int3
       memcpy(blobs[bp] + op, &p, 4);
     }
   }
+  addr_ctx_free(&c);
+  return 0;
+}
+
+static void count(const oracle_mapping* m, const addr_ctx* c, uint64_t i, int32_t k, uint64_t* hits,
+                  uint32_t* const* heat) {
+  if (hits) hits[k] += 1;
+  if (heat) {
+    int32_t b;
+    uint64_t o;
+    addr_of(c, i, k, &b, &o);
+    for (int32_t j = 0; j < m->leaf_size[k]; ++j) heat[b][o + (uint64_t)j] += 1;
+  }
+}
+
+int oracle_copy_counted(const oracle_mapping* src, const uint8_t* const* src_blobs, const oracle_mapping* dst,
+                        uint8_t* const* dst_blobs, uint64_t* src_hits, uint64_t* dst_hits,
+                        uint32_t* const* src_heat, uint32_t* const* dst_heat) {
+  int rc = oracle_copy(src, src_blobs, dst, dst_blobs, 1);
+  if (rc) return rc;
+  addr_ctx cs, cd;
+  addr_ctx_init(&cs, src);
+  addr_ctx_init(&cd, dst);
+  int64_t n = oracle_record_count(src);
+  for (int64_t i = 0; i < n; ++i)
+    for (int32_t k = 0; k < src->n_leaves; ++k) {
+      count(src, &cs, (uint64_t)i, k, src_hits, src_heat); /* the read of (i, k) */
+      count(dst, &cd, (uint64_t)i, k, dst_hits, dst_heat); /* the write of (i, k) */
+    }
+  addr_ctx_free(&cs);
+  addr_ctx_free(&cd);
+  return 0;
+}
+
+int oracle_nbody_move_counted(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos,
+                              const int32_t* vel, float dt, uint64_t* hits, uint32_t* const* heat) {
+  int64_t n = oracle_record_count(m);
+  int rc = oracle_nbody_move(m, blobs, pos, vel, dt, 0, n);
+  if (rc) return rc;
+  addr_ctx c;
+  addr_ctx_init(&c, m);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      count(m, &c, (uint64_t)i, pos[k], hits, heat); /* Pos_c += ...: one resolution */
+      count(m, &c, (uint64_t)i, vel[k], hits, heat); /* ... Vel_c * dt: one resolution */
+    }
   addr_ctx_free(&c);
   return 0;
 }

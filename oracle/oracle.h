@@ -32,6 +32,10 @@ extern "C" {
 /* Mapping kinds. */
 enum { ORACLE_AOS = 0, ORACLE_SOA_SB = 1, ORACLE_SOA_MB = 2, ORACLE_AOSOA = 3, ORACLE_ONE = 4, ORACLE_SPLIT = 5 };
 
+/* Linearisations of the array index ("storage order ... row- or
+ * column-major ... space filling curves such as Morton codes"). */
+enum { ORACLE_ROW_MAJOR = 0, ORACLE_COL_MAJOR = 1, ORACLE_MORTON = 2 };
+
 /* A mapping as the oracle sees it: the flattened leaf sizes (DFS order; each
  * leaf's alignment equals its size), the array extents (row-major),
  * the kind, the AoSoA lane count L (ignored otherwise) and packed/aligned.
@@ -52,6 +56,7 @@ typedef struct oracle_mapping {
   const struct oracle_mapping* inner_b;
   const int32_t* leaves_a;
   int32_t n_a;
+  int32_t lin; /* ORACLE_ROW_MAJOR (default) / COL_MAJOR / MORTON; a split's parts carry their own */
 } oracle_mapping;
 
 /* Returns 0 if the mapping is well formed, -1 otherwise. */
@@ -60,8 +65,15 @@ int oracle_validate(const oracle_mapping* m);
 /* Number of records = product of extents. */
 int64_t oracle_record_count(const oracle_mapping* m);
 
-/* Row-major linearisation, last index fastest.
- * Returns -1 on an out-of-range index. */
+/* The mapping's linearisation of an array index (its storage position):
+ *   row-major, last index fastest;
+ *   column-major, first index fastest;
+ *   Morton: bit b of index[d] goes to bit b*rank + (rank-1-d) of the code
+ *   (all extents equal powers of two; reading #26).
+ * Returns -1 on an out-of-range index.  Records are otherwise identified
+ * everywhere in this oracle by their array index's ROW-MAJOR rank i (the
+ * iteration order); the address functions below apply the
+ * mapping's linearisation to it. */
 int64_t oracle_linearize(const oracle_mapping* m, const int64_t* index);
 
 /* Record-level offsets.  offsets[k] of leaf k within
@@ -114,6 +126,18 @@ int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
  * Returns 0, or -1 for an invalid mapping / leaf / range. */
 int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos, const int32_t* vel,
                       float dt, int64_t i0, int64_t i1);
+
+/* Trace and Heatmap: the
+ * whole-view copy and the move, counting every address resolution.
+ * *_hits[k] += 1 per resolution of leaf k (NULL: not counted);
+ * *_heat[b][o] += 1 for every byte o of the resolved range in blob b (NULL:
+ * not counted).  The copy resolves each (i, k) once on each side; the move
+ * resolves Pos_c once (the compound +=) and Vel_c once per particle. */
+int oracle_copy_counted(const oracle_mapping* src, const uint8_t* const* src_blobs, const oracle_mapping* dst,
+                        uint8_t* const* dst_blobs, uint64_t* src_hits, uint64_t* dst_hits,
+                        uint32_t* const* src_heat, uint32_t* const* dst_heat);
+int oracle_nbody_move_counted(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos,
+                              const int32_t* vel, float dt, uint64_t* hits, uint32_t* const* heat);
 
 #ifdef __cplusplus
 }
