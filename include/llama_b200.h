@@ -117,9 +117,48 @@ llama_status llama_mapping_create_from_schema(const char* schema, const int64_t*
  * split's blobs are a's blobs followed by b's.  a and b may themselves be
  * splits; they are copied, so they may be destroyed afterwards.
  * Errors: INVALID_ARGUMENT (NULL, bad leaf list, leaf count or extents that
- * do not add up), UNSUPPORTED (more than LLAMA_MAX_BLOBS blobs). */
+ * do not add up, a and b linearised differently), UNSUPPORTED (more than
+ * LLAMA_MAX_BLOBS blobs).  The split takes a's linearisation. */
 llama_status llama_mapping_create_split(const llama_mapping* a, const llama_mapping* b, const int32_t* leaves_a,
                                         int32_t n_a, llama_mapping** out);
+
+/* Linearisation of the array index into a storage position (P:140-142
+ * "storage order ... row- or column-major ... Morton codes").
+ * ROW_MAJOR (the default of every create call): last index fastest;
+ * COL_MAJOR: first index fastest; MORTON: bit b of index[d] goes to bit
+ * b*rank + (rank-1-d) (all extents equal powers of two; #26).
+ * Data belongs to the array index: a copy between views of different
+ * linearisations moves record (index) to record (index), i.e. it also
+ * transposes / reorders (naive path only); views of equal linearisation use
+ * every path.  llama_blob_nr_and_offset applies the linearisation. */
+typedef enum { LLAMA_ROW_MAJOR = 0, LLAMA_COL_MAJOR = 1, LLAMA_MORTON = 2 } llama_linearizer;
+
+/* A copy of `m` (any kind, splits included) with linearisation `lin`.
+ * Errors: INVALID_ARGUMENT (NULL, bad lin, MORTON with unequal or
+ * non-power-of-two extents). */
+llama_status llama_mapping_with_linearizer(const llama_mapping* m, llama_linearizer lin, llama_mapping** out);
+
+/* Instrumentation (#27): a traced mapping is
+ * `inner` (copied) plus device counters owned by the new mapping, allocated
+ * on the current device:
+ *   LLAMA_TRACE_FIELDS  (Trace)   one uint64 counter per leaf
+ *   LLAMA_TRACE_BYTES   (Heatmap) one uint32 counter per blob byte
+ * (a bit mask; both may be set).  Every llama_copy / llama_nbody_move through
+ * a traced view counts its address resolutions -- a copy resolves each
+ * (record, leaf) once per side; the move resolves each Pos and Vel component
+ * once per particle -- and therefore runs the element-wise kernels (copy:
+ * NAIVE; move: GENERIC; forcing another path is UNSUPPORTED).  Counters
+ * start at 0, accumulate over calls, and are read (synchronously, after all
+ * work on the device) or reset (on `stream`) below.
+ * Errors: INVALID_ARGUMENT, CUDA (allocation), OOM. */
+typedef enum { LLAMA_TRACE_FIELDS = 1, LLAMA_TRACE_BYTES = 2 } llama_trace_kind;
+llama_status llama_mapping_create_traced(const llama_mapping* inner, int32_t kinds, llama_mapping** out);
+/* hits[k] for k < min(capacity, leaf count); INVALID_ARGUMENT if not traced with FIELDS. */
+llama_status llama_trace_field_hits(const llama_mapping* m, uint64_t* hits, int32_t capacity);
+/* counters of blob `blob` (its blob size many); INVALID_ARGUMENT if not traced with BYTES,
+ * blob out of range or capacity below the blob size. */
+llama_status llama_trace_byte_hits(const llama_mapping* m, int32_t blob, uint32_t* hits, uint64_t capacity);
+llama_status llama_trace_reset(const llama_mapping* m, void* stream);
 
 /* Destroys a mapping; NULL-safe.  Plans cached for pairs involving it are
  * released. */

@@ -23,6 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libllama_b200.so")
 
 KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3, "one": 4}
+LINS = {"row": 0, "col": 1, "morton": 2}
 PATHS = {"auto": 0, "naive": 1, "blobcopy": 2, "run": 3, "permute": 4}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_MISMATCH",
@@ -31,6 +32,8 @@ STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_
 
 # Symbols declared in include/llama_b200.h (checked by tests/test_capi_host.py).
 EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_mapping_create_split",
+           "llama_mapping_with_linearizer", "llama_mapping_create_traced", "llama_trace_field_hits",
+           "llama_trace_byte_hits", "llama_trace_reset",
            "llama_mapping_destroy",
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
@@ -77,6 +80,11 @@ def _load():
                                                      P(ctypes.c_void_p)]
     lib.llama_mapping_create_split.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(ctypes.c_int32),
                                                 ctypes.c_int32, P(ctypes.c_void_p)]
+    lib.llama_mapping_with_linearizer.argtypes = [ctypes.c_void_p, ctypes.c_int, P(ctypes.c_void_p)]
+    lib.llama_mapping_create_traced.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_void_p)]
+    lib.llama_trace_field_hits.argtypes = [ctypes.c_void_p, P(ctypes.c_uint64), ctypes.c_int32]
+    lib.llama_trace_byte_hits.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_uint32), ctypes.c_uint64]
+    lib.llama_trace_reset.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.llama_mapping_destroy.argtypes = [ctypes.c_void_p]
     lib.llama_mapping_destroy.restype = None
     lib.llama_blob_count.argtypes = [ctypes.c_void_p]
@@ -130,6 +138,7 @@ class Mapping:
         self.kind = kind
         self.lanes = int(lanes)
         self.aligned = bool(aligned)
+        self.lin = "row"
         if kind not in KINDS:
             raise ValueError(f"unknown mapping kind {kind!r}")
         ext = (ctypes.c_int64 * len(self.extents))(*self.extents)
@@ -157,22 +166,60 @@ class Mapping:
         self.kind = "split"
         self.lanes = 1
         self.aligned = False
+        self.lin = a.lin
         self.parts = (a, b, [int(k) for k in leaves_a])
         return self
 
+    def with_linearizer(self, lin):
+        """A copy with storage order lin: 'row' | 'col' | 'morton'."""
+        c = self.__class__.__new__(self.__class__)
+        h = ctypes.c_void_p()
+        _check(_lib.llama_mapping_with_linearizer(self._h, LINS[lin], ctypes.byref(h)))
+        c.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_h"})
+        c._h = h
+        c.lin = lin
+        return c
+
+    def traced(self, fields=True, bytes=False):
+        """Trace (per-leaf counters) and/or Heatmap (per-byte counters) of this
+        mapping: a new mapping owning device counters."""
+        c = self.__class__.__new__(self.__class__)
+        h = ctypes.c_void_p()
+        _check(_lib.llama_mapping_create_traced(self._h, (1 if fields else 0) | (2 if bytes else 0), ctypes.byref(h)))
+        c.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_h"})
+        c._h = h
+        return c
+
+    def field_hits(self):
+        n = self.leaf_count
+        out = (ctypes.c_uint64 * n)()
+        _check(_lib.llama_trace_field_hits(self._h, out, n))
+        return [int(v) for v in out]
+
+    def byte_hits(self, blob):
+        import numpy as np
+        n = self.blob_sizes()[blob]
+        out = np.zeros(max(1, n), np.uint32)
+        _check(_lib.llama_trace_byte_hits(self._h, int(blob), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), n))
+        return out[:n]
+
+    def reset_trace(self, stream=None):
+        _check(_lib.llama_trace_reset(self._h, _stream(stream)))
+
     @classmethod
-    def from_spec(cls, schema, extents, spec):
+    def from_spec(cls, schema, extents, spec, lin="row"):
         """A mapping from (kind, lanes, aligned) or a split tree
         (leaves_a, spec_a, spec_b) (argument marshalling: the parts' leaf
         type lists are selected from the full record's)."""
         if len(spec) == 3 and isinstance(spec[0], str):
             kind, lanes, aligned = spec
-            return cls(schema, extents, kind, lanes, aligned)
+            m = cls(schema, extents, kind, lanes, aligned)
+            return m if lin == "row" else m.with_linearizer(lin)
         types = schema if not isinstance(schema, str) else cls(schema, [0]).leaf_types()
         leaves_a, spec_a, spec_b = spec
         sel = set(int(k) for k in leaves_a)
-        a = cls.from_spec([types[k] for k in sorted(sel)], extents, spec_a)
-        b = cls.from_spec([t for k, t in enumerate(types) if k not in sel], extents, spec_b)
+        a = cls.from_spec([types[k] for k in sorted(sel)], extents, spec_a, lin)
+        b = cls.from_spec([t for k, t in enumerate(types) if k not in sel], extents, spec_b, lin)
         return cls.split(a, b, sorted(sel))
 
     @property

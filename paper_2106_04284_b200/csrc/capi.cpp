@@ -124,6 +124,23 @@ llama_status llama_mapping_create_split(const llama_mapping* a, const llama_mapp
   }
 }
 
+llama_status llama_mapping_with_linearizer(const llama_mapping* m, llama_linearizer lin, llama_mapping** out) {
+  if (!m || !out) return fail(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    auto* c = new llama_mapping(*m);
+    std::string err;
+    llama_status st = llb::set_linearizer(&c->m, lin, &err);
+    if (st != LLAMA_OK) {
+      delete c;
+      return fail(st, err);
+    }
+    *out = c;
+    return LLAMA_OK;
+  } catch (...) {
+    return fail(LLAMA_ERR_OOM, "out of host memory");
+  }
+}
+
 void llama_mapping_destroy(llama_mapping* m) {
   if (!m) return;
   {
@@ -159,13 +176,10 @@ llama_status llama_blob_nr_and_offset(const llama_mapping* m, const int64_t* ind
   if (!m || !index || !blob || !offset) return fail(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
   const llb::Mapping& mm = m->m;
   if (leaf < 0 || leaf >= mm.K()) return fail(LLAMA_ERR_INVALID_ARGUMENT, "leaf out of range");
-  uint64_t flat = 0;  // row-major, last index fastest
-  for (size_t d = 0; d < mm.extents.size(); ++d) {
+  for (size_t d = 0; d < mm.extents.size(); ++d)
     if (index[d] < 0 || index[d] >= mm.extents[d]) return fail(LLAMA_ERR_INVALID_ARGUMENT, "index out of range");
-    flat = flat * (uint64_t)mm.extents[d] + (uint64_t)index[d];
-  }
   *blob = (int32_t)mm.blob[leaf];
-  *offset = mm.offset(flat, leaf);
+  *offset = mm.offset(mm.storage(index), leaf);  // linearisation, then the normal form
   return LLAMA_OK;
 }
 
@@ -314,6 +328,7 @@ llama_status llama_generate(const llama_mapping* m, void* const* blobs, uint64_t
     g->seed = seed;
     g->K = mm.K();
     for (int k = 0; k < mm.K(); ++k) g->dl[k] = mm.dev_leaf(k);
+    g->lin = mm.dev_lin();
     for (int b = 0; b < mm.nblobs(); ++b) g->db[b] = static_cast<uint8_t*>(blobs[b]);
     if ((e = llb::launch_gen(*g, stream))) return cuda_fail(e, "generate launch");
     return LLAMA_OK;

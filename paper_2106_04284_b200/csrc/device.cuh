@@ -20,6 +20,39 @@ __device__ __forceinline__ uint64_t nf_offset(uint64_t i, const DevSide& s, cons
   return l.base + q * s.B + l.F + (i - q * s.L) * l.size;
 }
 
+// Storage position of the record whose array index has row-major rank i
+// (#26).
+__device__ __forceinline__ uint64_t lin_storage(uint64_t i, const DevLin& l) {
+  if (l.kind == LLAMA_ROW_MAJOR) return i;
+  uint64_t idx[kMaxRank];
+  for (int d = (int)l.rank - 1; d >= 0; --d) {
+    idx[d] = i % l.ext[d];
+    i /= l.ext[d];
+  }
+  uint64_t f = 0;
+  if (l.kind == LLAMA_COL_MAJOR) {
+    for (int d = (int)l.rank - 1; d >= 0; --d) f = f * l.ext[d] + idx[d];
+    return f;
+  }
+  for (uint32_t b = 0; b < l.bits; ++b)  // MORTON
+    for (uint32_t d = 0; d < l.rank; ++d) f |= ((idx[d] >> b) & 1ull) << (b * l.rank + (l.rank - 1 - d));
+  return f;
+}
+
+// Heatmap: one count per byte of a resolved range.
+__device__ __forceinline__ void trace_bytes(const DevTrace& t, uint32_t blob, uint64_t off, uint32_t size) {
+  if (!t.heat) return;
+  uint32_t* h = t.heat + t.heat_base[blob] + off;
+  for (uint32_t j = 0; j < size; ++j) atomicAdd(h + j, 1u);
+}
+
+// Trace: adds this thread's resolution count of leaf k, summed
+// over the warp first (every lane of the warp must call it).
+__device__ __forceinline__ void trace_hits(const DevTrace& t, int k, uint32_t cnt) {
+  const uint32_t w = __reduce_add_sync(0xffffffffu, cnt);
+  if (t.hits && (threadIdx.x & 31) == 0 && w) atomicAdd(t.hits + k, (unsigned long long)w);
+}
+
 // The same with the leaf's own L and B (composite Split / One mappings).
 __device__ __forceinline__ uint64_t leaf_offset(uint64_t i, const DevLeaf& l) {
   const uint64_t q = l.lshift != kNoShift ? (i >> l.lshift) : (i / l.L);

@@ -52,30 +52,48 @@ int grid_for(uint64_t work, int per_sm) {
 
 // ---------------------------------------------------------------- generic
 // Particles [i0, N) -- i0 > 0 when it finishes the tail of the AoS kernel.
-template <bool kAligned>
+// kTraced: count the resolutions (Trace / Heatmap): Pos_c once
+// (the compound +=) and Vel_c once per particle.
+template <bool kAligned, bool kTraced>
 __global__ void __launch_bounds__(kThreads) k_move_generic(const __grid_constant__ MoveParams p, uint64_t i0) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t cnt = 0;
   for (uint64_t i = i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.N; i += stride) {
     uint8_t* xa[3];
     float x[3], v[3];
+    ++cnt;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      xa[c] = p.blobs[p.pos[c].blob] + leaf_offset(i, p.pos[c]);
+      const uint64_t op = leaf_offset(i, p.pos[c]), ov = leaf_offset(i, p.vel[c]);
+      xa[c] = p.blobs[p.pos[c].blob] + op;
       x[c] = load_f32(xa[c], kAligned);
-      v[c] = load_f32(p.blobs[p.vel[c].blob] + leaf_offset(i, p.vel[c]), kAligned);
+      v[c] = load_f32(p.blobs[p.vel[c].blob] + ov, kAligned);
+      if (kTraced) {
+        trace_bytes(p.tr, p.pos[c].blob, op, 4);
+        trace_bytes(p.tr, p.vel[c].blob, ov, 4);
+      }
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) store_f32(xa[c], move1(x[c], v[c], p.dt), kAligned);
   }
+  if (kTraced)
+    for (int c = 0; c < 3; ++c) {
+      trace_hits(p.tr, (int)p.lpos[c], cnt);
+      trace_hits(p.tr, (int)p.lvel[c], cnt);
+    }
 }
 
 int launch_move_generic_range(const MoveParams& p, uint64_t i0, void* stream) {
   if (p.N <= i0) return 0;
   const int grid = grid_for(p.N - i0, 16);
-  if (p.aligned)
-    k_move_generic<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
+  if (p.traced && p.aligned)
+    k_move_generic<true, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
+  else if (p.traced)
+    k_move_generic<false, true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
+  else if (p.aligned)
+    k_move_generic<true, false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
   else
-    k_move_generic<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
+    k_move_generic<false, false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(p, i0);
   count_launch();
   return (int)cudaGetLastError();
 }

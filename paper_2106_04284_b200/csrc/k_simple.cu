@@ -51,22 +51,41 @@ int max_optin_smem(int* bytes) {
 // ------------------------------------------------------------------ naive
 // One thread per record, leaves in the inner loop, one s_k-byte element copy
 // through both mappings' address functions.
+// kTraced: also count every address resolution (Trace / Heatmap):
+// each (record, leaf) is resolved once on each side.
+template <bool kTraced>
 __global__ void __launch_bounds__(kThreads) k_naive(const __grid_constant__ NaiveParams p) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t cnt = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.N; i += stride) {
+    ++cnt;
     for (int k = 0; k < p.K; ++k) {
       const DevLeaf& sl = p.sl[k];
       const DevLeaf& dl = p.dl[k];
-      const uint8_t* s = p.sb[sl.blob] + leaf_offset(i, sl);
-      uint8_t* d = p.db[dl.blob] + leaf_offset(i, dl);
-      copy_elem(d, s, sl.size);
+      // i = row-major rank of the array index; each side's storage position
+      const uint64_t fs = p.relin ? lin_storage(i, p.slin) : i;
+      const uint64_t fd = p.relin ? lin_storage(i, p.dlin) : i;
+      const uint64_t os = leaf_offset(fs, sl), od = leaf_offset(fd, dl);
+      copy_elem(p.db[dl.blob] + od, p.sb[sl.blob] + os, sl.size);
+      if (kTraced) {
+        trace_bytes(p.tr[0], sl.blob, os, sl.size);
+        trace_bytes(p.tr[1], dl.blob, od, dl.size);
+      }
     }
   }
+  if (kTraced)
+    for (int k = 0; k < p.K; ++k) {
+      trace_hits(p.tr[0], k, cnt);
+      trace_hits(p.tr[1], k, cnt);
+    }
 }
 
 int launch_naive(const NaiveParams& p, void* stream) {
   if (p.N == 0) return 0;
-  k_naive<<<grid_for(p.N, 16), kThreads, 0, (cudaStream_t)stream>>>(p);
+  if (p.traced)
+    k_naive<true><<<grid_for(p.N, 16), kThreads, 0, (cudaStream_t)stream>>>(p);
+  else
+    k_naive<false><<<grid_for(p.N, 16), kThreads, 0, (cudaStream_t)stream>>>(p);
   count_launch();
   return (int)cudaGetLastError();
 }
@@ -83,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) k_gen(const __grid_constant__ GenPar
       // the last of them in index order, as a sequential generator would
       if (dl.B == 0 && i + dl.L < p.N) continue;
       uint64_t v = splitmix64(p.seed ^ (i * (uint64_t)p.K + (uint64_t)k));
-      uint8_t* d = p.db[dl.blob] + leaf_offset(i, dl);
+      uint8_t* d = p.db[dl.blob] + leaf_offset(lin_storage(i, p.lin), dl);  // data follows the array index
       copy_elem(d, reinterpret_cast<const uint8_t*>(&v), dl.size);
     }
   }

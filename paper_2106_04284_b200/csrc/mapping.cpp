@@ -173,12 +173,55 @@ DevLeaf Mapping::dev_leaf(int k) const {
   return l;
 }
 
+uint64_t next_mapping_id() { return g_next_id.fetch_add(1); }
+
+DevLin Mapping::dev_lin() const {
+  DevLin l{};
+  l.kind = (uint32_t)lin;
+  l.rank = (uint32_t)extents.size();
+  for (size_t d = 0; d < extents.size(); ++d) l.ext[d] = (uint64_t)extents[d];
+  if (lin == LLAMA_MORTON && !extents.empty()) {
+    while ((1ull << l.bits) < (uint64_t)extents[0]) ++l.bits;
+  }
+  return l;
+}
+
+uint64_t Mapping::storage(const int64_t* index) const {
+  const size_t r = extents.size();
+  uint64_t f = 0;
+  if (lin == LLAMA_COL_MAJOR) {
+    for (size_t d = r; d-- > 0;) f = f * (uint64_t)extents[d] + (uint64_t)index[d];
+  } else if (lin == LLAMA_MORTON) {
+    const DevLin l = dev_lin();
+    for (uint32_t b = 0; b < l.bits; ++b)
+      for (uint32_t d = 0; d < l.rank; ++d) f |= (((uint64_t)index[d] >> b) & 1ull) << (b * l.rank + (l.rank - 1 - d));
+  } else {
+    for (size_t d = 0; d < r; ++d) f = f * (uint64_t)extents[d] + (uint64_t)index[d];
+  }
+  return f;
+}
+
+llama_status set_linearizer(Mapping* m, llama_linearizer lin, std::string* err) {
+  if (lin < LLAMA_ROW_MAJOR || lin > LLAMA_MORTON) { *err = "bad linearizer"; return LLAMA_ERR_INVALID_ARGUMENT; }
+  if (lin == LLAMA_MORTON) {
+    for (int64_t e : m->extents)
+      if (e != m->extents[0] || e < 1 || (e & (e - 1)) != 0) {
+        *err = "MORTON needs equal power-of-two extents (S:176)";
+        return LLAMA_ERR_INVALID_ARGUMENT;
+      }
+  }
+  m->lin = lin;
+  m->id = g_next_id.fetch_add(1);
+  return LLAMA_OK;
+}
+
 llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leaves_a, int32_t n_a, Mapping* m,
                          std::string* err) {
   const int K = a.K() + b.K();
   if (n_a != a.K()) { *err = "leaves_a must list exactly a's leaves"; return LLAMA_ERR_INVALID_ARGUMENT; }
   if (K > LLAMA_MAX_LEAVES) { *err = "more than LLAMA_MAX_LEAVES leaves"; return LLAMA_ERR_UNSUPPORTED; }
   if (a.extents != b.extents) { *err = "a and b must have the same extents"; return LLAMA_ERR_INVALID_ARGUMENT; }
+  if (a.lin != b.lin) { *err = "a and b must have the same linearizer"; return LLAMA_ERR_INVALID_ARGUMENT; }
   if (a.nblobs() + b.nblobs() > LLAMA_MAX_BLOBS) { *err = "more than LLAMA_MAX_BLOBS blobs"; return LLAMA_ERR_UNSUPPORTED; }
   std::vector<int> in_a(K, -1);
   for (int j = 0; j < n_a; ++j) {
@@ -193,6 +236,7 @@ llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leav
   m->N = a.N;
   m->kind = LLAMA_SPLIT;
   m->uniform = false;
+  m->lin = a.lin;
   m->E = std::max(a.E, b.E);  // records the blobs cover: the largest of the parts
   int ib = 0;
   for (int k = 0; k < K; ++k) {

@@ -3,6 +3,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,17 @@ struct Part {
   bool soa() const { return kind == LLAMA_SOA_SINGLE_BLOB || kind == LLAMA_SOA_MULTI_BLOB; }
 };
 
+// Device counters of a traced mapping (Trace / Heatmap); shared
+// by the copies of a mapping handle, freed with the last one.
+struct TraceBuffers {
+  unsigned long long* hits = nullptr;  // one per leaf
+  uint32_t* heat = nullptr;            // one per blob byte, blobs back to back
+  std::vector<uint64_t> heat_base;     // start of each blob's counters
+  uint64_t heat_count = 0;
+  int device = 0;
+  ~TraceBuffers();
+};
+
 struct Mapping {
   uint64_t id = 0;  // unique per process, keys the plan cache
   std::vector<llama_scalar> types;
@@ -47,12 +59,14 @@ struct Mapping {
   // hold them per leaf (they differ between the parts of a Split).
   uint64_t L = 1, B = 0;
   bool uniform = true;  // every leaf shares L and B (not a Split)
+  llama_linearizer lin = LLAMA_ROW_MAJOR;  // storage order of the array index
   std::vector<uint64_t> Lk, Bk;
   std::vector<uint64_t> base, F;
   std::vector<uint32_t> blob;
   std::vector<uint64_t> blob_sizes;
   uint64_t E = 0;            // records covered by the blobs (blocked: nblocks*L; SoA: N)
   std::vector<Part> parts;   // one for the classic kinds; a split's parts in blob order
+  std::shared_ptr<TraceBuffers> trace;  // non-null: instrumented (Trace / Heatmap)
 
   int K() const { return (int)sizes.size(); }
   int nblobs() const { return (int)blob_sizes.size(); }
@@ -69,10 +83,19 @@ struct Mapping {
   uint64_t offset(uint64_t i, int k) const { return base[k] + (i / Lk[k]) * Bk[k] + F[k] + (i % Lk[k]) * sizes[k]; }
   DevSide dev_side() const;
   DevLeaf dev_leaf(int k) const;
+  DevLin dev_lin() const;
+  // storage position of an array index (row-major rank -> linearisation)
+  uint64_t storage(const int64_t* index) const;
 };
 
 // Builds the descriptor; returns LLAMA_OK or an error with *err set.
 llama_status build_mapping(const llama_mapping_desc& d, Mapping* m, std::string* err);
+
+uint64_t next_mapping_id();
+DevTrace dev_trace(const Mapping& m);  // trace.cpp; zeros when not traced
+
+// Sets the linearisation (validated; a new id for the plan cache).
+llama_status set_linearizer(Mapping* m, llama_linearizer lin, std::string* err);
 
 // Split: leaves_a of the full record go to a, the rest to b.
 llama_status build_split(const Mapping& a, const Mapping& b, const int32_t* leaves_a, int32_t n_a, Mapping* m,

@@ -67,6 +67,17 @@ llama_status llama_nbody_move_ex(const llama_mapping* mh, void* const* blobs, co
       p.vel[c] = m.dev_leaf(leaves[3 + c]);
     }
     for (int j = 0; j < 6; ++j) p.aligned &= leaf_aligned4(m, leaves[j]) ? 1u : 0u;
+    for (int c = 0; c < 3; ++c) {
+      p.lpos[c] = (uint32_t)leaves[c];
+      p.lvel[c] = (uint32_t)leaves[3 + c];
+    }
+    if (m.trace) {  // Trace / Heatmap: the element-wise kernel counts its resolutions
+      p.traced = 1;
+      p.tr = llb::dev_trace(m);
+      if (path != LLAMA_MOVE_AUTO && path != LLAMA_MOVE_GENERIC)
+        return llb::set_error(LLAMA_ERR_UNSUPPORTED, "a traced view moves through the GENERIC path");
+      path = LLAMA_MOVE_GENERIC;
+    }
     for (int b = 0; b < m.nblobs(); ++b) p.blobs[b] = static_cast<uint8_t*>(blobs[b]);
 
     // RUNS: every Pos / Vel leaf in 16-byte aligned runs of >= 4 particles

@@ -12,6 +12,7 @@ namespace llb {
 constexpr int kMaxLeaves = LLAMA_MAX_LEAVES;
 constexpr int kMaxBlobs = LLAMA_MAX_BLOBS;
 constexpr int kMaxMoves = 512;
+constexpr int kMaxRank = LLAMA_MAX_RANK;
 constexpr uint32_t kNoShift = 0xFFFFFFFFu;
 
 // One side's mapping in the AoSoA normal form:
@@ -22,6 +23,16 @@ struct DevSide {
   uint64_t B;       // block stride in bytes
   uint32_t lshift;  // log2(L) when L is a power of two, else kNoShift
   uint32_t pad_;
+};
+
+// Linearisation of the array index: the storage position of the
+// record whose array index has row-major rank i (kind 0: i itself).
+struct DevLin {
+  uint32_t kind;   // llama_linearizer
+  uint32_t rank;
+  uint32_t bits;   // MORTON: log2 of the (equal) extents
+  uint32_t pad_;
+  uint64_t ext[kMaxRank];
 };
 
 // One leaf's normal form (per leaf, so composite Split mappings and One fit):
@@ -38,10 +49,22 @@ struct DevLeaf {
 };
 
 // ---------------------------------------------------------------- naive / gen
+// Trace / Heatmap counters of one side: hits[k] per leaf, heat
+// per blob byte at heat + heat_base[blob] (NULL: not counted).
+struct DevTrace {
+  unsigned long long* hits;
+  uint32_t* heat;
+  uint64_t heat_base[kMaxBlobs];
+};
+
 struct NaiveParams {
   uint64_t N;
   int32_t K;
-  int32_t pad_;
+  int32_t relin;      // 1: the sides are linearised differently (records located per side)
+  DevLin slin, dlin;
+  int32_t traced;     // 1: count address resolutions (tr[0] = src, tr[1] = dst)
+  int32_t pad2_;
+  DevTrace tr[2];
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];
@@ -53,6 +76,7 @@ struct GenParams {
   uint64_t seed;
   int32_t K;
   int32_t pad_;
+  DevLin lin;
   DevLeaf dl[kMaxLeaves];
   uint8_t* db[kMaxBlobs];
 };
@@ -217,6 +241,9 @@ struct MoveParams {
   uint32_t tile, ns;          // AOS path, TMA kernel: records per tile, ring stages (tile = 0: LSU kernel)
   DevLeaf pos[3], vel[3];     // GENERIC / RUNS paths
   uint8_t* blobs[kMaxBlobs];
+  uint32_t traced;            // GENERIC path: count resolutions into tr
+  uint32_t lpos[3], lvel[3];  // leaf indices of Pos / Vel (trace counters)
+  DevTrace tr;
 };
 
 // kernel parameter blocks travel as __grid_constant__ arguments (<= 32764 B)

@@ -72,6 +72,12 @@ void plan_naive(const Mapping& s, const Mapping& d, Plan* p) {
   std::memset(&n, 0, sizeof(n));
   n.N = s.N;
   n.K = s.K();
+  n.relin = s.lin != d.lin ? 1 : 0;
+  n.slin = s.dev_lin();
+  n.dlin = d.dev_lin();
+  n.traced = (s.trace || d.trace) ? 1 : 0;
+  n.tr[0] = dev_trace(s);
+  n.tr[1] = dev_trace(d);
   for (int k = 0; k < s.K(); ++k) {
     n.sl[k] = s.dev_leaf(k);
     n.dl[k] = d.dev_leaf(k);
@@ -455,6 +461,16 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
     return LLAMA_OK;
   }
   std::string why;
+  // record (index) -> record (index) across storage orders, or counting every
+  // address resolution (Trace / Heatmap): the element-wise kernel only
+  if (s.lin != d.lin || s.trace || d.trace) {
+    if (path != LLAMA_PATH_AUTO && path != LLAMA_PATH_NAIVE) {
+      *err = "path not applicable to this mapping pair: linearised differently or traced (naive only)";
+      return LLAMA_ERR_UNSUPPORTED;
+    }
+    plan_naive(s, d, out);
+    return LLAMA_OK;
+  }
   switch (path) {
     case LLAMA_PATH_AUTO:
       // the warp-specialised TMA permute measured fastest on B200 for every

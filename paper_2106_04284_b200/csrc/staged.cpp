@@ -167,6 +167,10 @@ llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, v
     const uint64_t N = s.N;
     if (d.collides())
       return llb::set_error(LLAMA_ERR_UNSUPPORTED, "destination maps several records onto one location");
+    if (s.trace || d.trace)
+      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a traced view (use llama_copy)");
+    if (s.lin != d.lin)  // equal storage orders: slabs of storage positions correspond
+      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy between differently linearised views");
     if (!s.uniform || !d.uniform || s.kind == LLAMA_ONE || d.kind == LLAMA_ONE)
       return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a split / one mapping (copy its blobs, then llama_copy)");
     if (d.footprint_bytes() == 0) return LLAMA_OK;

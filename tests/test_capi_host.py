@@ -221,3 +221,36 @@ def test_split_errors_and_plans():
         b = llama.Mapping(schema, big, *W.MAPPINGS[other])
         assert llama.plan(a, b)["path"] == "permute", (name, other)
         assert llama.plan(b, a)["path"] == "permute", (other, name)
+
+
+# ------------------------------------------------------- linearisations (f4)
+@pytest.mark.parametrize("lin,ext", [("col", [4, 3]), ("col", [2, 3, 5]), ("morton", [4, 4]), ("morton", [2, 2, 2])])
+@pytest.mark.parametrize("name", ["aos", "soa_sb", "aosoa4", "split_pos"])
+def test_linearized_descriptor_matches_oracle(oracle_mod, lin, ext, name):
+    spec = W.resolve_spec(name) if name != "aosoa4" else ("aosoa", 4, False)
+    m = llama.Mapping.from_spec(W.LISTING1, ext, spec, lin=lin)
+    o = oracle_mod.mapping_from_spec(W.LISTING1, ext, spec, lin=lin)
+    assert m.blob_sizes() == o.blob_sizes()
+    for flat in range(int(np.prod(ext))):
+        idx = [int(x) for x in np.unravel_index(flat, ext)]
+        for k in range(o.n_leaves):
+            assert m.blob_nr_and_offset(idx, k) == o.addr(flat, k)
+
+
+def test_linearizer_errors_and_plans():
+    row = llama.Mapping(W.PARTICLE7, [64, 64])
+    col = row.with_linearizer("col")
+    assert llama.plan(row, col)["path"] == "naive"  # a transposing copy: naive only
+    with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
+        llama.plan(row, col, path="permute")
+    soa_col = llama.Mapping(W.PARTICLE7, [64, 64], "soa_mb").with_linearizer("col")
+    assert llama.plan(col, soa_col)["path"] == "permute"  # equal storage orders: every path
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping(W.PARTICLE7, [64, 32]).with_linearizer("morton")
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping(W.PARTICLE7, [48, 48]).with_linearizer("morton")
+    sizes = llama.Mapping(W.LISTING1, [4]).leaf_types()
+    a = llama.Mapping(sizes[:2], [4], "soa_mb").with_linearizer("col")
+    b = llama.Mapping(sizes[2:], [4], "aos")
+    with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
+        llama.Mapping.split(a, b, [0, 1])
