@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libllama_b200.so")
 
 KINDS = {"aos": 0, "soa_sb": 1, "soa_mb": 2, "aosoa": 3, "one": 4}
 LINS = {"row": 0, "col": 1, "morton": 2}
-PATHS = {"auto": 0, "naive": 1, "blobcopy": 2, "run": 3, "permute": 4}
+PATHS = {"auto": 0, "naive": 1, "blobcopy": 2, "run": 3, "permute": 4, "transpose": 5}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 STATUS = {0: "LLAMA_OK", -1: "LLAMA_ERR_INVALID_ARGUMENT", -2: "LLAMA_ERR_SHAPE_MISMATCH",
           -3: "LLAMA_ERR_RECORD_MISMATCH", -4: "LLAMA_ERR_UNSUPPORTED", -5: "LLAMA_ERR_ALIGNMENT",

@@ -247,7 +247,8 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
 
     int e = 0;
     switch (plan->path) {
-      case LLAMA_PATH_NAIVE: {
+      case LLAMA_PATH_NAIVE:
+      case LLAMA_PATH_TRANSPOSE: {
         if (plan->naive_zero_fill) {
           llb::FillParams f = *plan->fill;
           for (int b = 0; b < f.nb; ++b) f.ptr[b] = static_cast<uint8_t*>(dst_blobs[b]);
@@ -256,7 +257,7 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
         llb::NaiveParams p = *plan->naive;
         for (int b = 0; b < s.nblobs(); ++b) p.sb[b] = static_cast<const uint8_t*>(src_blobs[b]);
         for (int b = 0; b < d.nblobs(); ++b) p.db[b] = static_cast<uint8_t*>(dst_blobs[b]);
-        e = llb::launch_naive(p, stream);
+        e = plan->path == LLAMA_PATH_TRANSPOSE ? llb::launch_transpose2d(p, stream) : llb::launch_naive(p, stream);
         break;
       }
       case LLAMA_PATH_BLOBCOPY: {

@@ -39,6 +39,17 @@ __device__ __forceinline__ uint64_t lin_storage(uint64_t i, const DevLin& l) {
   return f;
 }
 
+// The same for a 2-d index (y, x) without divisions.
+__device__ __forceinline__ uint64_t lin_storage2d(uint64_t y, uint64_t x, const DevLin& l) {
+  if (l.kind == LLAMA_COL_MAJOR) return x * l.ext[0] + y;
+  if (l.kind == LLAMA_MORTON) {
+    uint64_t f = 0;
+    for (uint32_t b = 0; b < l.bits; ++b) f |= (((y >> b) & 1ull) << (2 * b + 1)) | (((x >> b) & 1ull) << (2 * b));
+    return f;
+  }
+  return y * l.ext[1] + x;
+}
+
 // Heatmap: one count per byte of a resolved range.
 __device__ __forceinline__ void trace_bytes(const DevTrace& t, uint32_t blob, uint64_t off, uint32_t size) {
   if (!t.heat) return;

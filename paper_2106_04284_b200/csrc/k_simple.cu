@@ -90,6 +90,123 @@ int launch_naive(const NaiveParams& p, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// -------------------------------------------------------------- transpose
+// 2-d views of different linearisations (row / column-major / Morton, P:140-
+// 142): a CTA moves 32x32-record tiles, reading them in the source's storage
+// order (consecutive threads = consecutive source positions) into a
+// leaf-major shared tile (rows padded to 33 elements against bank
+// conflicts), then writing them in the destination's storage order.
+__device__ __forceinline__ void tile_order(uint32_t kind, uint32_t q, uint32_t& dy, uint32_t& dx) {
+  if (kind == LLAMA_COL_MAJOR) {
+    dy = q & 31;
+    dx = q >> 5;
+  } else if (kind == LLAMA_MORTON) {  // the last index supplies bit 0 (reading #26)
+    dx = (q & 1) | ((q >> 1) & 2) | ((q >> 2) & 4) | ((q >> 3) & 8) | ((q >> 4) & 16);
+    dy = ((q >> 1) & 1) | ((q >> 2) & 2) | ((q >> 3) & 4) | ((q >> 4) & 8) | ((q >> 5) & 16);
+  } else {
+    dy = q >> 5;
+    dx = q & 31;
+  }
+}
+
+// One element of `size` bytes; kAligned: every element of both sides is
+// naturally aligned (planner), so a typed access without runtime checks.
+template <bool kAligned>
+__device__ __forceinline__ void move_elem(uint8_t* d, const uint8_t* s, uint32_t size) {
+  if (!kAligned) {
+    copy_elem(d, s, size);
+    return;
+  }
+  switch (size) {
+    case 8: *reinterpret_cast<uint64_t*>(d) = *reinterpret_cast<const uint64_t*>(s); break;
+    case 4: *reinterpret_cast<uint32_t*>(d) = *reinterpret_cast<const uint32_t*>(s); break;
+    case 2: *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s); break;
+    default: *d = *s; break;
+  }
+}
+
+// Each thread owns the tile positions q = tid + 256*j (j < 4) of a side's
+// storage order; leaves in the outer loop so the four records' accesses of
+// one leaf are independent.  kUniform: every leaf of a side shares L and B
+// (not a split), so a record's block / lane are computed once, not per leaf.
+template <bool kUniform>
+__device__ __forceinline__ uint64_t tile_leaf_offset(uint64_t f, uint64_t q, uint64_t r, const DevLeaf& l) {
+  if (!kUniform) return leaf_offset(f, l);
+  return l.base + q * l.B + l.F + r * l.size;
+}
+
+template <bool kAligned, bool kUniform>
+__global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant__ NaiveParams p) {
+  extern __shared__ __align__(16) uint8_t tsm[];
+  const uint64_t tiles_x = (p.W + 31) / 32, n_tiles = tiles_x * ((p.H + 31) / 32);
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint64_t y0 = (t / tiles_x) * 32, x0 = (t % tiles_x) * 32;
+    uint64_t f[4], qb[4], rl[4];
+    uint32_t e[4];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t dy, dx;
+      tile_order(p.slin.kind, threadIdx.x + kThreads * j, dy, dx);
+      ok[j] = y0 + dy < p.H && x0 + dx < p.W;
+      f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.slin) : 0;
+      e[j] = dy * 33 + dx;
+      const DevLeaf& l0 = p.sl[0];
+      qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
+      rl[j] = f[j] - qb[j] * l0.L;
+    }
+    for (int k = 0; k < p.K; ++k) {
+      const DevLeaf l = p.sl[k];
+      const uint8_t* sb = p.sb[l.blob];
+      uint8_t* t = tsm + p.tbase[k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ok[j]) move_elem<kAligned>(t + e[j] * l.size, sb + tile_leaf_offset<kUniform>(f[j], qb[j], rl[j], l), l.size);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t dy, dx;
+      tile_order(p.dlin.kind, threadIdx.x + kThreads * j, dy, dx);
+      ok[j] = y0 + dy < p.H && x0 + dx < p.W;
+      f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.dlin) : 0;
+      e[j] = dy * 33 + dx;
+      const DevLeaf& l0 = p.dl[0];
+      qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
+      rl[j] = f[j] - qb[j] * l0.L;
+    }
+    for (int k = 0; k < p.K; ++k) {
+      const DevLeaf l = p.dl[k];
+      uint8_t* db = p.db[l.blob];
+      const uint8_t* t = tsm + p.tbase[k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ok[j]) move_elem<kAligned>(db + tile_leaf_offset<kUniform>(f[j], qb[j], rl[j], l), t + e[j] * l.size, l.size);
+    }
+    __syncthreads();
+  }
+}
+
+int launch_transpose2d(const NaiveParams& p, void* stream) {
+  const uint64_t n_tiles = ((p.W + 31) / 32) * ((p.H + 31) / 32);
+  if (n_tiles == 0) return 0;
+  static LaunchCache cache[4][64];
+  int dev = 0, per_sm = 1, sms = 148;
+  cudaGetDevice(&dev);
+  void (*const kerns[4])(NaiveParams) = {k_transpose2d<false, false>, k_transpose2d<true, false>,
+                                         k_transpose2d<false, true>, k_transpose2d<true, true>};
+  auto kern = kerns[(p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0)];
+  int e = prepare_kernel(kern, kThreads, (int)p.tsmem, &cache[(p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0)][dev & 63],
+                         &per_sm);
+  if (e) return e;
+  current_device_sms(&sms);
+  uint64_t grid = (uint64_t)sms * per_sm;
+  if (grid > n_tiles) grid = n_tiles;
+  kern<<<(unsigned)grid, kThreads, p.tsmem, (cudaStream_t)stream>>>(p);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
 // -------------------------------------------------------------- generator
 // Input recipe (not the method): byte b of leaf k of record i is byte b of
 // splitmix64(seed ^ (i*K + k)), written through the mapping's address function.

@@ -6,6 +6,7 @@
 namespace llb {
 
 int launch_naive(const NaiveParams& p, void* stream);
+int launch_transpose2d(const NaiveParams& p, void* stream);
 int launch_gen(const GenParams& p, void* stream);
 int launch_fill(const FillParams& p, void* stream);
 int launch_blobcopy(const BlobCopyParams& p, void* stream);

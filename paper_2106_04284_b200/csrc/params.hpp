@@ -63,8 +63,12 @@ struct NaiveParams {
   int32_t relin;      // 1: the sides are linearised differently (records located per side)
   DevLin slin, dlin;
   int32_t traced;     // 1: count address resolutions (tr[0] = src, tr[1] = dst)
-  int32_t pad2_;
+  uint32_t tsmem;     // TRANSPOSE: shared-memory bytes of a 32x32-record tile
   DevTrace tr[2];
+  uint64_t H, W;      // TRANSPOSE: the 2-d extents
+  uint32_t tbase[kMaxLeaves];  // TRANSPOSE: leaf k's 32x33-element tile at smem + tbase[k]
+  uint32_t taligned;           // TRANSPOSE: every element of both sides naturally aligned
+  uint32_t tuniform;           // TRANSPOSE: both sides share one L and B over all leaves
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];

@@ -86,6 +86,38 @@ void plan_naive(const Mapping& s, const Mapping& d, Plan* p) {
   if (p->naive_zero_fill) p->fill.reset(new FillParams(make_fill(d, 0)));
 }
 
+// 2-d views of different linearisations, records small enough for 32x32
+// tiles in <= 48 KB of shared memory, not traced.
+bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
+  if (s.trace || d.trace) { *why = "traced views count through the naive kernel"; return false; }
+  if (s.lin == d.lin) { *why = "equal linearisations"; return false; }
+  if (s.extents.size() != 2) { *why = "TRANSPOSE is for 2-d views"; return false; }
+  uint64_t smem = 0;
+  uint32_t base[kMaxLeaves];
+  for (int k = 0; k < s.K(); ++k) {
+    smem = (smem + 7) & ~7ull;
+    base[k] = (uint32_t)smem;
+    smem += 32ull * 33 * s.sizes[k];
+  }
+  if (smem > 48 * 1024) { *why = "records too wide for 32x32 tiles"; return false; }
+  plan_naive(s, d, p);
+  p->path = LLAMA_PATH_TRANSPOSE;
+  NaiveParams& n = *p->naive;
+  n.H = (uint64_t)s.extents[0];
+  n.W = (uint64_t)s.extents[1];
+  n.tsmem = (uint32_t)smem;
+  for (int k = 0; k < s.K(); ++k) n.tbase[k] = base[k];
+  n.tuniform = (s.uniform && d.uniform) ? 1 : 0;
+  n.taligned = 1;  // blobs are 16-B aligned: check the normal forms
+  for (const Mapping* m : {&s, &d})
+    for (int k = 0; k < m->K(); ++k) {
+      const uint64_t z = m->sizes[k];
+      const bool one_block = m->Bk[k] == 0 && m->Lk[k] >= m->N;
+      if ((m->base[k] + m->F[k]) % z || (!one_block && m->Bk[k] % z)) n.taligned = 0;
+    }
+  return true;
+}
+
 bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
   if (!same_layout(s, d)) { *why = "layouts differ"; return false; }
   if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
@@ -464,12 +496,18 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   // record (index) -> record (index) across storage orders, or counting every
   // address resolution (Trace / Heatmap): the element-wise kernel only
   if (s.lin != d.lin || s.trace || d.trace) {
+    if ((path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) && plan_transpose(s, d, out, &why))
+      return LLAMA_OK;
     if (path != LLAMA_PATH_AUTO && path != LLAMA_PATH_NAIVE) {
-      *err = "path not applicable to this mapping pair: linearised differently or traced (naive only)";
+      *err = "path not applicable to this mapping pair: linearised differently or traced: " + why;
       return LLAMA_ERR_UNSUPPORTED;
     }
     plan_naive(s, d, out);
     return LLAMA_OK;
+  }
+  if (path == LLAMA_PATH_TRANSPOSE) {
+    *err = "path not applicable to this mapping pair: TRANSPOSE needs differently linearised views";
+    return LLAMA_ERR_UNSUPPORTED;
   }
   switch (path) {
     case LLAMA_PATH_AUTO:

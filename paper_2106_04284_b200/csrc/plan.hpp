@@ -35,6 +35,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
 
 // Path-specific builders; return false (with *why) when not applicable.
 bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
+bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
 bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why);
 void plan_naive(const Mapping& s, const Mapping& d, Plan* p);

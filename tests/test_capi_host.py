@@ -240,7 +240,11 @@ def test_linearized_descriptor_matches_oracle(oracle_mod, lin, ext, name):
 def test_linearizer_errors_and_plans():
     row = llama.Mapping(W.PARTICLE7, [64, 64])
     col = row.with_linearizer("col")
-    assert llama.plan(row, col)["path"] == "naive"  # a transposing copy: naive only
+    assert llama.plan(row, col)["path"] == "transpose"  # a transposing copy: 32x32-record tiles
+    assert llama.plan(row, col, path="naive")["path"] == "naive"
+    with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
+        llama.plan(row, llama.Mapping(W.PARTICLE7, [64, 64], "soa_mb"), path="transpose")
+
     with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
         llama.plan(row, col, path="permute")
     soa_col = llama.Mapping(W.PARTICLE7, [64, 64], "soa_mb").with_linearizer("col")

@@ -45,20 +45,21 @@ def _pair(llama, oracle, schema, ext, sspec, slin, dspec, dlin, seed=3, paths=("
 KINDS = [("aos", 1, False), ("soa_mb", 1, False), ("aosoa", 8, False), ("aos", 1, True)]
 
 
-@pytest.mark.parametrize("ext", [[64, 33], [5, 7, 3], [1, 1]])
+@pytest.mark.parametrize("ext", [[64, 33], [5, 7, 3], [1, 1], [100, 37], [31, 1000]])
 @pytest.mark.parametrize("lins", [("row", "col"), ("col", "row"), ("col", "col")])
 def test_row_col_copies(llama, oracle_mod, ext, lins):
     for sk in KINDS:
         for dk in KINDS:
             _pair(llama, oracle_mod, W.LISTING1, ext, sk, lins[0], dk, lins[1],
-                  paths=("auto", "naive", "permute", "run", "blobcopy"))
+                  paths=("auto", "naive", "permute", "run", "blobcopy", "transpose"))
 
 
 @pytest.mark.parametrize("ext", [[32, 32], [8, 8, 8], [256]])
 def test_morton_copies(llama, oracle_mod, ext):
     for sk, dk in [(KINDS[0], KINDS[1]), (KINDS[2], KINDS[0]), (KINDS[1], KINDS[3])]:
         for lins in [("row", "morton"), ("morton", "col"), ("morton", "morton")]:
-            _pair(llama, oracle_mod, W.PARTICLE7, ext, sk, lins[0], dk, lins[1], paths=("auto", "naive", "permute"))
+            _pair(llama, oracle_mod, W.PARTICLE7, ext, sk, lins[0], dk, lins[1],
+                  paths=("auto", "naive", "permute", "transpose"))
 
 
 def test_split_linearised(llama, oracle_mod):
