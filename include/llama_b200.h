@@ -207,7 +207,9 @@ typedef enum {
   LLAMA_PATH_NAIVE = 1,    /* element-wise: thread per record, leaf loop */
   LLAMA_PATH_BLOBCOPY = 2, /* identical layout without padding: raw blob copy */
   LLAMA_PATH_RUN = 3,      /* field-run copy: common contiguous runs >= 16 B */
-  LLAMA_PATH_PERMUTE = 4   /* TMA-staged tile permute through shared memory */
+  LLAMA_PATH_PERMUTE = 4,  /* TMA-staged tile permute through shared memory */
+  LLAMA_PATH_TRANSPOSE = 5 /* 2-d views of different linearisations: 32x32-record tiles through
+                              shared memory, read in source and written in destination storage order */
 } llama_path;
 
 typedef struct {
