@@ -232,6 +232,7 @@ typedef struct {
   uint64_t src_bytes;       /* sum of source blob sizes */
   uint64_t dst_bytes;       /* sum of destination blob sizes */
   int32_t word_moves;       /* PERMUTE: > 0 if AoS <-> AoS word mode is used (words per record) */
+  int32_t direct;           /* PERMUTE: 1 = direct variant (AoS side through TMA, SoA side element-wise) */
 } llama_plan_info;
 
 llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_map,

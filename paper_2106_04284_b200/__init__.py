@@ -64,7 +64,8 @@ class _Options(ctypes.Structure):
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("moves", ctypes.c_int32), ("tma", ctypes.c_int32), ("src_bytes", ctypes.c_uint64),
-                ("dst_bytes", ctypes.c_uint64), ("word_moves", ctypes.c_int32)]
+                ("dst_bytes", ctypes.c_uint64), ("word_moves", ctypes.c_int32),
+                ("direct", ctypes.c_int32)]
 
 
 def _load():
@@ -353,7 +354,7 @@ def plan(src_map, dst_map, path=None, tile_records=0):
     _check(_lib.llama_plan(src_map.handle, dst_map.handle, ctypes.byref(opt), ctypes.byref(info)))
     return {"path": PATH_NAMES[info.path], "tile_records": info.tile_records, "smem_bytes": info.smem_bytes,
             "moves": info.moves, "tma": bool(info.tma), "src_bytes": int(info.src_bytes),
-            "dst_bytes": int(info.dst_bytes), "word_moves": int(info.word_moves)}
+            "dst_bytes": int(info.dst_bytes), "word_moves": int(info.word_moves), "direct": bool(info.direct)}
 
 
 def generate(m, blobs, seed=42, pad_byte=0, stream=None):

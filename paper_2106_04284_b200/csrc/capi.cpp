@@ -203,6 +203,13 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
       out->tma = (int32_t)plan->perm->tma;
       out->word_moves = (int32_t)plan->perm->n_wmoves;
     }
+    if (plan->direct) {
+      out->tile_records = (int32_t)plan->direct->T;
+      out->smem_bytes = plan->smem_bytes;
+      out->moves = (int32_t)plan->direct->K;
+      out->tma = 1;
+      out->direct = 1;
+    }
     return LLAMA_OK;
   } catch (...) {
     return fail(LLAMA_ERR_OOM, "planning failed");
@@ -286,6 +293,13 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
         break;
       }
       case LLAMA_PATH_PERMUTE: {
+        if (plan->direct) {
+          llb::DirectParams q = *plan->direct;
+          for (int b = 0; b < s.nblobs(); ++b) q.blobs[0][b] = static_cast<uint8_t*>(const_cast<void*>(src_blobs[b]));
+          for (int b = 0; b < d.nblobs(); ++b) q.blobs[1][b] = static_cast<uint8_t*>(dst_blobs[b]);
+          e = llb::launch_permute_direct(q, stream);
+          break;
+        }
         llb::PermParams p = *plan->perm;
         for (int b = 0; b < s.nblobs(); ++b) p.blobs[0][b] = static_cast<uint8_t*>(const_cast<void*>(src_blobs[b]));
         for (int b = 0; b < d.nblobs(); ++b) p.blobs[1][b] = static_cast<uint8_t*>(dst_blobs[b]);

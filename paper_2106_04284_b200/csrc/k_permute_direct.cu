@@ -1,0 +1,245 @@
+// k_permute_direct.cu -- AoS <-> SoA for records with many leaves (HEP100,
+// P:775): the tile permute's SoA side would be K TMA ops of T * s_k bytes per
+// tile (100 ops of 64-512 B for HEP), so here only the AoS side goes through
+// shared memory (one TMA op per tile, an ns-stage ring) and the SoA side is
+// read / written element by element by the consumer warps: a warp takes one
+// leaf of 32 consecutive records, so every global access is a contiguous
+// 32 * s_k-byte run.  Warp-specialised like k_permute_ws:
+//   AoS -> SoA: full[s]  source tile landed  (TMA -> consumers)
+//               empty[s] consumers done      (consumers -> producer: refill)
+//   SoA -> AoS: dfull[s] destination tile written (consumers -> producer: store)
+//               dempty[s] its store read it out    (producer -> consumers)
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace llb {
+
+namespace {
+constexpr int kCons = 256;  // consumer threads
+constexpr int kBars = 128;  // 2 rings x <= 8 stages x 8 B
+}  // namespace
+
+// An element of `s` bytes at a shared-memory address aligned to `a`.
+__device__ __forceinline__ uint64_t sm_gather(const uint8_t* p, uint32_t s, uint32_t a) {
+  if (a >= s) {
+    switch (s) {
+      case 8: return *reinterpret_cast<const uint64_t*>(p);
+      case 4: return *reinterpret_cast<const uint32_t*>(p);
+      case 2: return *reinterpret_cast<const uint16_t*>(p);
+      default: return *p;
+    }
+  }
+  uint64_t v = 0;
+  if (a == 4) {
+    v = (uint64_t)*reinterpret_cast<const uint32_t*>(p) | ((uint64_t)*reinterpret_cast<const uint32_t*>(p + 4) << 32);
+  } else if (a == 2) {
+    for (uint32_t j = 0; j < s; j += 2) v |= (uint64_t)*reinterpret_cast<const uint16_t*>(p + j) << (8 * j);
+  } else {
+    for (uint32_t j = 0; j < s; ++j) v |= (uint64_t)p[j] << (8 * j);
+  }
+  return v;
+}
+
+__device__ __forceinline__ void sm_scatter(uint8_t* p, uint64_t v, uint32_t s, uint32_t a) {
+  if (a >= s) {
+    switch (s) {
+      case 8: *reinterpret_cast<uint64_t*>(p) = v; return;
+      case 4: *reinterpret_cast<uint32_t*>(p) = (uint32_t)v; return;
+      case 2: *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; return;
+      default: *p = (uint8_t)v; return;
+    }
+  }
+  if (a == 4) {
+    *reinterpret_cast<uint32_t*>(p) = (uint32_t)v;
+    *reinterpret_cast<uint32_t*>(p + 4) = (uint32_t)(v >> 32);
+  } else if (a == 2) {
+    for (uint32_t j = 0; j < s; j += 2) *reinterpret_cast<uint16_t*>(p + j) = (uint16_t)(v >> (8 * j));
+  } else {
+    for (uint32_t j = 0; j < s; ++j) p[j] = (uint8_t)(v >> (8 * j));
+  }
+}
+
+__device__ __forceinline__ uint64_t gl_load(const uint8_t* p, uint32_t s, uint32_t a) {
+  if (a < s) {
+    uint64_t v = 0;
+    for (uint32_t j = 0; j < s; ++j) v |= (uint64_t)__ldcs(p + j) << (8 * j);
+    return v;
+  }
+  switch (s) {
+    case 8: return __ldcs(reinterpret_cast<const unsigned long long*>(p));
+    case 4: return __ldcs(reinterpret_cast<const unsigned int*>(p));
+    case 2: return __ldcs(reinterpret_cast<const unsigned short*>(p));
+    default: return __ldcs(p);
+  }
+}
+
+__device__ __forceinline__ void gl_store(uint8_t* p, uint64_t v, uint32_t s, uint32_t a) {
+  if (a < s) {
+    for (uint32_t j = 0; j < s; ++j) __stcs(p + j, (uint8_t)(v >> (8 * j)));
+    return;
+  }
+  switch (s) {
+    case 8: __stcs(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v); return;
+    case 4: __stcs(reinterpret_cast<unsigned int*>(p), (unsigned int)v); return;
+    case 2: __stcs(reinterpret_cast<unsigned short*>(p), (unsigned short)v); return;
+    default: __stcs(p, (uint8_t)v); return;
+  }
+}
+
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory"); }
+
+template <bool kA2S>
+__global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_constant__ DirectParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* ready = reinterpret_cast<uint64_t*>(smem);  // A2S: full; S2A: dfull
+  uint64_t* freed = ready + 8;                         // A2S: empty; S2A: dempty
+  uint8_t* ring = smem + kBars;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!kA2S)  // destination padding bytes are never written: zero the ring once
+    for (uint32_t o = 16 * tid; o < p.ns * p.stage; o += 16 * (kCons + 32))
+      *reinterpret_cast<uint4*>(ring + o) = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (uint32_t s = 0; s < p.ns; ++s) {
+      mbar_init(&ready[s], 1);
+      mbar_init(&freed[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (kA2S && blockIdx.x == 0 && warp < kCons / 32)
+    for (uint32_t g = 0; g < p.n_gaps; ++g)
+      for (uint32_t o = tid; o < p.gap_len[g]; o += kCons) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
+
+  const uint64_t first = blockIdx.x, stride = gridDim.x;
+  const uint32_t n_my = first < p.n_tiles ? (uint32_t)((p.n_tiles - first + stride - 1) / stride) : 0;
+  const int X = kA2S ? 0 : 1;  // the AoS side
+  uint8_t* ag = p.blobs[X][p.ablob] + p.abase;
+  auto tile_rec = [&](uint32_t i) -> uint32_t {
+    const uint64_t t0 = (first + (uint64_t)i * stride) * p.T;
+    return (uint32_t)(p.N - t0 < p.T ? p.N - t0 : p.T);
+  };
+
+  if (warp == kCons / 32) {  // --------------------------------- producer
+    if (lane == 0) {
+      if (kA2S) {
+        auto load = [&](uint32_t i, uint32_t s) {
+          const uint64_t t0 = (first + (uint64_t)i * stride) * p.T;
+          const uint32_t body = (tile_rec(i) * p.S) & ~15u;
+          mbar_arrive_expect_tx(&ready[s], body);
+          if (body) bulk_g2s(ring + (size_t)s * p.stage, ag + t0 * p.S, body, &ready[s]);
+        };
+        for (uint32_t i = 0; i < p.ns && i < n_my; ++i) load(i, i);
+        uint32_t s = 0, ph = 0;
+        for (uint32_t i = 0; i + p.ns < n_my; ++i) {
+          mbar_wait(&freed[s], ph);
+          load(i + p.ns, s);
+          if (++s == p.ns) { s = 0; ph ^= 1; }
+        }
+      } else {
+        uint32_t s = 0, ph = 0;
+        for (uint32_t i = 0; i < n_my; ++i) {
+          const uint64_t t0 = (first + (uint64_t)i * stride) * p.T;
+          const uint32_t body = (tile_rec(i) * p.S) & ~15u;
+          mbar_wait(&ready[s], ph);
+          if (body) bulk_s2g(ag + t0 * p.S, ring + (size_t)s * p.stage, body);
+          bulk_commit();
+          bulk_wait_read<0>();
+          mbar_arrive(&freed[s]);
+          if (++s == p.ns) { s = 0; ph ^= 1; }
+        }
+        bulk_wait_all();
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  uint32_t s = 0, ph = 0;
+  for (uint32_t i = 0; i < n_my; ++i) {
+    const uint64_t t0 = (first + (uint64_t)i * stride) * p.T;
+    const uint32_t nrec = tile_rec(i);
+    const uint32_t bytes = nrec * p.S, body = bytes & ~15u;
+    uint8_t* img = ring + (size_t)s * p.stage;
+    if (tid == 0) mbar_wait(kA2S ? &ready[s] : &freed[s], kA2S ? ph : ph ^ 1);
+    cons_sync();
+    if (kA2S && body < bytes) {  // sub-16-byte tail of the last tile
+      for (uint32_t o = body + tid; o < bytes; o += kCons) img[o] = ag[t0 * p.S + o];
+      cons_sync();
+    }
+    // warp w takes leaves w, w+8, ...; kU leaves at a time, so each lane has
+    // 2*kU independent accesses in flight (records lane and lane+32; T = 64)
+    constexpr int kU = kA2S ? 4 : 8;  // SoA -> AoS: more global loads in flight
+    const bool ok0 = lane < nrec, ok1 = lane + 32 < nrec;
+    for (uint32_t k0 = warp; k0 < p.K; k0 += kU * (kCons / 32)) {
+      uint64_t v[kU][2];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t k = k0 + u * (kCons / 32);
+        if (k >= p.K) break;
+        const DirectLeaf& l = p.leaf[k];
+        if (kA2S) {
+          v[u][0] = ok0 ? sm_gather(img + lane * p.S + l.F, l.size, l.a_img) : 0;
+          v[u][1] = ok1 ? sm_gather(img + (lane + 32) * p.S + l.F, l.size, l.a_img) : 0;
+        } else {
+          const uint8_t* g = p.blobs[0][l.blob] + l.gbase + t0 * l.size;
+          v[u][0] = ok0 ? gl_load(g + (uint64_t)lane * l.size, l.size, l.a_glob) : 0;
+          v[u][1] = ok1 ? gl_load(g + (uint64_t)(lane + 32) * l.size, l.size, l.a_glob) : 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t k = k0 + u * (kCons / 32);
+        if (k >= p.K) break;
+        const DirectLeaf& l = p.leaf[k];
+        if (kA2S) {
+          uint8_t* g = p.blobs[1][l.blob] + l.gbase + t0 * l.size;
+          if (ok0) gl_store(g + (uint64_t)lane * l.size, v[u][0], l.size, l.a_glob);
+          if (ok1) gl_store(g + (uint64_t)(lane + 32) * l.size, v[u][1], l.size, l.a_glob);
+        } else {
+          if (ok0) sm_scatter(img + lane * p.S + l.F, v[u][0], l.size, l.a_img);
+          if (ok1) sm_scatter(img + (lane + 32) * p.S + l.F, v[u][1], l.size, l.a_img);
+        }
+      }
+    }
+    if (!kA2S) {
+      if (body < bytes) {  // the last tile's sub-16-byte tail goes out directly
+        cons_sync();
+        for (uint32_t o = body + tid; o < bytes; o += kCons) ag[t0 * p.S + o] = img[o];
+      }
+      fence_proxy_async_smem();  // generic-proxy image writes -> the TMA store's reads
+    }
+    cons_sync();
+    if (tid == 0) mbar_arrive(kA2S ? &freed[s] : &ready[s]);
+    if (++s == p.ns) { s = 0; ph ^= 1; }
+  }
+}
+
+int launch_permute_direct(const DirectParams& p, void* stream) {
+  if (p.n_tiles == 0) return 0;
+  static LaunchCache cache[2][64];
+  int dev = 0, per_sm = 1, sms = 148;
+  cudaGetDevice(&dev);
+  const int smem = kBars + (int)(p.ns * p.stage);
+  auto kern = p.a2s ? k_permute_direct<true> : k_permute_direct<false>;
+  int e = prepare_kernel(kern, kCons + 32, smem, &cache[p.a2s ? 1 : 0][dev & 63], &per_sm);
+  if (e) return e;
+  current_device_sms(&sms);
+  uint64_t grid = (uint64_t)sms * per_sm;
+  if (grid > p.n_tiles) grid = p.n_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kCons + 32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, p);
+  count_launch();
+  return le != cudaSuccess ? (int)le : (int)cudaGetLastError();
+}
+
+}  // namespace llb

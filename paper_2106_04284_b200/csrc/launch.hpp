@@ -15,6 +15,7 @@ int launch_run(const RunParams& p, void* stream);
 int launch_permute(const PermParams& p, int smem_bytes, void* stream);     // chooses v1 / warp-specialised
 int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream);
 int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream);
+int launch_permute_direct(const DirectParams& p, void* stream);
 
 int launch_move_generic(const MoveParams& p, void* stream);
 int launch_move_runs(const MoveParams& p, void* stream);

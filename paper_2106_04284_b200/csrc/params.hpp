@@ -250,6 +250,37 @@ struct MoveParams {
   DevTrace tr;
 };
 
+// ------------------------------------------------------- direct permute
+// AoS <-> SoA with many leaves (HEP100): the AoS side moves as one TMA op per
+// tile through a shared-memory ring, the SoA side element by element with
+// coalesced global accesses (a warp = 32 consecutive records of one leaf) --
+// no per-leaf TMA segments of T * s_k bytes.
+struct DirectLeaf {
+  uint64_t gbase;    // SoA side: byte offset of record 0's element in its blob
+  uint32_t F;        // AoS side: offset of the leaf inside a record
+  uint32_t blob;     // SoA side blob
+  uint16_t size;
+  uint8_t a_img;     // alignment of every (r * S + F) in the AoS image (1, 2, 4, 8)
+  uint8_t a_glob;    // alignment of every SoA element address
+  uint32_t pad_;
+};
+
+struct DirectParams {
+  uint64_t N, n_tiles;
+  uint32_t T, K, S;  // S: AoS record stride
+  uint32_t a2s;      // 1: AoS -> SoA (ring holds source tiles); 0: SoA -> AoS (ring holds destination tiles)
+  uint32_t ns, stage;
+  uint64_t abase;    // AoS side: byte offset of record 0 in blob `ablob`
+  uint32_t ablob;
+  uint32_t n_gaps;   // AoS -> aligned SoA SB: padding between sub-arrays, zeroed by CTA 0
+  uint32_t gap_blob[kMaxLeaves];
+  uint32_t gap_len[kMaxLeaves];
+  uint64_t gap_off[kMaxLeaves];
+  DirectLeaf leaf[kMaxLeaves];
+  uint8_t* blobs[2][kMaxBlobs];
+};
+static_assert(sizeof(DirectParams) <= 32764, "DirectParams exceeds the kernel parameter limit");
+
 // kernel parameter blocks travel as __grid_constant__ arguments (<= 32764 B)
 static_assert(sizeof(PermParams) <= 32764, "PermParams exceeds the kernel parameter limit");
 static_assert(sizeof(NaiveParams) <= 32764, "NaiveParams exceeds the kernel parameter limit");

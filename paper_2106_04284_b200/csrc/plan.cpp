@@ -189,6 +189,74 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
   return true;
 }
 
+// AoS <-> SoA with many leaves (measured on HEP100): the AoS side
+// through a TMA ring, the SoA side element-wise with coalesced accesses.
+bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
+  const uint64_t mode = env_u64("LLAMA_DIRECT", 1);  // 0: off; 2: any leaf count (tests)
+  if (mode == 0) { *why = "disabled"; return false; }
+  if (!s.uniform || !d.uniform) { *why = "split"; return false; }
+  const bool a2s = s.kind == LLAMA_AOS && d.soa();
+  const bool s2a = s.soa() && d.kind == LLAMA_AOS;
+  if (!a2s && !s2a) { *why = "not AoS <-> SoA"; return false; }
+  if (s.K() <= 16 && mode != 2) { *why = "few leaves: the tile permute"; return false; }
+  const Mapping& A = a2s ? s : d;
+  const Mapping& So = a2s ? d : s;
+  const uint64_t S = A.B;
+  if (S == 0 || A.L != 1) { *why = "AoS stride"; return false; }
+  // measured: a win for naturally aligned AoS records (HEP aligned <-> SoA MB
+  // 2.4 -> 3.4 TB/s), a loss for packed ones whose misaligned leaves split
+  // into 1-4 byte pieces (2.8 -> 2.5 TB/s)
+  if (mode != 2)
+    for (int k = 0; k < A.K(); ++k)
+      if (A.F[k] % A.sizes[k] || S % A.sizes[k]) { *why = "packed AoS: the tile permute"; return false; }
+  // T = 64 records per tile (two per lane); ns = 2 stages, so several CTAs
+  // per SM keep enough consumer warps busy (measured on HEP100)
+  const uint64_t T = 64;
+  if (tile_records > 0 && tile_records != 64) { *why = "the direct variant uses 64-record tiles"; return false; }
+  const uint64_t stage = align16(T * S);
+  const uint64_t ns = std::min<uint64_t>(8, std::max<uint64_t>(2, env_u64("LLAMA_DIRECT_STAGES", 2)));
+  if (ns * stage > 200 * 1024) { *why = "record too wide"; return false; }
+  p->direct.reset(new DirectParams);
+  DirectParams& dp = *p->direct;
+  std::memset(&dp, 0, sizeof(dp));
+  dp.N = s.N;
+  dp.T = (uint32_t)T;
+  dp.K = (uint32_t)s.K();
+  dp.S = (uint32_t)S;
+  dp.a2s = a2s ? 1 : 0;
+  dp.ns = (uint32_t)ns;
+  dp.stage = (uint32_t)stage;
+  dp.n_tiles = ceil_div(s.N, T);
+  dp.abase = A.base[0];
+  dp.ablob = A.blob[0];
+  auto lb = [](uint64_t x) { return x ? (x & (~x + 1)) : 16ull; };
+  for (int k = 0; k < s.K(); ++k) {
+    DirectLeaf& l = dp.leaf[k];
+    l.gbase = So.base[k] + So.F[k];
+    l.blob = So.blob[k];
+    l.F = (uint32_t)A.F[k];
+    l.size = (uint16_t)s.sizes[k];
+    l.a_img = (uint8_t)std::min<uint64_t>(8, std::min(lb(S), lb(A.F[k])));
+    l.a_glob = (uint8_t)std::min<uint64_t>(8, std::min<uint64_t>(lb(l.gbase), 16));
+  }
+  if (a2s && d.has_padding()) {  // aligned SoA SB: the gaps between sub-arrays
+    if (d.kind != LLAMA_SOA_SINGLE_BLOB) { *why = "padded destination"; return false; }
+    uint64_t end = 0;
+    for (int k = 0; k < d.K(); ++k) {
+      if (d.base[k] > end) {
+        dp.gap_blob[dp.n_gaps] = d.blob[k];
+        dp.gap_off[dp.n_gaps] = end;
+        dp.gap_len[dp.n_gaps] = (uint32_t)(d.base[k] - end);
+        ++dp.n_gaps;
+      }
+      end = d.base[k] + d.N * d.sizes[k];
+    }
+  }
+  p->path = LLAMA_PATH_PERMUTE;
+  p->smem_bytes = (int)(128 + ns * stage);
+  return true;
+}
+
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
   // every part must spread its records over its blobs (not One)
   for (const Mapping* m : {&s, &d}) {
@@ -517,6 +585,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       // identities of SoA layouts with many leaves (many blobs / segments): the bulk blob copy
       // (HEP SoA MB: 6.4 TB/s vs 1.8 for 200 TMA segment ops per tile)
       if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      if (plan_direct(s, d, tile_records, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
       if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
@@ -532,6 +601,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
       break;
     case LLAMA_PATH_PERMUTE:
+      if (plan_direct(s, d, tile_records, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
       break;
     default:

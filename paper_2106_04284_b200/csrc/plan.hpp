@@ -23,6 +23,7 @@ struct Plan {
   std::unique_ptr<BulkCopyParams> bulkcopy;  // TMA variant of the blob copy
   std::unique_ptr<RunParams> run;
   std::unique_ptr<PermParams> perm;
+  std::unique_ptr<DirectParams> direct;  // PERMUTE path, direct variant (AoS <-> SoA, many leaves)
 };
 
 // Checks S:484-486 (same leaf types, same extents).
@@ -38,6 +39,7 @@ bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why
 bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
 bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why);
+bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why);
 void plan_naive(const Mapping& s, const Mapping& d, Plan* p);
 
 FillParams make_fill(const Mapping& m, uint8_t value);

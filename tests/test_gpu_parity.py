@@ -352,3 +352,31 @@ def test_one_and_mapping_c_sources(llama, oracle_mod, n):
         with pytest.raises(llama.LlamaError, match="UNSUPPORTED"):
             llama.copy(sm, sm.alloc("cuda"), llama.Mapping(W.LISTING1, [n], "one"),
                        llama.Mapping(W.LISTING1, [n], "one").alloc("cuda"))
+
+
+# ------------------------------------------------ direct AoS <-> SoA variant
+@pytest.mark.parametrize("schema_name", ["listing1", "particle7", "hep100"])
+@pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097])
+def test_direct_variant_forced(llama, oracle_mod, schema_name, n, monkeypatch):
+    """The direct permute (AoS side through TMA, SoA side element-wise) for
+    every AoS <-> SoA pair, forced for few-leaf records too (LLAMA_DIRECT=2):
+    odd record strides exercise the byte-wise shared-memory accesses."""
+    monkeypatch.setenv("LLAMA_DIRECT", "2")
+    schema = W.SCHEMAS[schema_name]
+    names = ["aos", "aos_aligned", "soa_mb", "soa_sb", "soa_sb_aligned"]
+    for a in names:
+        for b in names:
+            if ("aos" in a) == ("aos" in b):
+                continue
+            sm = llama.Mapping(schema, [n], *KINDS[a])
+            dm = llama.Mapping(schema, [n], *KINDS[b])
+            assert llama.plan(sm, dm)["direct"], (a, b)
+            run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b])
+
+
+def test_direct_chosen_for_hep(llama):
+    m = {k: llama.Mapping(W.HEP100, [4096], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
+    assert llama.plan(m["aos_aligned"], m["soa_mb"])["direct"]
+    assert llama.plan(m["soa_mb"], m["aos_aligned"])["direct"]
+    assert not llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: misaligned leaves
+    assert not llama.plan(m["aos"], m["aos_aligned"])["direct"]
