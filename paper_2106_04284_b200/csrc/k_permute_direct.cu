@@ -29,15 +29,17 @@ __device__ __forceinline__ uint64_t sm_gather(const uint8_t* p, uint32_t s, uint
       default: return *p;
     }
   }
-  uint64_t v = 0;
-  if (a == 4) {
-    v = (uint64_t)*reinterpret_cast<const uint32_t*>(p) | ((uint64_t)*reinterpret_cast<const uint32_t*>(p + 4) << 32);
-  } else if (a == 2) {
-    for (uint32_t j = 0; j < s; j += 2) v |= (uint64_t)*reinterpret_cast<const uint16_t*>(p + j) << (8 * j);
-  } else {
-    for (uint32_t j = 0; j < s; ++j) v |= (uint64_t)p[j] << (8 * j);
-  }
-  return v;
+  if (a == 4)  // s == 8
+    return (uint64_t)*reinterpret_cast<const uint32_t*>(p) | ((uint64_t)*reinterpret_cast<const uint32_t*>(p + 4) << 32);
+  if (s == 1) return *p;
+  // misaligned: the aligned 32-bit words covering the element, funnel-shifted
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)3);
+  const uint32_t sh = 8 * (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3);
+  const uint32_t w0 = w[0], w1 = w[1];
+  const uint32_t lo = __funnelshift_r(w0, w1, sh);
+  if (s <= 4) return s == 4 ? lo : (s == 2 ? (lo & 0xFFFFu) : lo);
+  const uint32_t hi = __funnelshift_r(w1, w[2], sh);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
 __device__ __forceinline__ void sm_scatter(uint8_t* p, uint64_t v, uint32_t s, uint32_t a) {
@@ -220,7 +222,7 @@ int launch_permute_direct(const DirectParams& p, void* stream) {
   static LaunchCache cache[2][64];
   int dev = 0, per_sm = 1, sms = 148;
   cudaGetDevice(&dev);
-  const int smem = kBars + (int)(p.ns * p.stage);
+  const int smem = kBars + (int)(p.ns * p.stage) + 16;  // + slack: funnel reads of the last element
   auto kern = p.a2s ? k_permute_direct<true> : k_permute_direct<false>;
   int e = prepare_kernel(kern, kCons + 32, smem, &cache[p.a2s ? 1 : 0][dev & 63], &per_sm);
   if (e) return e;

@@ -253,7 +253,7 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
     }
   }
   p->path = LLAMA_PATH_PERMUTE;
-  p->smem_bytes = (int)(128 + ns * stage);
+  p->smem_bytes = (int)(128 + ns * stage + 16);
   return true;
 }
 
