@@ -275,6 +275,16 @@ void llama_stager_destroy(llama_stager* st); /* NULL-safe; synchronises its stre
 llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
                                const llama_mapping* dst_map, void* const* dst_blobs, void* stream);
 
+/* `count` staged copies as one pipeline: the staging buffers rotate from one
+ * copy's slabs straight into the next's, so the DMA engines do not drain
+ * between copies (one fill / drain per batch instead of per copy).  Every copy
+ * is validated before anything is enqueued; same contract as
+ * llama_copy_staged per copy.  src_blobs[i] / dst_blobs[i]: copy i's blob
+ * pointer arrays. */
+llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llama_mapping* const* src_maps,
+                                     void* const* const* src_blobs, const llama_mapping* const* dst_maps,
+                                     void* const* const* dst_blobs, void* stream);
+
 /* ------------------------------------------------------------------------
  * n-body move (Listing P:643-645, §4.1, §4.2
  * P:698-743): in place on one view, for every particle i and c in {X,Y,Z}

@@ -38,7 +38,7 @@ EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_ma
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
            "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
-           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_nbody_move",
+           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_copy_staged_batch", "llama_nbody_move",
            "llama_nbody_move_ex"]
 MOVE_PATHS = {"auto": 0, "generic": 1, "runs": 2, "aos": 3}
 MOVE_PATH_NAMES = {v: k for k, v in MOVE_PATHS.items()}
@@ -103,6 +103,8 @@ def _load():
     lib.llama_stager_destroy.argtypes = [ctypes.c_void_p]
     lib.llama_stager_destroy.restype = None
     lib.llama_copy_staged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
+    lib.llama_copy_staged_batch.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_void_p), P(vpp),
+                                            P(ctypes.c_void_p), P(vpp), ctypes.c_void_p]
     lib.llama_launch_count.restype = ctypes.c_uint64
     lib.llama_status_string.restype = ctypes.c_char_p
     lib.llama_nbody_move.argtypes = [ctypes.c_void_p, vpp, P(ctypes.c_int32), P(ctypes.c_int32), ctypes.c_float,
@@ -346,6 +348,20 @@ def copy_staged(stager, src_map, src_blobs, dst_map, dst_blobs, stream=None):
     d = _ptrs(dst_blobs, dst_map.blob_sizes(), "dst_blobs", device_only=False)
     _check(_lib.llama_copy_staged(stager.handle, src_map.handle, s, dst_map.handle, d, _stream(stream)))
 
+
+
+def copy_staged_batch(stager, copies, stream=None):
+    """Several staged copies as one pipeline (llama_copy_staged_batch):
+    copies = [(src_map, src_blobs, dst_map, dst_blobs), ...]."""
+    n = len(copies)
+    vp = ctypes.POINTER(ctypes.c_void_p)
+    sm = (ctypes.c_void_p * n)(*[c[0].handle for c in copies])
+    dm = (ctypes.c_void_p * n)(*[c[2].handle for c in copies])
+    keep = [(_ptrs(c[1], c[0].blob_sizes(), "src_blobs", device_only=False),
+             _ptrs(c[3], c[2].blob_sizes(), "dst_blobs", device_only=False)) for c in copies]
+    sb = (vp * n)(*[ctypes.cast(k[0], vp) for k in keep])
+    db = (vp * n)(*[ctypes.cast(k[1], vp) for k in keep])
+    _check(_lib.llama_copy_staged_batch(stager.handle, n, sm, sb, dm, db, _stream(stream)))
 
 def plan(src_map, dst_map, path=None, tile_records=0):
     """The planner's decision for a pair (no device work)."""

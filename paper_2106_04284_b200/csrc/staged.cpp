@@ -151,108 +151,149 @@ llama_status llama_stager_create(uint64_t slab_bytes, llama_stager** out) {
 
 void llama_stager_destroy(llama_stager* st) { delete st; }
 
-llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
-                               const llama_mapping* dst_map, void* const* dst_blobs, void* stream) {
-  if (!st || !src_map || !dst_map || !src_blobs || !dst_blobs)
+}  // extern "C"
+
+namespace {
+
+// One copy of a batch: validated, with its slab size.
+struct StagedJob {
+  const llama_mapping* sm;
+  void* const* sb;
+  const llama_mapping* dm;
+  void* const* db;
+  uint64_t n = 0;  // records per slab
+};
+
+llama_status prepare_job(llama_stager* st, StagedJob* jb) {
+  if (!jb->sm || !jb->dm || !jb->sb || !jb->db) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  const llb::Mapping& s = jb->sm->m;
+  const llb::Mapping& d = jb->dm->m;
+  if (s.types != d.types) return llb::set_error(LLAMA_ERR_RECORD_MISMATCH, "record dimensions differ");
+  if (s.extents != d.extents) return llb::set_error(LLAMA_ERR_SHAPE_MISMATCH, "array extents differ");
+  for (int b = 0; b < s.nblobs(); ++b)
+    if (s.blob_sizes[b] && !jb->sb[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL src blob");
+  for (int b = 0; b < d.nblobs(); ++b)
+    if (d.blob_sizes[b] && !jb->db[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL dst blob");
+  const uint64_t N = s.N;
+  if (d.collides())
+    return llb::set_error(LLAMA_ERR_UNSUPPORTED, "destination maps several records onto one location");
+  if (s.trace || d.trace)
+    return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a traced view (use llama_copy)");
+  if (s.lin != d.lin)  // equal storage orders: slabs of storage positions correspond
+    return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy between differently linearised views");
+  if (!s.uniform || !d.uniform || s.kind == LLAMA_ONE || d.kind == LLAMA_ONE)
+    return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a split / one mapping (copy its blobs, then llama_copy)");
+  if (d.footprint_bytes() == 0) return LLAMA_OK;
+  // slab unit: whole blocks of every blocked side (lcm of the lane counts)
+  uint64_t unit = 1;
+  for (const llb::Mapping* m : {&s, &d})
+    if (!m->soa()) unit = unit / gcd64(unit, m->L) * m->L;
+  // slab size from the per-record footprint, then shrunk until both 1-D
+  // views fit one staging buffer
+  const uint64_t per = std::max<uint64_t>(1, std::max(s.footprint_bytes(), d.footprint_bytes()) / std::max<uint64_t>(N, 1));
+  uint64_t n = std::max<uint64_t>(unit, st->cap / per / unit * unit);
+  if (n > N) n = (N + unit - 1) / unit * unit;
+  std::vector<uint64_t> lbs, lbd;
+  for (;;) {
+    const uint64_t nn = std::min(n, N);
+    llama_mapping* ls = st->view(jb->sm, nn);
+    llama_mapping* ld = st->view(jb->dm, nn);
+    if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
+    if (layout_local(ls->m, &lbs) <= st->cap && layout_local(ld->m, &lbd) <= st->cap) break;
+    if (n <= unit) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "one slab of whole AoSoA blocks exceeds the staging buffer");
+    n = std::max(unit, (n / 2) / unit * unit);
+  }
+  jb->n = n;
+  return LLAMA_OK;
+}
+
+// Enqueues the slabs of one job; c counts slabs over the whole batch, so the
+// three buffers keep rotating from one job into the next (no drain between).
+llama_status enqueue_job(llama_stager* st, const StagedJob& jb, uint64_t* c) {
+  const llb::Mapping& s = jb.sm->m;
+  const llb::Mapping& d = jb.dm->m;
+  if (jb.n == 0) return LLAMA_OK;  // nothing to write
+  const uint64_t N = s.N, n = jb.n;
+  cudaError_t e;
+  // destination padding outside every slab range: gaps between aligned
+  // SoA single-blob sub-arrays (reading #9) -> zero them from the device
+  if (d.kind == LLAMA_SOA_SINGLE_BLOB && d.aligned) {
+    uint64_t end = 0;
+    for (int k = 0; k < d.K(); ++k) {
+      if (d.base[k] > end) {
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(jb.db[0]) + end, st->zero, d.base[k] - end, cudaMemcpyDefault,
+                            st->d2h);
+        if (e != cudaSuccess) return cuda_err(e, "gap fill");
+      }
+      end = d.base[k] + d.N * d.sizes[k];
+    }
+  }
+  std::vector<uint64_t> lbs, lbd;
+  std::vector<Range> rs, rd;
+  for (uint64_t a = 0; a < N; a += n, ++*c) {
+    const uint64_t b = std::min(N, a + n);
+    const int j = (int)(*c % kNB);
+    llama_mapping* ls = st->view(jb.sm, b - a);
+    llama_mapping* ld = st->view(jb.dm, b - a);
+    if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
+    layout_local(ls->m, &lbs);
+    layout_local(ld->m, &lbd);
+    slab_ranges(s, ls->m, a, b, &rs);
+    slab_ranges(d, ld->m, a, b, &rd);
+    // h2d: buffer j is free once the slab that used it has gone back out
+    if (*c >= (uint64_t)kNB && (e = cudaStreamWaitEvent(st->h2d, st->e_out[j], 0)) != cudaSuccess)
+      return cuda_err(e, "h2d wait");
+    for (const Range& r : rs) {
+      e = cudaMemcpyAsync(st->buf[j][0] + lbs[r.lblob] + r.loff, static_cast<const uint8_t*>(jb.sb[r.gblob]) + r.goff,
+                          r.len, cudaMemcpyDefault, st->h2d);
+      if (e != cudaSuccess) return cuda_err(e, "h2d copy");
+    }
+    if ((e = cudaEventRecord(st->e_in[j], st->h2d)) != cudaSuccess) return cuda_err(e, "h2d event");
+    // relayout of the slab's 1-D views in staging memory
+    if ((e = cudaStreamWaitEvent(st->comp, st->e_in[j], 0)) != cudaSuccess) return cuda_err(e, "comp wait");
+    std::vector<void*> ps(ls->m.nblobs()), pd(ld->m.nblobs());
+    for (int q = 0; q < ls->m.nblobs(); ++q) ps[q] = st->buf[j][0] + lbs[q];
+    for (int q = 0; q < ld->m.nblobs(); ++q) pd[q] = st->buf[j][1] + lbd[q];
+    llama_status cs = llama_copy(ls, ps.data(), ld, pd.data(), st->comp);
+    if (cs != LLAMA_OK) return cs;
+    if ((e = cudaEventRecord(st->e_comp[j], st->comp)) != cudaSuccess) return cuda_err(e, "comp event");
+    // d2h
+    if ((e = cudaStreamWaitEvent(st->d2h, st->e_comp[j], 0)) != cudaSuccess) return cuda_err(e, "d2h wait");
+    for (const Range& r : rd) {
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(jb.db[r.gblob]) + r.goff, st->buf[j][1] + lbd[r.lblob] + r.loff, r.len,
+                          cudaMemcpyDefault, st->d2h);
+      if (e != cudaSuccess) return cuda_err(e, "d2h copy");
+    }
+    if ((e = cudaEventRecord(st->e_out[j], st->d2h)) != cudaSuccess) return cuda_err(e, "d2h event");
+  }
+  return LLAMA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llama_mapping* const* src_maps,
+                                     void* const* const* src_blobs, const llama_mapping* const* dst_maps,
+                                     void* const* const* dst_blobs, void* stream) {
+  if (!st || count < 0 || (count > 0 && (!src_maps || !src_blobs || !dst_maps || !dst_blobs)))
     return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
   try {
-    const llb::Mapping& s = src_map->m;
-    const llb::Mapping& d = dst_map->m;
-    if (s.types != d.types) return llb::set_error(LLAMA_ERR_RECORD_MISMATCH, "record dimensions differ");
-    if (s.extents != d.extents) return llb::set_error(LLAMA_ERR_SHAPE_MISMATCH, "array extents differ");
-    for (int b = 0; b < s.nblobs(); ++b)
-      if (s.blob_sizes[b] && !src_blobs[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL src blob");
-    for (int b = 0; b < d.nblobs(); ++b)
-      if (d.blob_sizes[b] && !dst_blobs[b]) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL dst blob");
-    const uint64_t N = s.N;
-    if (d.collides())
-      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "destination maps several records onto one location");
-    if (s.trace || d.trace)
-      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a traced view (use llama_copy)");
-    if (s.lin != d.lin)  // equal storage orders: slabs of storage positions correspond
-      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy between differently linearised views");
-    if (!s.uniform || !d.uniform || s.kind == LLAMA_ONE || d.kind == LLAMA_ONE)
-      return llb::set_error(LLAMA_ERR_UNSUPPORTED, "staged copy of a split / one mapping (copy its blobs, then llama_copy)");
-    if (d.footprint_bytes() == 0) return LLAMA_OK;
-
-    // slab unit: whole blocks of every blocked side (lcm of the lane counts)
-    uint64_t unit = 1;
-    for (const llb::Mapping* m : {&s, &d})
-      if (!m->soa()) unit = unit / gcd64(unit, m->L) * m->L;
-    // slab size from the per-record footprint, then shrunk until both 1-D
-    // views fit one staging buffer
-    const uint64_t per = std::max<uint64_t>(1, std::max(s.footprint_bytes(), d.footprint_bytes()) / std::max<uint64_t>(N, 1));
-    uint64_t n = std::max<uint64_t>(unit, st->cap / per / unit * unit);
-    if (n > N) n = (N + unit - 1) / unit * unit;
-    std::vector<uint64_t> lbs, lbd;
-    for (;;) {
-      const uint64_t nn = std::min(n, N);
-      llama_mapping* ls = st->view(src_map, nn);
-      llama_mapping* ld = st->view(dst_map, nn);
-      if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
-      if (layout_local(ls->m, &lbs) <= st->cap && layout_local(ld->m, &lbd) <= st->cap) break;
-      if (n <= unit) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "one slab of whole AoSoA blocks exceeds the staging buffer");
-      n = std::max(unit, (n / 2) / unit * unit);
+    std::vector<StagedJob> jobs(count);
+    for (int i = 0; i < count; ++i) {  // every copy is validated before anything is enqueued
+      jobs[i] = StagedJob{src_maps[i], src_blobs[i], dst_maps[i], dst_blobs[i], 0};
+      llama_status s = prepare_job(st, &jobs[i]);
+      if (s != LLAMA_OK) return s;
     }
-
     cudaError_t e = cudaEventRecord(st->e_start, (cudaStream_t)stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->h2d, st->e_start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->comp, st->e_start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->d2h, st->e_start, 0);
     if (e != cudaSuccess) return cuda_err(e, "stream ordering");
-
-    // destination padding outside every slab range: gaps between aligned
-    // SoA single-blob sub-arrays (reading #9) -> zero them from the device
-    if (d.kind == LLAMA_SOA_SINGLE_BLOB && d.aligned) {
-      uint64_t end = 0;
-      for (int k = 0; k < d.K(); ++k) {
-        if (d.base[k] > end) {
-          e = cudaMemcpyAsync(static_cast<uint8_t*>(dst_blobs[0]) + end, st->zero, d.base[k] - end,
-                              cudaMemcpyDefault, st->d2h);
-          if (e != cudaSuccess) return cuda_err(e, "gap fill");
-        }
-        end = d.base[k] + d.N * d.sizes[k];
-      }
-    }
-
-    std::vector<Range> rs, rd;
     uint64_t c = 0;
-    for (uint64_t a = 0; a < N; a += n, ++c) {
-      const uint64_t b = std::min(N, a + n);
-      const int j = (int)(c % kNB);
-      llama_mapping* ls = st->view(src_map, b - a);
-      llama_mapping* ld = st->view(dst_map, b - a);
-      if (!ls || !ld) return llb::set_error(LLAMA_ERR_UNSUPPORTED, "cannot build slab views");
-      layout_local(ls->m, &lbs);
-      layout_local(ld->m, &lbd);
-      slab_ranges(s, ls->m, a, b, &rs);
-      slab_ranges(d, ld->m, a, b, &rd);
-      // h2d: buffer j is free once the slab that used it has gone back out
-      if (c >= (uint64_t)kNB && (e = cudaStreamWaitEvent(st->h2d, st->e_out[j], 0)) != cudaSuccess)
-        return cuda_err(e, "h2d wait");
-      for (const Range& r : rs) {
-        e = cudaMemcpyAsync(st->buf[j][0] + lbs[r.lblob] + r.loff,
-                            static_cast<const uint8_t*>(src_blobs[r.gblob]) + r.goff, r.len, cudaMemcpyDefault,
-                            st->h2d);
-        if (e != cudaSuccess) return cuda_err(e, "h2d copy");
-      }
-      if ((e = cudaEventRecord(st->e_in[j], st->h2d)) != cudaSuccess) return cuda_err(e, "h2d event");
-      // relayout of the slab's 1-D views in staging memory
-      if ((e = cudaStreamWaitEvent(st->comp, st->e_in[j], 0)) != cudaSuccess) return cuda_err(e, "comp wait");
-      std::vector<void*> ps(ls->m.nblobs()), pd(ld->m.nblobs());
-      for (int q = 0; q < ls->m.nblobs(); ++q) ps[q] = st->buf[j][0] + lbs[q];
-      for (int q = 0; q < ld->m.nblobs(); ++q) pd[q] = st->buf[j][1] + lbd[q];
-      llama_status cs = llama_copy(ls, ps.data(), ld, pd.data(), st->comp);
-      if (cs != LLAMA_OK) return cs;
-      if ((e = cudaEventRecord(st->e_comp[j], st->comp)) != cudaSuccess) return cuda_err(e, "comp event");
-      // d2h
-      if ((e = cudaStreamWaitEvent(st->d2h, st->e_comp[j], 0)) != cudaSuccess) return cuda_err(e, "d2h wait");
-      for (const Range& r : rd) {
-        e = cudaMemcpyAsync(static_cast<uint8_t*>(dst_blobs[r.gblob]) + r.goff, st->buf[j][1] + lbd[r.lblob] + r.loff,
-                            r.len, cudaMemcpyDefault, st->d2h);
-        if (e != cudaSuccess) return cuda_err(e, "d2h copy");
-      }
-      if ((e = cudaEventRecord(st->e_out[j], st->d2h)) != cudaSuccess) return cuda_err(e, "d2h event");
+    for (const StagedJob& jb : jobs) {
+      llama_status s = enqueue_job(st, jb, &c);
+      if (s != LLAMA_OK) return s;
     }
     if ((e = cudaEventRecord(st->e_done, st->d2h)) != cudaSuccess) return cuda_err(e, "done event");
     if ((e = cudaStreamWaitEvent((cudaStream_t)stream, st->e_done, 0)) != cudaSuccess) return cuda_err(e, "join");
@@ -260,6 +301,11 @@ llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, v
   } catch (...) {
     return llb::set_error(LLAMA_ERR_OOM, "staged copy failed");
   }
+}
+
+llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
+                               const llama_mapping* dst_map, void* const* dst_blobs, void* stream) {
+  return llama_copy_staged_batch(st, 1, &src_map, &src_blobs, &dst_map, &dst_blobs, stream);
 }
 
 }  // extern "C"

@@ -287,6 +287,30 @@ def test_staged_copy_host_buffers(llama, oracle_mod, cap):
             assert np.array_equal(x.numpy(), exp[j])
 
 
+@pytest.mark.parametrize("cap", [4096, 1 << 16, 0])
+def test_staged_copy_batch(llama, oracle_mod, cap):
+    """llama_copy_staged_batch: the same cases as one pipeline (the buffers
+    rotate from one copy into the next), every destination byte checked."""
+    st = llama.Stager(cap)
+    cases = [(W.PARTICLE7, 5000, "aos", "soa_mb"), (W.LISTING1, 3001, "aosoa32", "soa_sb"),
+             (W.LISTING1, 999, "aos", "soa_sb_aligned"), (W.HEP100, 333, "aos", "aos_aligned"),
+             (W.PARTICLE7, 0, "aos", "soa_mb"), (W.PARTICLE7, 4097, "aosoa8", "aosoa32")]
+    batch, expect = [], []
+    for schema, n, a, b in cases:
+        sm, dm = llama.Mapping(schema, [n], *KINDS[a]), llama.Mapping(schema, [n], *KINDS[b])
+        so, do = oracle_mod.Mapping(schema, [n], *KINDS[a]), oracle_mod.Mapping(schema, [n], *KINDS[b])
+        src_host = oracle_mod.make_view(so, 9, pad_fill=0xCD)
+        hs = [torch.from_numpy(x).pin_memory() for x in src_host]
+        hd = [torch.full((max(x, 1),), 0x5A, dtype=torch.uint8).pin_memory() for x in dm.blob_sizes()]
+        batch.append((sm, hs, dm, hd))
+        expect.append(oracle_mod.copy(so, src_host, do))
+    llama.copy_staged_batch(st, batch)
+    torch.cuda.synchronize()
+    for (sm, hs, dm, hd), exp, case in zip(batch, expect, cases):
+        for j, x in enumerate(hd):
+            assert np.array_equal(x.numpy()[:dm.blob_sizes()[j]], exp[j][:dm.blob_sizes()[j]]), (case, j, cap)
+
+
 # ------------------------------------------------------------ One / Split (f1)
 def run_spec_case(llama, oracle, schema, ext, s_spec, d_spec, seed=7, pad=0xCD):
     """run_case for workloads spec trees (MAPPINGS tuples or split trees)."""
