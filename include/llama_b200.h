@@ -312,6 +312,14 @@ llama_status llama_nbody_move_ex(const llama_mapping* m, void* const* blobs, con
                                  const int32_t* vel_leaves, float dt, llama_move_path path,
                                  llama_move_path* path_used, void* stream);
 
+/* The n-body move on a view whose blobs may live in host memory (pinned for
+ * full PCIe speed): slabs are DMA'd into staging memory, moved in place there
+ * (llama_nbody_move on the slab's 1-D view) and DMA'd back, the three steps of
+ * consecutive slabs overlapped (the f2 pipeline applied to f3).  Errors as
+ * llama_nbody_move and llama_copy_staged. */
+llama_status llama_nbody_move_staged(llama_stager* st, const llama_mapping* m, void* const* blobs,
+                                     const int32_t* pos_leaves, const int32_t* vel_leaves, float dt, void* stream);
+
 /* Number of kernels this library has launched in this process (monotonic). */
 uint64_t llama_launch_count(void);
 

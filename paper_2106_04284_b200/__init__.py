@@ -38,7 +38,8 @@ EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_ma
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
            "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
            "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
-           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_copy_staged_batch", "llama_nbody_move",
+           "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_copy_staged_batch",
+           "llama_nbody_move_staged", "llama_nbody_move",
            "llama_nbody_move_ex"]
 MOVE_PATHS = {"auto": 0, "generic": 1, "runs": 2, "aos": 3}
 MOVE_PATH_NAMES = {v: k for k, v in MOVE_PATHS.items()}
@@ -103,6 +104,8 @@ def _load():
     lib.llama_stager_destroy.argtypes = [ctypes.c_void_p]
     lib.llama_stager_destroy.restype = None
     lib.llama_copy_staged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
+    lib.llama_nbody_move_staged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, vpp, P(ctypes.c_int32),
+                                            P(ctypes.c_int32), ctypes.c_float, ctypes.c_void_p]
     lib.llama_copy_staged_batch.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_void_p), P(vpp),
                                             P(ctypes.c_void_p), P(vpp), ctypes.c_void_p]
     lib.llama_launch_count.restype = ctypes.c_uint64
@@ -401,3 +404,12 @@ def nbody_move(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), path="auto", stream=N
     _check(_lib.llama_nbody_move_ex(m.handle, ptrs, p3, v3, ctypes.c_float(dt), MOVE_PATHS[path],
                                     ctypes.byref(used), _stream(stream)))
     return MOVE_PATH_NAMES[used.value]
+
+
+def nbody_move_staged(stager, m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), stream=None):
+    """n-body move of a view in host (pinned) or device memory through the
+    stager's slab pipeline (llama_nbody_move_staged)."""
+    ptrs = _ptrs(blobs, m.blob_sizes(), "blobs", device_only=False)
+    p3 = (ctypes.c_int32 * 3)(*pos)
+    v3 = (ctypes.c_int32 * 3)(*vel)
+    _check(_lib.llama_nbody_move_staged(stager.handle, m.handle, ptrs, p3, v3, ctypes.c_float(dt), _stream(stream)))

@@ -162,6 +162,10 @@ struct StagedJob {
   const llama_mapping* dm;
   void* const* db;
   uint64_t n = 0;  // records per slab
+  // n-body move instead of a copy (sm == dm, sb == db): in place per slab
+  bool move = false;
+  int32_t pos[3] = {0, 0, 0}, vel[3] = {0, 0, 0};
+  float dt = 0.f;
 };
 
 llama_status prepare_job(llama_stager* st, StagedJob* jb) {
@@ -253,15 +257,16 @@ llama_status enqueue_job(llama_stager* st, const StagedJob& jb, uint64_t* c) {
     if ((e = cudaStreamWaitEvent(st->comp, st->e_in[j], 0)) != cudaSuccess) return cuda_err(e, "comp wait");
     std::vector<void*> ps(ls->m.nblobs()), pd(ld->m.nblobs());
     for (int q = 0; q < ls->m.nblobs(); ++q) ps[q] = st->buf[j][0] + lbs[q];
-    for (int q = 0; q < ld->m.nblobs(); ++q) pd[q] = st->buf[j][1] + lbd[q];
-    llama_status cs = llama_copy(ls, ps.data(), ld, pd.data(), st->comp);
+    for (int q = 0; q < ld->m.nblobs(); ++q) pd[q] = st->buf[j][jb.move ? 0 : 1] + lbd[q];
+    llama_status cs = jb.move ? llama_nbody_move(ls, ps.data(), jb.pos, jb.vel, jb.dt, st->comp)
+                              : llama_copy(ls, ps.data(), ld, pd.data(), st->comp);
     if (cs != LLAMA_OK) return cs;
     if ((e = cudaEventRecord(st->e_comp[j], st->comp)) != cudaSuccess) return cuda_err(e, "comp event");
     // d2h
     if ((e = cudaStreamWaitEvent(st->d2h, st->e_comp[j], 0)) != cudaSuccess) return cuda_err(e, "d2h wait");
     for (const Range& r : rd) {
-      e = cudaMemcpyAsync(static_cast<uint8_t*>(jb.db[r.gblob]) + r.goff, st->buf[j][1] + lbd[r.lblob] + r.loff, r.len,
-                          cudaMemcpyDefault, st->d2h);
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(jb.db[r.gblob]) + r.goff,
+                          st->buf[j][jb.move ? 0 : 1] + lbd[r.lblob] + r.loff, r.len, cudaMemcpyDefault, st->d2h);
       if (e != cudaSuccess) return cuda_err(e, "d2h copy");
     }
     if ((e = cudaEventRecord(st->e_out[j], st->d2h)) != cudaSuccess) return cuda_err(e, "d2h event");
@@ -306,6 +311,38 @@ llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llam
 llama_status llama_copy_staged(llama_stager* st, const llama_mapping* src_map, void* const* src_blobs,
                                const llama_mapping* dst_map, void* const* dst_blobs, void* stream) {
   return llama_copy_staged_batch(st, 1, &src_map, &src_blobs, &dst_map, &dst_blobs, stream);
+}
+
+llama_status llama_nbody_move_staged(llama_stager* st, const llama_mapping* m, void* const* blobs,
+                                     const int32_t* pos_leaves, const int32_t* vel_leaves, float dt, void* stream) {
+  if (!st || !m || !blobs || !pos_leaves || !vel_leaves) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    for (int c = 0; c < 3; ++c)
+      for (int32_t k : {pos_leaves[c], vel_leaves[c]})
+        if (k < 0 || k >= m->m.K() || m->m.sizes[k] != 4)
+          return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "Pos / Vel leaves must be 4-byte leaf indices");
+    StagedJob jb{m, blobs, m, blobs, 0};
+    jb.move = true;
+    for (int c = 0; c < 3; ++c) {
+      jb.pos[c] = pos_leaves[c];
+      jb.vel[c] = vel_leaves[c];
+    }
+    jb.dt = dt;
+    llama_status s = prepare_job(st, &jb);
+    if (s != LLAMA_OK) return s;
+    cudaError_t e = cudaEventRecord(st->e_start, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->h2d, st->e_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->comp, st->e_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st->d2h, st->e_start, 0);
+    if (e != cudaSuccess) return cuda_err(e, "stream ordering");
+    uint64_t c = 0;
+    if ((s = enqueue_job(st, jb, &c)) != LLAMA_OK) return s;
+    if ((e = cudaEventRecord(st->e_done, st->d2h)) != cudaSuccess) return cuda_err(e, "done event");
+    if ((e = cudaStreamWaitEvent((cudaStream_t)stream, st->e_done, 0)) != cudaSuccess) return cuda_err(e, "join");
+    return LLAMA_OK;
+  } catch (...) {
+    return llb::set_error(LLAMA_ERR_OOM, "staged move failed");
+  }
 }
 
 }  // extern "C"

@@ -157,3 +157,21 @@ def test_move_aos_lsu_variant(llama, oracle_mod, n, monkeypatch):
     assert llama.nbody_move(dm, db, DT, path="aos") == "aos"
     torch.cuda.synchronize()
     assert np.array_equal(db[0].cpu().numpy(), exp[0])
+
+
+@pytest.mark.parametrize("cap", [4096, 1 << 20])
+@pytest.mark.parametrize("name", ["aos", "soa_mb", "aosoa8"])
+def test_move_staged_host(llama, oracle_mod, name, cap):
+    """llama_nbody_move_staged on pinned host blobs: many slabs, a partial last one."""
+    n = 10_007
+    vals = W.particle_values(n, seed=12)
+    om = oracle_mod.mapping_from_spec(W.PARTICLE7, [n], _spec(name))
+    ob = oracle_mod.copy(oracle_mod.Mapping(W.PARTICLE7, [n], "aos"),
+                         [np.frombuffer(vals.tobytes(), np.uint8).copy()], om)
+    host = [torch.from_numpy(b.copy()).pin_memory() for b in ob]
+    exp = oracle_mod.nbody_move(om, ob, DT)
+    dm = llama.Mapping.from_spec(W.PARTICLE7, [n], _spec(name))
+    llama.nbody_move_staged(llama.Stager(cap), dm, host, DT)
+    torch.cuda.synchronize()
+    for j, h in enumerate(host):
+        assert np.array_equal(h.numpy(), exp[j]), (name, cap, j)
