@@ -6,6 +6,7 @@ Each case generates the source on the GPU (llama_generate) and on the CPU
 the GPU into destination blobs pre-filled with garbage (so an unwritten byte
 cannot pass), and compares every byte of every destination blob with the
 oracle's copy.  Source padding is poisoned with 0xCD (reading #13)."""
+import os
 import random
 
 import numpy as np
@@ -404,3 +405,21 @@ def test_direct_chosen_for_hep(llama):
     assert llama.plan(m["soa_mb"], m["aos_aligned"])["direct"]
     assert not llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: misaligned leaves
     assert not llama.plan(m["aos"], m["aos_aligned"])["direct"]
+
+
+def test_c5_symmetric_memory_path_one_rank(llama):
+    """bench.py --config C5 (cross-device relayout through peer pointers from
+    torch symmetric memory) under torchrun with one rank: the peer is this
+    GPU; every rank's received destination is checked against the oracle."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+                        "--gpus", "1", "--config", "C5", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["parity_sampled"] is True
+    assert line["value"] > 0
