@@ -297,6 +297,8 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
           llb::DirectParams q = *plan->direct;
           for (int b = 0; b < s.nblobs(); ++b) q.blobs[0][b] = static_cast<uint8_t*>(const_cast<void*>(src_blobs[b]));
           for (int b = 0; b < d.nblobs(); ++b) q.blobs[1][b] = static_cast<uint8_t*>(dst_blobs[b]);
+          for (uint32_t k = 0; k < q.K; ++k)  // the SoA side's element pointers
+            q.leaf[k].gptr = q.blobs[q.a2s ? 1 : 0][q.leaf[k].blob] + q.leaf[k].gbase;
           e = llb::launch_permute_direct(q, stream);
           break;
         }

@@ -120,6 +120,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// The same, but the waiting thread may be suspended (up to `hint_ns` per try)
+// instead of spinning: for a producer lane whose spin would take issue slots
+// from the consumer warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 20000) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LLB_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra LLB_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+}
+
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
 // Requires 16-B aligned addresses and a 16-B multiple size.
 __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {

@@ -90,6 +90,88 @@ __device__ __forceinline__ void gl_store(uint8_t* p, uint64_t v, uint32_t s, uin
 
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory"); }
 
+template <uint32_t SZ> struct UT;
+template <> struct UT<1> { typedef uint8_t T; };
+template <> struct UT<2> { typedef uint16_t T; };
+template <> struct UT<4> { typedef uint32_t T; };
+template <> struct UT<8> { typedef unsigned long long T; };
+
+// One class of leaves (equal size, alignment classes) for the tile's records
+// lane and lane + 32: warps take the class's leaves in turn, kU at a time, so
+// each lane has 2 * kU independent accesses in flight.
+template <bool kA2S, uint32_t SZ, bool kImgA, bool kGlobA>
+__device__ __forceinline__ void direct_class(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                             uint64_t t0, uint32_t nrec, int warp, int lane) {
+  typedef typename UT<SZ>::T U;
+  constexpr int kU = kA2S ? 4 : (SZ == 8 ? 4 : 8);
+  const bool ok0r = (uint32_t)lane < nrec, ok1r = (uint32_t)lane + 32 < nrec;
+  const uint32_t r0 = (uint32_t)lane * p.S, r1 = ((uint32_t)lane + 32) * p.S;
+  for (uint32_t i0 = c.k0 + warp; i0 < c.k1; i0 += kU * (kCons / 32)) {
+    U v[kU][2];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * (kCons / 32);
+      const bool has = i < c.k1;
+      const DirectLeaf& l = p.leaf[p.order[has ? i : c.k0]];
+      const bool ok0 = has && ok0r, ok1 = has && ok1r;
+      if (kA2S) {
+        if (kImgA) {
+          v[u][0] = ok0 ? *reinterpret_cast<const U*>(img + r0 + l.F) : U(0);
+          v[u][1] = ok1 ? *reinterpret_cast<const U*>(img + r1 + l.F) : U(0);
+        } else {
+          v[u][0] = ok0 ? (U)sm_gather(img + r0 + l.F, SZ, l.a_img) : U(0);
+          v[u][1] = ok1 ? (U)sm_gather(img + r1 + l.F, SZ, l.a_img) : U(0);
+        }
+      } else {
+        const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
+        if (kGlobA) {
+          v[u][0] = ok0 ? __ldcs(g + lane) : U(0);
+          v[u][1] = ok1 ? __ldcs(g + lane + 32) : U(0);
+        } else {
+          v[u][0] = ok0 ? (U)gl_load(reinterpret_cast<const uint8_t*>(g + lane), SZ, 1) : U(0);
+          v[u][1] = ok1 ? (U)gl_load(reinterpret_cast<const uint8_t*>(g + lane + 32), SZ, 1) : U(0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * (kCons / 32);
+      const bool has = i < c.k1;
+      const DirectLeaf& l = p.leaf[p.order[has ? i : c.k0]];
+      const bool ok0 = has && ok0r, ok1 = has && ok1r;
+      if (kA2S) {
+        U* g = reinterpret_cast<U*>(l.gptr) + t0;
+        if (kGlobA) {
+          if (ok0) __stcs(g + lane, v[u][0]);
+          if (ok1) __stcs(g + lane + 32, v[u][1]);
+        } else {
+          if (ok0) gl_store(reinterpret_cast<uint8_t*>(g + lane), v[u][0], SZ, 1);
+          if (ok1) gl_store(reinterpret_cast<uint8_t*>(g + lane + 32), v[u][1], SZ, 1);
+        }
+      } else {
+        if (kImgA) {
+          if (ok0) *reinterpret_cast<U*>(img + r0 + l.F) = v[u][0];
+          if (ok1) *reinterpret_cast<U*>(img + r1 + l.F) = v[u][1];
+        } else {
+          if (ok0) sm_scatter(img + r0 + l.F, v[u][0], SZ, l.a_img);
+          if (ok1) sm_scatter(img + r1 + l.F, v[u][1], SZ, l.a_img);
+        }
+      }
+    }
+  }
+}
+
+template <bool kA2S, uint32_t SZ>
+__device__ __forceinline__ void direct_class_a(const DirectParams& p, const DirectClass& c, uint8_t* img, uint64_t t0,
+                                               uint32_t nrec, int warp, int lane) {
+  switch (c.kind & 48) {
+    case 48: direct_class<kA2S, SZ, true, true>(p, c, img, t0, nrec, warp, lane); break;
+    case 16: direct_class<kA2S, SZ, true, false>(p, c, img, t0, nrec, warp, lane); break;
+    case 32: direct_class<kA2S, SZ, false, true>(p, c, img, t0, nrec, warp, lane); break;
+    default: direct_class<kA2S, SZ, false, false>(p, c, img, t0, nrec, warp, lane); break;
+  }
+}
+
 template <bool kA2S>
 __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_constant__ DirectParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -135,7 +217,7 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
         for (uint32_t i = 0; i < p.ns && i < n_my; ++i) load(i, i);
         uint32_t s = 0, ph = 0;
         for (uint32_t i = 0; i + p.ns < n_my; ++i) {
-          mbar_wait(&freed[s], ph);
+          mbar_wait_sleep(&freed[s], ph);
           load(i + p.ns, s);
           if (++s == p.ns) { s = 0; ph ^= 1; }
         }
@@ -144,7 +226,7 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
         for (uint32_t i = 0; i < n_my; ++i) {
           const uint64_t t0 = (first + (uint64_t)i * stride) * p.T;
           const uint32_t body = (tile_rec(i) * p.S) & ~15u;
-          mbar_wait(&ready[s], ph);
+          mbar_wait_sleep(&ready[s], ph);
           if (body) bulk_s2g(ag + t0 * p.S, ring + (size_t)s * p.stage, body);
           bulk_commit();
           bulk_wait_read<0>();
@@ -169,39 +251,15 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
       for (uint32_t o = body + tid; o < bytes; o += kCons) img[o] = ag[t0 * p.S + o];
       cons_sync();
     }
-    // warp w takes leaves w, w+8, ...; kU leaves at a time, so each lane has
-    // 2*kU independent accesses in flight (records lane and lane+32; T = 64)
-    constexpr int kU = kA2S ? 4 : 8;  // SoA -> AoS: more global loads in flight
-    const bool ok0 = lane < nrec, ok1 = lane + 32 < nrec;
-    for (uint32_t k0 = warp; k0 < p.K; k0 += kU * (kCons / 32)) {
-      uint64_t v[kU][2];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint32_t k = k0 + u * (kCons / 32);
-        if (k >= p.K) break;
-        const DirectLeaf& l = p.leaf[k];
-        if (kA2S) {
-          v[u][0] = ok0 ? sm_gather(img + lane * p.S + l.F, l.size, l.a_img) : 0;
-          v[u][1] = ok1 ? sm_gather(img + (lane + 32) * p.S + l.F, l.size, l.a_img) : 0;
-        } else {
-          const uint8_t* g = p.blobs[0][l.blob] + l.gbase + t0 * l.size;
-          v[u][0] = ok0 ? gl_load(g + (uint64_t)lane * l.size, l.size, l.a_glob) : 0;
-          v[u][1] = ok1 ? gl_load(g + (uint64_t)(lane + 32) * l.size, l.size, l.a_glob) : 0;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint32_t k = k0 + u * (kCons / 32);
-        if (k >= p.K) break;
-        const DirectLeaf& l = p.leaf[k];
-        if (kA2S) {
-          uint8_t* g = p.blobs[1][l.blob] + l.gbase + t0 * l.size;
-          if (ok0) gl_store(g + (uint64_t)lane * l.size, v[u][0], l.size, l.a_glob);
-          if (ok1) gl_store(g + (uint64_t)(lane + 32) * l.size, v[u][1], l.size, l.a_glob);
-        } else {
-          if (ok0) sm_scatter(img + lane * p.S + l.F, v[u][0], l.size, l.a_img);
-          if (ok1) sm_scatter(img + (lane + 32) * p.S + l.F, v[u][1], l.size, l.a_img);
-        }
+    // classes of equal-size leaves, each a specialised loop (warp w takes a
+    // class's leaves w, w+8, ...; records lane and lane + 32; T = 64)
+    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
+      const DirectClass c = p.cls[ci];
+      switch (c.kind & 15) {
+        case 8: direct_class_a<kA2S, 8>(p, c, img, t0, nrec, warp, lane); break;
+        case 4: direct_class_a<kA2S, 4>(p, c, img, t0, nrec, warp, lane); break;
+        case 2: direct_class_a<kA2S, 2>(p, c, img, t0, nrec, warp, lane); break;
+        default: direct_class_a<kA2S, 1>(p, c, img, t0, nrec, warp, lane); break;
       }
     }
     if (!kA2S) {

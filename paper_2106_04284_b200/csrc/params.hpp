@@ -257,12 +257,20 @@ struct MoveParams {
 // no per-leaf TMA segments of T * s_k bytes.
 struct DirectLeaf {
   uint64_t gbase;    // SoA side: byte offset of record 0's element in its blob
+  uint8_t* gptr;     // SoA side: blob + gbase (filled per launch)
   uint32_t F;        // AoS side: offset of the leaf inside a record
   uint32_t blob;     // SoA side blob
   uint16_t size;
   uint8_t a_img;     // alignment of every (r * S + F) in the AoS image (1, 2, 4, 8)
   uint8_t a_glob;    // alignment of every SoA element address
   uint32_t pad_;
+};
+
+// Leaves of equal size and alignment classes, handled by one specialised loop:
+// kind = size | 16 (image accesses aligned) | 32 (global accesses aligned).
+struct DirectClass {
+  uint16_t k0, k1;   // range in DirectParams::order
+  uint32_t kind;
 };
 
 struct DirectParams {
@@ -277,6 +285,9 @@ struct DirectParams {
   uint32_t gap_len[kMaxLeaves];
   uint64_t gap_off[kMaxLeaves];
   DirectLeaf leaf[kMaxLeaves];
+  uint32_t n_cls;
+  DirectClass cls[16];
+  uint16_t order[kMaxLeaves];  // leaf ids grouped by class
   uint8_t* blobs[2][kMaxBlobs];
 };
 static_assert(sizeof(DirectParams) <= 32764, "DirectParams exceeds the kernel parameter limit");

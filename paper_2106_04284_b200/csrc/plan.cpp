@@ -203,10 +203,11 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   const Mapping& So = a2s ? d : s;
   const uint64_t S = A.B;
   if (S == 0 || A.L != 1) { *why = "AoS stride"; return false; }
-  // measured: a win for naturally aligned AoS records (HEP aligned <-> SoA MB
-  // 2.4 -> 3.4 TB/s), a loss for packed ones whose misaligned leaves split
-  // into 1-4 byte pieces (2.8 -> 2.5 TB/s)
-  if (mode != 2)
+  // measured on HEP100: AoS -> SoA wins for packed and aligned records (2.8 ->
+  // 3.5 TB/s; misaligned leaves are funnel-shifted out of aligned words);
+  // SoA -> AoS only for naturally aligned records (misaligned leaves would be
+  // scattered into shared memory in 1-2 byte pieces: 2.9 -> 2.0 TB/s)
+  if (mode != 2 && s2a)
     for (int k = 0; k < A.K(); ++k)
       if (A.F[k] % A.sizes[k] || S % A.sizes[k]) { *why = "packed AoS: the tile permute"; return false; }
   // T = 64 records per tile (two per lane); ns = 2 stages, so several CTAs
@@ -238,6 +239,25 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
     l.size = (uint16_t)s.sizes[k];
     l.a_img = (uint8_t)std::min<uint64_t>(8, std::min(lb(S), lb(A.F[k])));
     l.a_glob = (uint8_t)std::min<uint64_t>(8, std::min<uint64_t>(lb(l.gbase), 16));
+  }
+  // leaf classes: (size, image aligned, global aligned), leaves grouped
+  {
+    std::vector<int> idx(s.K());
+    for (int k = 0; k < s.K(); ++k) idx[k] = k;
+    auto kind = [&](int k) {
+      const DirectLeaf& l = dp.leaf[k];
+      return (uint32_t)l.size | (l.a_img >= l.size ? 16u : 0u) | (l.a_glob >= l.size ? 32u : 0u);
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return kind(x) < kind(y); });
+    for (int i = 0; i < s.K(); ++i) {
+      dp.order[i] = (uint16_t)idx[i];
+      if (i == 0 || kind(idx[i]) != kind(idx[i - 1])) {
+        if (dp.n_cls >= 16) { *why = "too many leaf classes"; return false; }
+        dp.cls[dp.n_cls++] = DirectClass{(uint16_t)i, (uint16_t)(i + 1), kind(idx[i])};
+      } else {
+        dp.cls[dp.n_cls - 1].k1 = (uint16_t)(i + 1);
+      }
+    }
   }
   if (a2s && d.has_padding()) {  // aligned SoA SB: the gaps between sub-arrays
     if (d.kind != LLAMA_SOA_SINGLE_BLOB) { *why = "padded destination"; return false; }

@@ -403,7 +403,8 @@ def test_direct_chosen_for_hep(llama):
     m = {k: llama.Mapping(W.HEP100, [4096], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
     assert llama.plan(m["aos_aligned"], m["soa_mb"])["direct"]
     assert llama.plan(m["soa_mb"], m["aos_aligned"])["direct"]
-    assert not llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: misaligned leaves
+    assert llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: funnel-shifted gathers
+    assert not llama.plan(m["soa_mb"], m["aos"])["direct"]  # packed destination: the tile permute
     assert not llama.plan(m["aos"], m["aos_aligned"])["direct"]
 
 
