@@ -110,13 +110,13 @@ __global__ void __launch_bounds__(NC + 32, NC == 256 ? 3 : 1) k_permute_ws(const
       const bool fl = tile < n_full;
       auto refill = [&]() {  // refill the source stage tile i used
         if (i + p.ns < n_my) {
-          if (lane == 0) mbar_wait(&empty[s], sph);
+          if (lane == 0) mbar_wait_sleep(&empty[s], sph);
           __syncwarp();
           load(i + p.ns, s);
         }
       };
       if (p.order == 2) refill();
-      if (lane == 0) mbar_wait(&dfull[d], dph);
+      if (lane == 0) mbar_wait_sleep(&dfull[d], dph);
       __syncwarp();
       uint8_t* dimg = dbuf + (size_t)d * p.dst_stage;
       for (int j = lane; j < nds; j += 32) {
