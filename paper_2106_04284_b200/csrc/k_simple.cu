@@ -135,15 +135,59 @@ __device__ __forceinline__ uint64_t tile_leaf_offset(uint64_t f, uint64_t q, uin
   return l.base + q * l.B + l.F + r * l.size;
 }
 
-template <bool kAligned, bool kUniform>
+// Raw AoS side of a full tile: its 1024 records in the side's storage order
+// are 32 contiguous segments of 32 records (rows or columns) or, for Morton,
+// one segment of 1024; moved as 16-byte vectors between global memory and a
+// record-major shared buffer (record q of the storage order at q * S).
+__device__ __forceinline__ void raw_tile(uint8_t* g0, uint8_t* raw, const DevLin& lin, uint64_t y0, uint64_t x0,
+                                         uint32_t S, bool load) {
+  const uint32_t nseg = lin.kind == LLAMA_MORTON ? 1 : 32;
+  const uint32_t seg_vecs = (1024 / nseg) * S / 16;
+  for (uint32_t v = threadIdx.x; v < nseg * seg_vecs; v += kThreads) {
+    const uint32_t j = v / seg_vecs, o = v - j * seg_vecs;
+    const uint64_t y = y0 + (lin.kind == LLAMA_ROW_MAJOR ? j : 0), x = x0 + (lin.kind == LLAMA_COL_MAJOR ? j : 0);
+    uint4* g = reinterpret_cast<uint4*>(g0 + lin_storage2d(y, x, lin) * S) + o;
+    uint4* r = reinterpret_cast<uint4*>(raw) + v;
+    if (load)
+      *r = __ldcs(g);
+    else
+      __stcs(g, *r);
+  }
+}
+
+// kRaw: a raw AoS side exists (separate instantiation: the raw code costs
+// registers, and element-only tiles are latency-bound, so occupancy matters)
+template <bool kAligned, bool kUniform, bool kRaw>
 __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant__ NaiveParams p) {
   extern __shared__ __align__(16) uint8_t tsm[];
   const uint64_t tiles_x = (p.W + 31) / 32, n_tiles = tiles_x * ((p.H + 31) / 32);
+  uint8_t* raw = tsm + p.rawoff;
   for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const uint64_t y0 = (t / tiles_x) * 32, x0 = (t % tiles_x) * 32;
+    const bool full = y0 + 32 <= p.H && x0 + 32 <= p.W;
     uint64_t f[4], qb[4], rl[4];
     uint32_t e[4];
     bool ok[4];
+    if (kRaw && p.sraw && full) {  // coalesced vectors in, then records -> the leaf-major tile
+      raw_tile(const_cast<uint8_t*>(p.sb[p.sl[0].blob]) + p.sl[0].base, raw, p.slin, y0, x0, p.sS, true);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t q = threadIdx.x + kThreads * j;
+        uint32_t dy, dx;
+        tile_order(p.slin.kind, q, dy, dx);
+        e[j] = dy * 33 + dx;
+        f[j] = (uint64_t)q * p.sS;
+      }
+      for (int k = 0; k < p.K; ++k) {
+        const uint32_t size = p.sl[k].size, F = (uint32_t)p.sl[k].F;
+        uint8_t* tk = tsm + p.tbase[k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) move_elem<kAligned>(tk + e[j] * size, raw + f[j] + F, size);
+      }
+      __syncthreads();
+      goto store_phase;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t dy, dx;
@@ -164,6 +208,32 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
         if (ok[j]) move_elem<kAligned>(t + e[j] * l.size, sb + tile_leaf_offset<kUniform>(f[j], qb[j], rl[j], l), l.size);
     }
     __syncthreads();
+  store_phase:
+    if (kRaw && p.draw && full) {  // the leaf-major tile -> records, then coalesced vectors out
+      if (p.dpad) {  // destination padding goes out as 0 (reading #12)
+        for (uint32_t o = 16 * threadIdx.x; o < 1024 * p.dS; o += 16 * kThreads)
+          *reinterpret_cast<uint4*>(raw + o) = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t q = threadIdx.x + kThreads * j;
+        uint32_t dy, dx;
+        tile_order(p.dlin.kind, q, dy, dx);
+        e[j] = dy * 33 + dx;
+        f[j] = (uint64_t)q * p.dS;
+      }
+      for (int k = 0; k < p.K; ++k) {
+        const uint32_t size = p.dl[k].size, F = (uint32_t)p.dl[k].F;
+        const uint8_t* tk = tsm + p.tbase[k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) move_elem<kAligned>(raw + f[j] + F, tk + e[j] * size, size);
+      }
+      __syncthreads();
+      raw_tile(p.db[p.dl[0].blob] + p.dl[0].base, raw, p.dlin, y0, x0, p.dS, false);
+      __syncthreads();
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t dy, dx;
@@ -190,14 +260,16 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
 int launch_transpose2d(const NaiveParams& p, void* stream) {
   const uint64_t n_tiles = ((p.W + 31) / 32) * ((p.H + 31) / 32);
   if (n_tiles == 0) return 0;
-  static LaunchCache cache[4][64];
+  static LaunchCache cache[8][64];
   int dev = 0, per_sm = 1, sms = 148;
   cudaGetDevice(&dev);
-  void (*const kerns[4])(NaiveParams) = {k_transpose2d<false, false>, k_transpose2d<true, false>,
-                                         k_transpose2d<false, true>, k_transpose2d<true, true>};
-  auto kern = kerns[(p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0)];
-  int e = prepare_kernel(kern, kThreads, (int)p.tsmem, &cache[(p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0)][dev & 63],
-                         &per_sm);
+  void (*const kerns[8])(NaiveParams) = {
+      k_transpose2d<false, false, false>, k_transpose2d<true, false, false>, k_transpose2d<false, true, false>,
+      k_transpose2d<true, true, false>,   k_transpose2d<false, false, true>, k_transpose2d<true, false, true>,
+      k_transpose2d<false, true, true>,   k_transpose2d<true, true, true>};
+  const int v = (p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0) + ((p.sraw || p.draw) ? 4 : 0);
+  auto kern = kerns[v];
+  int e = prepare_kernel(kern, kThreads, (int)p.tsmem, &cache[v][dev & 63], &per_sm);
   if (e) return e;
   current_device_sms(&sms);
   uint64_t grid = (uint64_t)sms * per_sm;

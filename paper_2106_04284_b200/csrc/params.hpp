@@ -69,6 +69,10 @@ struct NaiveParams {
   uint32_t tbase[kMaxLeaves];  // TRANSPOSE: leaf k's 32x33-element tile at smem + tbase[k]
   uint32_t taligned;           // TRANSPOSE: every element of both sides naturally aligned
   uint32_t tuniform;           // TRANSPOSE: both sides share one L and B over all leaves
+  uint32_t sraw, draw;         // TRANSPOSE: that side is a plain AoS moved as raw 16-byte vectors
+  uint32_t rawoff;             // TRANSPOSE: shared-memory offset of the raw record buffer
+  uint32_t sS, dS;             // TRANSPOSE: record strides of the raw sides
+  uint32_t dpad;               // TRANSPOSE: the raw destination has padding bytes (zero the buffer)
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];

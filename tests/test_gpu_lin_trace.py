@@ -45,7 +45,7 @@ def _pair(llama, oracle, schema, ext, sspec, slin, dspec, dlin, seed=3, paths=("
 KINDS = [("aos", 1, False), ("soa_mb", 1, False), ("aosoa", 8, False), ("aos", 1, True)]
 
 
-@pytest.mark.parametrize("ext", [[64, 33], [5, 7, 3], [1, 1], [100, 37], [31, 1000]])
+@pytest.mark.parametrize("ext", [[64, 33], [5, 7, 3], [1, 1], [100, 37], [31, 1000], [64, 96], [96, 64]])
 @pytest.mark.parametrize("lins", [("row", "col"), ("col", "row"), ("col", "col")])
 def test_row_col_copies(llama, oracle_mod, ext, lins):
     for sk in KINDS:
@@ -122,3 +122,13 @@ def test_traced_move(llama, oracle_mod, name):
     assert dm.field_hits() == [int(x) for x in hits] == [n] * 6 + [0]
     for b in range(dm.blob_count):
         assert np.array_equal(dm.byte_hits(b), heat[b][:dm.blob_sizes()[b]])
+
+
+@pytest.mark.parametrize("lins", [("row", "col"), ("col", "morton"), ("morton", "row")])
+def test_raw_aos_tiles(llama, oracle_mod, lins):
+    """Full 32x32 tiles with plain AoS on both sides take the raw 16-byte
+    vector path (Particle7, packed and aligned Listing1 with padding)."""
+    for schema, ext in ((W.PARTICLE7, [64, 64]), (W.LISTING1, [64, 64])):
+        for sk, dk in (((("aos", 1, False)), ("aos", 1, True)), (("aos", 1, True), ("aos", 1, False)),
+                       (("aos", 1, False), ("aos", 1, False))):
+            _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "naive"))
