@@ -161,9 +161,60 @@ __device__ __forceinline__ void direct_class(const DirectParams& p, const Direct
   }
 }
 
+// The same for naturally aligned images whose record stride is an even
+// number of words (HEP aligned: 480 B = 120 words): 32 lanes on one leaf of 32
+// records would hit 4 banks (8-way conflicts), so a warp access covers 4
+// leaves x 8 consecutive records (lane = 8 * leaf + record): at most 2-way
+// conflicts, and each leaf still writes / reads a contiguous 8 * SZ-byte run.
+template <bool kA2S, uint32_t SZ, bool kGlobA>
+__device__ __forceinline__ void direct_class_mix(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                                 uint64_t t0, uint32_t nrec, int warp, int lane) {
+  typedef typename UT<SZ>::T U;
+  const uint32_t sub = (uint32_t)lane >> 3, rl = (uint32_t)lane & 7;
+  for (uint32_t g0 = c.k0 + 4 * warp; g0 < c.k1; g0 += 4 * (kCons / 32)) {
+    const uint32_t i = g0 + sub;
+    const bool has = i < c.k1;
+    const DirectLeaf& l = p.leaf[p.order[has ? i : c.k0]];
+    const uint32_t F = l.F;
+    U* g = reinterpret_cast<U*>(l.gptr) + t0;
+    U v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t r = 8 * q + rl;
+      const bool ok = has && r < nrec;
+      if (kA2S) {
+        v[q] = ok ? *reinterpret_cast<const U*>(img + r * p.S + F) : U(0);
+      } else if (kGlobA) {
+        v[q] = ok ? __ldcs(g + r) : U(0);
+      } else {
+        v[q] = ok ? (U)gl_load(reinterpret_cast<const uint8_t*>(g + r), SZ, 1) : U(0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t r = 8 * q + rl;
+      if (!(has && r < nrec)) continue;
+      if (!kA2S) {
+        *reinterpret_cast<U*>(img + r * p.S + F) = v[q];
+      } else if (kGlobA) {
+        __stcs(g + r, v[q]);
+      } else {
+        gl_store(reinterpret_cast<uint8_t*>(g + r), v[q], SZ, 1);
+      }
+    }
+  }
+}
+
 template <bool kA2S, uint32_t SZ>
 __device__ __forceinline__ void direct_class_a(const DirectParams& p, const DirectClass& c, uint8_t* img, uint64_t t0,
                                                uint32_t nrec, int warp, int lane) {
+  if (p.mix && (c.kind & 16)) {
+    if (c.kind & 32)
+      direct_class_mix<kA2S, SZ, true>(p, c, img, t0, nrec, warp, lane);
+    else
+      direct_class_mix<kA2S, SZ, false>(p, c, img, t0, nrec, warp, lane);
+    return;
+  }
   switch (c.kind & 48) {
     case 48: direct_class<kA2S, SZ, true, true>(p, c, img, t0, nrec, warp, lane); break;
     case 16: direct_class<kA2S, SZ, true, false>(p, c, img, t0, nrec, warp, lane); break;
