@@ -33,8 +33,10 @@ __device__ __forceinline__ uint64_t sm_gather(const uint8_t* p, uint32_t s, uint
     return (uint64_t)*reinterpret_cast<const uint32_t*>(p) | ((uint64_t)*reinterpret_cast<const uint32_t*>(p + 4) << 32);
   if (s == 1) return *p;
   // misaligned: the aligned 32-bit words covering the element, funnel-shifted
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)3);
-  const uint32_t sh = 8 * (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3);
+  // (pointer arithmetic on p keeps the shared address space: LDS, not LD)
+  const uint32_t lo2 = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(p - lo2);
+  const uint32_t sh = 8 * lo2;
   const uint32_t w0 = w[0], w1 = w[1];
   const uint32_t lo = __funnelshift_r(w0, w1, sh);
   if (s <= 4) return s == 4 ? lo : (s == 2 ? (lo & 0xFFFFu) : lo);
@@ -99,12 +101,12 @@ template <> struct UT<8> { typedef unsigned long long T; };
 // One class of leaves (equal size, alignment classes) for the tile's records
 // lane and lane + 32: warps take the class's leaves in turn, kU at a time, so
 // each lane has 2 * kU independent accesses in flight.
-template <bool kA2S, uint32_t SZ, bool kImgA, bool kGlobA>
+template <bool kA2S, uint32_t SZ, bool kImgA, bool kGlobA, bool kFull>
 __device__ __forceinline__ void direct_class(const DirectParams& p, const DirectClass& c, uint8_t* img,
                                              uint64_t t0, uint32_t nrec, int warp, int lane) {
   typedef typename UT<SZ>::T U;
   constexpr int kU = kA2S ? 4 : (SZ == 8 ? 4 : 8);
-  const bool ok0r = (uint32_t)lane < nrec, ok1r = (uint32_t)lane + 32 < nrec;
+  const bool ok0r = kFull || (uint32_t)lane < nrec, ok1r = kFull || (uint32_t)lane + 32 < nrec;
   const uint32_t r0 = (uint32_t)lane * p.S, r1 = ((uint32_t)lane + 32) * p.S;
   for (uint32_t i0 = c.k0 + warp; i0 < c.k1; i0 += kU * (kCons / 32)) {
     U v[kU][2];
@@ -166,7 +168,7 @@ __device__ __forceinline__ void direct_class(const DirectParams& p, const Direct
 // records would hit 4 banks (8-way conflicts), so a warp access covers 4
 // leaves x 8 consecutive records (lane = 8 * leaf + record): at most 2-way
 // conflicts, and each leaf still writes / reads a contiguous 8 * SZ-byte run.
-template <bool kA2S, uint32_t SZ, bool kGlobA>
+template <bool kA2S, uint32_t SZ, bool kGlobA, bool kFull>
 __device__ __forceinline__ void direct_class_mix(const DirectParams& p, const DirectClass& c, uint8_t* img,
                                                  uint64_t t0, uint32_t nrec, int warp, int lane) {
   typedef typename UT<SZ>::T U;
@@ -181,7 +183,7 @@ __device__ __forceinline__ void direct_class_mix(const DirectParams& p, const Di
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint32_t r = 8 * q + rl;
-      const bool ok = has && r < nrec;
+      const bool ok = has && (kFull || r < nrec);
       if (kA2S) {
         v[q] = ok ? *reinterpret_cast<const U*>(img + r * p.S + F) : U(0);
       } else if (kGlobA) {
@@ -193,7 +195,7 @@ __device__ __forceinline__ void direct_class_mix(const DirectParams& p, const Di
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint32_t r = 8 * q + rl;
-      if (!(has && r < nrec)) continue;
+      if (!(has && (kFull || r < nrec))) continue;
       if (!kA2S) {
         *reinterpret_cast<U*>(img + r * p.S + F) = v[q];
       } else if (kGlobA) {
@@ -205,21 +207,36 @@ __device__ __forceinline__ void direct_class_mix(const DirectParams& p, const Di
   }
 }
 
-template <bool kA2S, uint32_t SZ>
+template <bool kA2S, uint32_t SZ, bool kFull>
 __device__ __forceinline__ void direct_class_a(const DirectParams& p, const DirectClass& c, uint8_t* img, uint64_t t0,
                                                uint32_t nrec, int warp, int lane) {
   if (p.mix && (c.kind & 16)) {
     if (c.kind & 32)
-      direct_class_mix<kA2S, SZ, true>(p, c, img, t0, nrec, warp, lane);
+      direct_class_mix<kA2S, SZ, true, kFull>(p, c, img, t0, nrec, warp, lane);
     else
-      direct_class_mix<kA2S, SZ, false>(p, c, img, t0, nrec, warp, lane);
+      direct_class_mix<kA2S, SZ, false, kFull>(p, c, img, t0, nrec, warp, lane);
     return;
   }
   switch (c.kind & 48) {
-    case 48: direct_class<kA2S, SZ, true, true>(p, c, img, t0, nrec, warp, lane); break;
-    case 16: direct_class<kA2S, SZ, true, false>(p, c, img, t0, nrec, warp, lane); break;
-    case 32: direct_class<kA2S, SZ, false, true>(p, c, img, t0, nrec, warp, lane); break;
-    default: direct_class<kA2S, SZ, false, false>(p, c, img, t0, nrec, warp, lane); break;
+    case 48: direct_class<kA2S, SZ, true, true, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    case 16: direct_class<kA2S, SZ, true, false, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    case 32: direct_class<kA2S, SZ, false, true, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    default: direct_class<kA2S, SZ, false, false, kFull>(p, c, img, t0, nrec, warp, lane); break;
+  }
+}
+
+// full tiles (every record present) and the partial last tile
+template <bool kA2S, bool kFull>
+__device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img, uint64_t t0, uint32_t nrec, int warp,
+                                            int lane) {
+  for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
+    const DirectClass c = p.cls[ci];
+    switch (c.kind & 15) {
+      case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
+      case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
+      case 2: direct_class_a<kA2S, 2, kFull>(p, c, img, t0, nrec, warp, lane); break;
+      default: direct_class_a<kA2S, 1, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    }
   }
 }
 
@@ -304,15 +321,10 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
     }
     // classes of equal-size leaves, each a specialised loop (warp w takes a
     // class's leaves w, w+8, ...; records lane and lane + 32; T = 64)
-    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
-      const DirectClass c = p.cls[ci];
-      switch (c.kind & 15) {
-        case 8: direct_class_a<kA2S, 8>(p, c, img, t0, nrec, warp, lane); break;
-        case 4: direct_class_a<kA2S, 4>(p, c, img, t0, nrec, warp, lane); break;
-        case 2: direct_class_a<kA2S, 2>(p, c, img, t0, nrec, warp, lane); break;
-        default: direct_class_a<kA2S, 1>(p, c, img, t0, nrec, warp, lane); break;
-      }
-    }
+    if (nrec == p.T)
+      direct_tile<kA2S, true>(p, img, t0, nrec, warp, lane);
+    else
+      direct_tile<kA2S, false>(p, img, t0, nrec, warp, lane);
     if (!kA2S) {
       if (body < bytes) {  // the last tile's sub-16-byte tail goes out directly
         cons_sync();
