@@ -94,8 +94,8 @@ int launch_naive(const NaiveParams& p, void* stream) {
 // 2-d views of different linearisations (row / column-major / Morton, P:140-
 // 142): a CTA moves 32x32-record tiles, reading them in the source's storage
 // order (consecutive threads = consecutive source positions) into a
-// leaf-major shared tile (rows padded to 33 elements against bank
-// conflicts), then writing them in the destination's storage order.
+// leaf-major shared tile (32 x 32, XOR-swizzled against bank conflicts, see
+// tile_slot), then writing them in the destination's storage order.
 __device__ __forceinline__ void tile_order(uint32_t kind, uint32_t q, uint32_t& dy, uint32_t& dx) {
   if (kind == LLAMA_COL_MAJOR) {
     dy = q & 31;
@@ -107,6 +107,13 @@ __device__ __forceinline__ void tile_order(uint32_t kind, uint32_t q, uint32_t& 
     dy = q >> 5;
     dx = q & 31;
   }
+}
+
+// Slot of tile element (dy, dx): rows of 32 with an XOR swizzle chosen so that
+// 32 lanes walking a row, a column, or a 4 x 8 Morton block hit 32 distinct
+// banks (4-byte elements): bank = dx ^ f(dy), f(4a + b) = 8b + a.
+__device__ __forceinline__ uint32_t tile_slot(uint32_t dy, uint32_t dx) {
+  return dy * 32 + (dx ^ (((dy & 3) << 3) | (dy >> 2)));
 }
 
 // One element of `size` bytes; kAligned: every element of both sides is
@@ -143,10 +150,13 @@ __device__ __forceinline__ void raw_tile(uint8_t* g0, uint8_t* raw, const DevLin
                                          uint32_t S, bool load) {
   const uint32_t nseg = lin.kind == LLAMA_MORTON ? 1 : 32;
   const uint32_t seg_vecs = (1024 / nseg) * S / 16;
+  // segment j starts at the tile corner's position + j rows (row-major) or
+  // + j columns (column-major); one Morton segment
+  const uint64_t f0 = lin_storage2d(y0, x0, lin);
+  const uint64_t fstep = lin.kind == LLAMA_ROW_MAJOR ? lin.ext[1] : lin.ext[0];
   for (uint32_t v = threadIdx.x; v < nseg * seg_vecs; v += kThreads) {
     const uint32_t j = v / seg_vecs, o = v - j * seg_vecs;
-    const uint64_t y = y0 + (lin.kind == LLAMA_ROW_MAJOR ? j : 0), x = x0 + (lin.kind == LLAMA_COL_MAJOR ? j : 0);
-    uint4* g = reinterpret_cast<uint4*>(g0 + lin_storage2d(y, x, lin) * S) + o;
+    uint4* g = reinterpret_cast<uint4*>(g0 + (f0 + j * fstep) * S) + o;
     uint4* r = reinterpret_cast<uint4*>(raw) + v;
     if (load)
       *r = __ldcs(g);
@@ -165,6 +175,9 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
   for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const uint64_t y0 = (t / tiles_x) * 32, x0 = (t % tiles_x) * 32;
     const bool full = y0 + 32 <= p.H && x0 + 32 <= p.W;
+    // storage positions of the tile corner (the rest follow without divisions
+    // or bit loops: a full aligned 32x32 block is 1024 consecutive Morton codes)
+
     uint64_t f[4], qb[4], rl[4];
     uint32_t e[4];
     bool ok[4];
@@ -176,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
         const uint32_t q = threadIdx.x + kThreads * j;
         uint32_t dy, dx;
         tile_order(p.slin.kind, q, dy, dx);
-        e[j] = dy * 33 + dx;
+        e[j] = tile_slot(dy, dx);
         f[j] = (uint64_t)q * p.sS;
       }
       for (int k = 0; k < p.K; ++k) {
@@ -194,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       tile_order(p.slin.kind, threadIdx.x + kThreads * j, dy, dx);
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.slin) : 0;
-      e[j] = dy * 33 + dx;
+      e[j] = tile_slot(dy, dx);
       const DevLeaf& l0 = p.sl[0];
       qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
       rl[j] = f[j] - qb[j] * l0.L;
@@ -220,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
         const uint32_t q = threadIdx.x + kThreads * j;
         uint32_t dy, dx;
         tile_order(p.dlin.kind, q, dy, dx);
-        e[j] = dy * 33 + dx;
+        e[j] = tile_slot(dy, dx);
         f[j] = (uint64_t)q * p.dS;
       }
       for (int k = 0; k < p.K; ++k) {
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       tile_order(p.dlin.kind, threadIdx.x + kThreads * j, dy, dx);
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.dlin) : 0;
-      e[j] = dy * 33 + dx;
+      e[j] = tile_slot(dy, dx);
       const DevLeaf& l0 = p.dl[0];
       qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
       rl[j] = f[j] - qb[j] * l0.L;

@@ -97,7 +97,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   for (int k = 0; k < s.K(); ++k) {
     smem = (smem + 7) & ~7ull;
     base[k] = (uint32_t)smem;
-    smem += 32ull * 33 * s.sizes[k];
+    smem += 32ull * 32 * s.sizes[k];  // 32 x 32 swizzled tile (k_simple.cu tile_slot)
   }
   if (smem > 48 * 1024) { *why = "records too wide for 32x32 tiles"; return false; }
   plan_naive(s, d, p);
