@@ -424,3 +424,52 @@ def test_c5_symmetric_memory_path_one_rank(llama):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["parity_sampled"] is True
     assert line["value"] > 0
+
+
+def _random_spec(rng, n_leaves, depth=0):
+    """A random mapping spec over n_leaves leaves: a plain kind or a split."""
+    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False),
+             ("soa_sb", 1, True), ("aosoa", rng.choice([2, 4, 8, 32]), False), ("aosoa", 8, True)]
+    if n_leaves >= 2 and depth < 2 and rng.random() < 0.5:
+        k = rng.randint(1, n_leaves - 1)
+        leaves_a = sorted(rng.sample(range(n_leaves), k))
+        return (leaves_a, _random_spec(rng, k, depth + 1), _random_spec(rng, n_leaves - k, depth + 1))
+    return rng.choice(kinds)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_split_lin_fuzz(llama, oracle_mod, seed):
+    """Random schemas x random (nested) splits x random storage orders, every
+    applicable path, against the oracle byte for byte."""
+    rng = random.Random(1000 + seed)
+    schema = _random_schema(rng)
+    k = len(oracle_mod.leaf_sizes(schema))
+    ext = rng.choice([[37], [64, 33], [32, 32], [5, 7, 3], [64, 64]])
+    lins = ["row", "col"] + (["morton"] if len(set(ext)) == 1 and ext[0] & (ext[0] - 1) == 0 else [])
+    for _ in range(6):
+        sspec, dspec = _random_spec(rng, k), _random_spec(rng, k)
+        slin = dlin = rng.choice(lins)
+        if len(ext) == 2 and rng.random() < 0.5:
+            dlin = rng.choice(lins)
+        sm = llama.Mapping.from_spec(schema, ext, sspec, lin=slin)
+        dm = llama.Mapping.from_spec(schema, ext, dspec, lin=dlin)
+        so = oracle_mod.mapping_from_spec(schema, ext, sspec, lin=slin)
+        do = oracle_mod.mapping_from_spec(schema, ext, dspec, lin=dlin)
+        sb = sm.alloc("cuda")
+        llama.generate(sm, sb, seed, pad_byte=0xCD)
+        src = oracle_mod.make_view(so, seed, pad_fill=0xCD)
+        for j, t in enumerate(sb):
+            assert np.array_equal(_host(t), src[j]), ("generated", sspec, slin)
+        exp = oracle_mod.copy(so, src, do)
+        for path in ("auto", "naive", "permute", "run", "blobcopy", "transpose"):
+            try:
+                llama.plan(sm, dm, path=path)
+            except llama.LlamaError:
+                continue
+            db = dm.alloc("cuda")
+            for t in db:
+                t.fill_(0x5A)
+            llama.copy(sm, sb, dm, db, path=path)
+            torch.cuda.synchronize()
+            for j, t in enumerate(db):
+                assert np.array_equal(_host(t), exp[j]), (schema, ext, sspec, slin, dspec, dlin, path, j)
