@@ -371,7 +371,7 @@ def run_ours(args, cfg):
         e2e = {"value": step_bytes * world / (ems * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems,
                "method": "llama_copy_staged_batch: pinned host src -> device relayout -> pinned host dst, "
-                         "256 MiB slabs, one pipeline over the step's 16 copies"}
+                         f"256 MiB slabs, one pipeline over the step's {len(pairs)} copies"}
         del hsrc, hdst
 
     cpu = None
