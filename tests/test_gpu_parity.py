@@ -473,3 +473,26 @@ def test_random_split_lin_fuzz(llama, oracle_mod, seed):
             torch.cuda.synchronize()
             for j, t in enumerate(db):
                 assert np.array_equal(_host(t), exp[j]), (schema, ext, sspec, slin, dspec, dlin, path, j)
+
+
+def test_empty_views_every_feature(llama, oracle_mod):
+    """Zero records through splits, One, storage orders, tracing, the move and
+    the staged copy: nothing launched that could touch memory, no errors."""
+    for spec in (W.resolve_spec("split_p7"), ("soa_mb", 1, False), ("aosoa", 8, False)):
+        for ext in ([0], [0, 32], [32, 0]):
+            sm = llama.Mapping.from_spec(W.PARTICLE7, ext, spec)
+            dm = llama.Mapping.from_spec(W.PARTICLE7, ext, ("aos", 1, False))
+            llama.copy(sm, sm.alloc("cuda"), dm, dm.alloc("cuda"))
+            assert llama.nbody_move(sm, sm.alloc("cuda"), 0.1) in ("runs", "aos", "generic")
+            if len(ext) == 2:
+                llama.copy(sm.with_linearizer("col"), sm.alloc("cuda"), dm, dm.alloc("cuda"))
+            t = sm.traced(fields=True, bytes=True)
+            llama.copy(t, t.alloc("cuda"), dm, dm.alloc("cuda"))
+            torch.cuda.synchronize()
+            assert t.field_hits() == [0] * 7
+    st = llama.Stager(1 << 16)
+    a, b = llama.Mapping(W.PARTICLE7, [0]), llama.Mapping(W.PARTICLE7, [0], "soa_mb")
+    llama.copy_staged(st, a, [torch.empty(16, dtype=torch.uint8).pin_memory()], b,
+                      [torch.empty(16, dtype=torch.uint8).pin_memory() for _ in range(7)])
+    llama.nbody_move_staged(st, b, [torch.empty(16, dtype=torch.uint8).pin_memory() for _ in range(7)], 0.1)
+    torch.cuda.synchronize()
