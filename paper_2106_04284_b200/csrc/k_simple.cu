@@ -142,6 +142,48 @@ __device__ __forceinline__ uint64_t tile_leaf_offset(uint64_t f, uint64_t q, uin
   return l.base + q * l.B + l.F + r * l.size;
 }
 
+// kLinear sides (every leaf either L = 1 or one block holding all records,
+// fewer than 2^32 records): leaf element of record f at g + f * m (m = B for
+// L = 1, the leaf size for one block); one 32-bit multiply-add into a 64-bit
+// address instead of the block / lane split (a 64-bit division for SoA, L = N).
+template <typename T, bool kLoad>
+__device__ __forceinline__ void lin_leaf_t(uint8_t* t, uint8_t* g, uint32_t m, const uint32_t (&f)[4],
+                                           const uint32_t (&e)[4], const bool (&ok)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (ok[j]) {
+      T* ge = reinterpret_cast<T*>(g + (uint64_t)f[j] * m);
+      T* te = reinterpret_cast<T*>(t) + e[j];
+      if (kLoad)
+        *te = *ge;
+      else
+        *ge = *te;
+    }
+}
+
+template <bool kAligned, bool kLoad>
+__device__ __forceinline__ void lin_leaf(uint8_t* t, uint8_t* g, uint32_t m, uint32_t size, const uint32_t (&f)[4],
+                                         const uint32_t (&e)[4], const bool (&ok)[4]) {
+  if (kAligned) {
+    switch (size) {
+      case 4: lin_leaf_t<uint32_t, kLoad>(t, g, m, f, e, ok); return;
+      case 8: lin_leaf_t<uint64_t, kLoad>(t, g, m, f, e, ok); return;
+      case 2: lin_leaf_t<uint16_t, kLoad>(t, g, m, f, e, ok); return;
+      case 1: lin_leaf_t<uint8_t, kLoad>(t, g, m, f, e, ok); return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (ok[j]) {
+      uint8_t* ge = g + (uint64_t)f[j] * m;
+      uint8_t* te = t + e[j] * size;
+      if (kLoad)
+        move_elem<kAligned>(te, ge, size);
+      else
+        move_elem<kAligned>(ge, te, size);
+    }
+}
+
 // Raw AoS side of a full tile: its 1024 records in the side's storage order
 // are 32 contiguous segments of 32 records (rows or columns) or, for Morton,
 // one segment of 1024; moved as 16-byte vectors between global memory and a
@@ -167,7 +209,7 @@ __device__ __forceinline__ void raw_tile(uint8_t* g0, uint8_t* raw, const DevLin
 
 // kRaw: a raw AoS side exists (separate instantiation: the raw code costs
 // registers, and element-only tiles are latency-bound, so occupancy matters)
-template <bool kAligned, bool kUniform, bool kRaw>
+template <bool kAligned, bool kUniform, bool kRaw, bool kLinear>
 __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant__ NaiveParams p) {
   extern __shared__ __align__(16) uint8_t tsm[];
   const uint64_t tiles_x = (p.W + 31) / 32, n_tiles = tiles_x * ((p.H + 31) / 32);
@@ -208,10 +250,22 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.slin) : 0;
       e[j] = tile_slot(dy, dx);
-      const DevLeaf& l0 = p.sl[0];
-      qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
-      rl[j] = f[j] - qb[j] * l0.L;
+      if (!kLinear) {
+        const DevLeaf& l0 = p.sl[0];
+        qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
+        rl[j] = f[j] - qb[j] * l0.L;
+      }
     }
+    if (kLinear) {
+      uint32_t fl[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
+      for (int k = 0; k < p.K; ++k) {
+        const DevLeaf& l = p.sl[k];
+        lin_leaf<kAligned, true>(tsm + p.tbase[k], const_cast<uint8_t*>(p.sb[l.blob]) + l.base + l.F,
+                                 l.L == 1 ? (uint32_t)l.B : l.size, l.size, fl, e, ok);
+      }
+    } else
     for (int k = 0; k < p.K; ++k) {
       const DevLeaf l = p.sl[k];
       const uint8_t* sb = p.sb[l.blob];
@@ -254,10 +308,22 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.dlin) : 0;
       e[j] = tile_slot(dy, dx);
-      const DevLeaf& l0 = p.dl[0];
-      qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
-      rl[j] = f[j] - qb[j] * l0.L;
+      if (!kLinear) {
+        const DevLeaf& l0 = p.dl[0];
+        qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
+        rl[j] = f[j] - qb[j] * l0.L;
+      }
     }
+    if (kLinear) {
+      uint32_t fl[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
+      for (int k = 0; k < p.K; ++k) {
+        const DevLeaf& l = p.dl[k];
+        lin_leaf<kAligned, false>(tsm + p.tbase[k], p.db[l.blob] + l.base + l.F, l.L == 1 ? (uint32_t)l.B : l.size,
+                                  l.size, fl, e, ok);
+      }
+    } else
     for (int k = 0; k < p.K; ++k) {
       const DevLeaf l = p.dl[k];
       uint8_t* db = p.db[l.blob];
@@ -273,14 +339,25 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
 int launch_transpose2d(const NaiveParams& p, void* stream) {
   const uint64_t n_tiles = ((p.W + 31) / 32) * ((p.H + 31) / 32);
   if (n_tiles == 0) return 0;
-  static LaunchCache cache[8][64];
+  static LaunchCache cache[16][64];
   int dev = 0, per_sm = 1, sms = 148;
   cudaGetDevice(&dev);
-  void (*const kerns[8])(NaiveParams) = {
-      k_transpose2d<false, false, false>, k_transpose2d<true, false, false>, k_transpose2d<false, true, false>,
-      k_transpose2d<true, true, false>,   k_transpose2d<false, false, true>, k_transpose2d<true, false, true>,
-      k_transpose2d<false, true, true>,   k_transpose2d<true, true, true>};
-  const int v = (p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0) + ((p.sraw || p.draw) ? 4 : 0);
+  // index: aligned + 2 uniform + 4 raw + 8 linear (linear sides are uniform)
+  void (*const kerns[16])(NaiveParams) = {
+      k_transpose2d<false, false, false, false>, k_transpose2d<true, false, false, false>,
+      k_transpose2d<false, true, false, false>,  k_transpose2d<true, true, false, false>,
+      k_transpose2d<false, false, true, false>,  k_transpose2d<true, false, true, false>,
+      k_transpose2d<false, true, true, false>,   k_transpose2d<true, true, true, false>,
+      nullptr,
+      nullptr,
+      k_transpose2d<false, true, false, true>,
+      k_transpose2d<true, true, false, true>,
+      nullptr,
+      nullptr,
+      k_transpose2d<false, true, true, true>,
+      k_transpose2d<true, true, true, true>};
+  const int v = (p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0) + ((p.sraw || p.draw) ? 4 : 0) +
+                ((p.tuniform && p.tlinear) ? 8 : 0);
   auto kern = kerns[v];
   int e = prepare_kernel(kern, kThreads, (int)p.tsmem, &cache[v][dev & 63], &per_sm);
   if (e) return e;

@@ -108,6 +108,13 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   n.tsmem = (uint32_t)smem;
   for (int k = 0; k < s.K(); ++k) n.tbase[k] = base[k];
   n.tuniform = (s.uniform && d.uniform) ? 1 : 0;
+  // linear sides: L = 1 (AoS, One) or one block of all records (SoA); the
+  // kernel then locates leaf elements with one 32-bit multiply-add
+  n.tlinear = n.tuniform && s.N < (1ull << 32);
+  for (const Mapping* m : {&s, &d})
+    for (int k = 0; k < m->K(); ++k)
+      if (!((m->Lk[k] == 1 && m->Bk[k] < (1ull << 32)) || m->Lk[k] >= m->N)) n.tlinear = 0;
+  if (!env_u64("LLAMA_TRANSPOSE_LINEAR", 1)) n.tlinear = 0;
   // plain AoS sides move whole tiles as 16-byte vectors through a raw record
   // buffer: every 32-record row / column segment (a 1024-record Morton tile)
   // must start 16-byte aligned
@@ -129,7 +136,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   // measured (4096^2 Particle7): raw on both sides 1.54 -> 2.37 TB/s; one
   // raw side next to an element-wise SoA side is slower than element-wise
   // on both (2.52 -> 2.22 TB/s: the raw code's registers cost occupancy)
-  if (!(n.sraw && n.draw)) n.sraw = n.draw = 0, raw_bytes = 0;
+  if (!(n.sraw && n.draw) && !(n.tlinear && env_u64("LLAMA_TRANSPOSE_RAW1", 1))) n.sraw = n.draw = 0, raw_bytes = 0;
   if (raw_bytes) {
     smem = (smem + 15) & ~15ull;
     n.rawoff = (uint32_t)smem;

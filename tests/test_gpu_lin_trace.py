@@ -132,3 +132,20 @@ def test_raw_aos_tiles(llama, oracle_mod, lins):
         for sk, dk in (((("aos", 1, False)), ("aos", 1, True)), (("aos", 1, True), ("aos", 1, False)),
                        (("aos", 1, False), ("aos", 1, False))):
             _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "naive"))
+
+
+@pytest.mark.parametrize("knobs", [{"LLAMA_TRANSPOSE_LINEAR": "0"}, {"LLAMA_TRANSPOSE_RAW1": "0"},
+                                   {"LLAMA_TRANSPOSE_RAW": "0"}, {}])
+def test_transpose_variants(llama, oracle_mod, monkeypatch, knobs):
+    """Every k_transpose2d instantiation: linear sides (one multiply-add per
+    element) or the block / lane split, a raw AoS side next to an element-wise
+    side, raw on both sides or none; full and ragged tiles, 4- and mixed-size
+    leaves, AoSoA sides (not linear)."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [70, 45]), (W.PARTICLE7, [64, 64])):
+        for sk, dk in ((("soa_mb", 1, False), ("aos", 1, False)), (("aos", 1, True), ("soa_sb", 1, True)),
+                       (("aos", 1, False), ("aos", 1, True)), (("aosoa", 8, False), ("aos", 1, False)),
+                       (("one", 1, True), ("soa_mb", 1, False))):
+            for lins in (("morton", "col") if ext[0] == ext[1] else ("row", "col"), ("col", "row")):
+                _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "transpose"))
