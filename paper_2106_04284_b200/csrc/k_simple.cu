@@ -184,6 +184,38 @@ __device__ __forceinline__ void lin_leaf(uint8_t* t, uint8_t* g, uint32_t m, uin
     }
 }
 
+// Element-wise source with linear sides whose leaves all have one naturally
+// aligned size T: two leaves x four records per pass, so eight loads of a
+// thread are in flight before the first is consumed (one leaf per pass: the
+// shared store waits on its load before the next leaf's loads issue).
+template <typename T>
+__device__ __forceinline__ void lin_load_fixed(uint8_t* tsm, const uint32_t* tbase, const DevLeaf* leaves,
+                                               const uint8_t* const* blobs, int K, const uint32_t (&f)[4],
+                                               const uint32_t (&e)[4], const bool (&ok)[4]) {
+  constexpr int U = 2;
+  for (int k0 = 0; k0 < K; k0 += U) {
+    T v[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + u < K) {
+        const DevLeaf& l = leaves[k0 + u];
+        const uint8_t* g = blobs[l.blob] + l.base + l.F;
+        const uint32_t m = l.L == 1 ? (uint32_t)l.B : (uint32_t)sizeof(T);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ok[j]) v[u][j] = *reinterpret_cast<const T*>(g + (uint64_t)f[j] * m);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + u < K) {
+        T* t = reinterpret_cast<T*>(tsm + tbase[k0 + u]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ok[j]) t[e[j]] = v[u][j];
+      }
+  }
+}
+
 // Raw AoS side of a full tile: its 1024 records in the side's storage order
 // are 32 contiguous segments of 32 records (rows or columns) or, for Morton,
 // one segment of 1024; moved as 16-byte vectors between global memory and a
@@ -209,7 +241,7 @@ __device__ __forceinline__ void raw_tile(uint8_t* g0, uint8_t* raw, const DevLin
 
 // kRaw: a raw AoS side exists (separate instantiation: the raw code costs
 // registers, and element-only tiles are latency-bound, so occupancy matters)
-template <bool kAligned, bool kUniform, bool kRaw, bool kLinear>
+template <bool kAligned, bool kUniform, bool kRaw, int kLin>
 __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant__ NaiveParams p) {
   extern __shared__ __align__(16) uint8_t tsm[];
   const uint64_t tiles_x = (p.W + 31) / 32, n_tiles = tiles_x * ((p.H + 31) / 32);
@@ -250,13 +282,21 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.slin) : 0;
       e[j] = tile_slot(dy, dx);
-      if (!kLinear) {
+      if (!kLin) {
         const DevLeaf& l0 = p.sl[0];
         qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
         rl[j] = f[j] - qb[j] * l0.L;
       }
     }
-    if (kLinear) {
+    if (kLin == 4 || kLin == 8) {
+      uint32_t fl[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
+      if (kLin == 4)
+        lin_load_fixed<uint32_t>(tsm, p.tbase, p.sl, p.sb, p.K, fl, e, ok);
+      else
+        lin_load_fixed<uint64_t>(tsm, p.tbase, p.sl, p.sb, p.K, fl, e, ok);
+    } else if (kLin) {
       uint32_t fl[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
@@ -308,13 +348,13 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       ok[j] = y0 + dy < p.H && x0 + dx < p.W;
       f[j] = ok[j] ? lin_storage2d(y0 + dy, x0 + dx, p.dlin) : 0;
       e[j] = tile_slot(dy, dx);
-      if (!kLinear) {
+      if (!kLin) {
         const DevLeaf& l0 = p.dl[0];
         qb[j] = l0.lshift != kNoShift ? (f[j] >> l0.lshift) : f[j] / l0.L;
         rl[j] = f[j] - qb[j] * l0.L;
       }
     }
-    if (kLinear) {
+    if (kLin) {  // (stores do not stall: the one-leaf pass; the two-leaf pass measured -3% here)
       uint32_t fl[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
@@ -339,25 +379,27 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
 int launch_transpose2d(const NaiveParams& p, void* stream) {
   const uint64_t n_tiles = ((p.W + 31) / 32) * ((p.H + 31) / 32);
   if (n_tiles == 0) return 0;
-  static LaunchCache cache[16][64];
+  static LaunchCache cache[24][64];
   int dev = 0, per_sm = 1, sms = 148;
   cudaGetDevice(&dev);
-  // index: aligned + 2 uniform + 4 raw + 8 linear (linear sides are uniform)
-  void (*const kerns[16])(NaiveParams) = {
-      k_transpose2d<false, false, false, false>, k_transpose2d<true, false, false, false>,
-      k_transpose2d<false, true, false, false>,  k_transpose2d<true, true, false, false>,
-      k_transpose2d<false, false, true, false>,  k_transpose2d<true, false, true, false>,
-      k_transpose2d<false, true, true, false>,   k_transpose2d<true, true, true, false>,
-      nullptr,
-      nullptr,
-      k_transpose2d<false, true, false, true>,
-      k_transpose2d<true, true, false, true>,
-      nullptr,
-      nullptr,
-      k_transpose2d<false, true, true, true>,
-      k_transpose2d<true, true, true, true>};
-  const int v = (p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0) + ((p.sraw || p.draw) ? 4 : 0) +
-                ((p.tuniform && p.tlinear) ? 8 : 0);
+  // index: aligned + 2 uniform + 4 raw (+ 8 linear, mixed leaf sizes; 16 / 20:
+  // linear with one aligned 4- / 8-byte leaf size; linear sides are uniform)
+  void (*const kerns[24])(NaiveParams) = {
+      k_transpose2d<false, false, false, 0>, k_transpose2d<true, false, false, 0>,
+      k_transpose2d<false, true, false, 0>,  k_transpose2d<true, true, false, 0>,
+      k_transpose2d<false, false, true, 0>,  k_transpose2d<true, false, true, 0>,
+      k_transpose2d<false, true, true, 0>,   k_transpose2d<true, true, true, 0>,
+      nullptr, nullptr, k_transpose2d<false, true, false, 1>, k_transpose2d<true, true, false, 1>,
+      nullptr, nullptr, k_transpose2d<false, true, true, 1>,  k_transpose2d<true, true, true, 1>,
+      nullptr, k_transpose2d<true, true, false, 4>, nullptr, k_transpose2d<true, true, true, 4>,
+      nullptr, k_transpose2d<true, true, false, 8>, nullptr, k_transpose2d<true, true, true, 8>};
+  int v = (p.taligned ? 1 : 0) + (p.tuniform ? 2 : 0) + ((p.sraw || p.draw) ? 4 : 0);
+  if (p.tuniform && p.tlinear) {
+    // (only for an element-wise source: with a raw source the loads are
+    // vectors and the variant's registers only cost occupancy, -5%)
+    const int fixed = p.taligned && (p.tlinear == 4 || p.tlinear == 8) && !p.sraw;
+    v = fixed ? (p.tlinear == 4 ? 16 : 20) + 1 + ((p.sraw || p.draw) ? 2 : 0) : v + 8;
+  }
   auto kern = kerns[v];
   int e = prepare_kernel(kern, kThreads, (int)p.tsmem, &cache[v][dev & 63], &per_sm);
   if (e) return e;

@@ -69,7 +69,8 @@ struct NaiveParams {
   uint32_t tbase[kMaxLeaves];  // TRANSPOSE: leaf k's 32x33-element tile at smem + tbase[k]
   uint32_t taligned;           // TRANSPOSE: every element of both sides naturally aligned
   uint32_t tuniform;           // TRANSPOSE: both sides share one L and B over all leaves
-  uint32_t tlinear;            // TRANSPOSE: every leaf of both sides at base + F + f * (L == 1 ? B : size), f < 2^32
+  uint32_t tlinear;            // TRANSPOSE: every leaf of both sides at base + F + f * (L == 1 ? B : size),
+                               // f < 2^32: 0 = no, else the one leaf size of all leaves (4 or 8) or 1 (mixed)
   uint32_t sraw, draw;         // TRANSPOSE: that side is a plain AoS moved as raw 16-byte vectors
   uint32_t rawoff;             // TRANSPOSE: shared-memory offset of the raw record buffer
   uint32_t sS, dS;             // TRANSPOSE: record strides of the raw sides

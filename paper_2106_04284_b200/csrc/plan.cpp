@@ -115,6 +115,12 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
     for (int k = 0; k < m->K(); ++k)
       if (!((m->Lk[k] == 1 && m->Bk[k] < (1ull << 32)) || m->Lk[k] >= m->N)) n.tlinear = 0;
   if (!env_u64("LLAMA_TRANSPOSE_LINEAR", 1)) n.tlinear = 0;
+  if (n.tlinear) {  // one leaf size of 4 or 8 bytes: the two-leaf pass (k_simple.cu lin_tile_fixed)
+    const uint64_t z = s.sizes[0];
+    bool same = (z == 4 || z == 8) && env_u64("LLAMA_TRANSPOSE_FIXED", 1);
+    for (int k = 0; k < s.K(); ++k) same = same && s.sizes[k] == z;
+    n.tlinear = same ? (uint32_t)z : 1;
+  }
   // plain AoS sides move whole tiles as 16-byte vectors through a raw record
   // buffer: every 32-record row / column segment (a 1024-record Morton tile)
   // must start 16-byte aligned

@@ -135,12 +135,14 @@ def test_raw_aos_tiles(llama, oracle_mod, lins):
 
 
 @pytest.mark.parametrize("knobs", [{"LLAMA_TRANSPOSE_LINEAR": "0"}, {"LLAMA_TRANSPOSE_RAW1": "0"},
+                                   {"LLAMA_TRANSPOSE_FIXED": "0"},
                                    {"LLAMA_TRANSPOSE_RAW": "0"}, {}])
 def test_transpose_variants(llama, oracle_mod, monkeypatch, knobs):
     """Every k_transpose2d instantiation: linear sides (one multiply-add per
     element) or the block / lane split, a raw AoS side next to an element-wise
-    side, raw on both sides or none; full and ragged tiles, 4- and mixed-size
-    leaves, AoSoA sides (not linear)."""
+    side, raw on both sides or none, the two-leaf pass for one 4-byte leaf
+    size; full and ragged tiles, 4- and mixed-size leaves, AoSoA sides (not
+    linear)."""
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [70, 45]), (W.PARTICLE7, [64, 64])):
