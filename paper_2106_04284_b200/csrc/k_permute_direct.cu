@@ -207,6 +207,52 @@ __device__ __forceinline__ void direct_class_mix(const DirectParams& p, const Di
   }
 }
 
+// SoA -> AoS, a class of 4- / 8-byte leaves aligned in both the image and
+// global memory: each element goes global -> shared by cp.async (LDGSTS), so
+// a lane has every element of its share of the class in flight without
+// holding registers (the register path waits on its loads every 8 leaves).
+// Lane mapping as in direct_class_mix (p.mix) or direct_class.
+template <uint32_t SZ, bool kFull>
+__device__ __forceinline__ void direct_class_async(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                                   uint64_t t0, uint32_t nrec, int warp, int lane) {
+  typedef typename UT<SZ>::T U;
+  const uint32_t base = smem_u32(img);
+  if (p.mix) {
+    const uint32_t sub = (uint32_t)lane >> 3, rl = (uint32_t)lane & 7;
+    for (uint32_t g0 = c.k0 + 4 * warp; g0 < c.k1; g0 += 4 * (kCons / 32)) {
+      const uint32_t i = g0 + sub;
+      if (i >= c.k1) continue;
+      const DirectLeaf& l = p.leaf[p.order[i]];
+      const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t r = 8 * q + rl;
+        if (kFull || r < nrec)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(base + r * p.S + l.F), "l"(g + r),
+                       "n"(SZ)
+                       : "memory");
+      }
+    }
+    return;
+  }
+  for (uint32_t i = c.k0 + warp; i < c.k1; i += kCons / 32) {
+    const DirectLeaf& l = p.leaf[p.order[i]];
+    const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t r = (uint32_t)lane + 32 * h;
+      if (kFull || r < nrec)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(base + r * p.S + l.F), "l"(g + r), "n"(SZ)
+                     : "memory");
+    }
+  }
+}
+
+__device__ __forceinline__ bool async_class(const DirectParams& p, const DirectClass& c) {
+  const uint32_t z = c.kind & 15;
+  return p.async && (c.kind & 48) == 48 && (z == 4 || z == 8);
+}
+
 template <bool kA2S, uint32_t SZ, bool kFull>
 __device__ __forceinline__ void direct_class_a(const DirectParams& p, const DirectClass& c, uint8_t* img, uint64_t t0,
                                                uint32_t nrec, int warp, int lane) {
@@ -229,8 +275,20 @@ __device__ __forceinline__ void direct_class_a(const DirectParams& p, const Dire
 template <bool kA2S, bool kFull>
 __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img, uint64_t t0, uint32_t nrec, int warp,
                                             int lane) {
+  if (!kA2S && p.async) {  // the cp.async classes first, then the register classes overlap them
+    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
+      const DirectClass c = p.cls[ci];
+      if (!async_class(p, c)) continue;
+      if ((c.kind & 15) == 8)
+        direct_class_async<8, kFull>(p, c, img, t0, nrec, warp, lane);
+      else
+        direct_class_async<4, kFull>(p, c, img, t0, nrec, warp, lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
     const DirectClass c = p.cls[ci];
+    if (!kA2S && async_class(p, c)) continue;
     switch (c.kind & 15) {
       case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
       case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
@@ -326,6 +384,7 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
     else
       direct_tile<kA2S, false>(p, img, t0, nrec, warp, lane);
     if (!kA2S) {
+      if (p.async) asm volatile("cp.async.wait_all;" ::: "memory");
       if (body < bytes) {  // the last tile's sub-16-byte tail goes out directly
         cons_sync();
         for (uint32_t o = body + tid; o < bytes; o += kCons) ag[t0 * p.S + o] = img[o];

@@ -285,6 +285,7 @@ struct DirectParams {
   uint32_t a2s;      // 1: AoS -> SoA (ring holds source tiles); 0: SoA -> AoS (ring holds destination tiles)
   uint32_t ns, stage;
   uint32_t mix;      // 1: aligned-image classes use the 4-leaves x 8-records warp mapping
+  uint32_t async;    // SoA -> AoS: 4- / 8-byte classes aligned on both sides land by cp.async
   uint32_t pad_;
   uint64_t abase;    // AoS side: byte offset of record 0 in blob `ablob`
   uint32_t ablob;

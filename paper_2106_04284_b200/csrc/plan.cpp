@@ -276,6 +276,8 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   dp.n_tiles = ceil_div(s.N, T);
   // an even record stride in words puts one leaf of 32 records on few banks
   dp.mix = ((S / 4) % 2 == 0 && S % 4 == 0 && env_u64("LLAMA_DIRECT_MIX", 1)) ? 1 : 0;
+  // SoA -> AoS: aligned 4- / 8-byte elements land in the image by cp.async
+  dp.async = (!a2s && env_u64("LLAMA_DIRECT_ASYNC", 1)) ? 1 : 0;
   dp.abase = A.base[0];
   dp.ablob = A.blob[0];
   auto lb = [](uint64_t x) { return x ? (x & (~x + 1)) : 16ull; };

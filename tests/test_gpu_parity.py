@@ -382,11 +382,14 @@ def test_one_and_mapping_c_sources(llama, oracle_mod, n):
 # ------------------------------------------------ direct AoS <-> SoA variant
 @pytest.mark.parametrize("schema_name", ["listing1", "particle7", "hep100"])
 @pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097])
-def test_direct_variant_forced(llama, oracle_mod, schema_name, n, monkeypatch):
+@pytest.mark.parametrize("use_async", ["1", "0"])
+def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async, monkeypatch):
     """The direct permute (AoS side through TMA, SoA side element-wise) for
     every AoS <-> SoA pair, forced for few-leaf records too (LLAMA_DIRECT=2):
-    odd record strides exercise the byte-wise shared-memory accesses."""
+    odd record strides exercise the byte-wise shared-memory accesses; SoA ->
+    AoS with the cp.async classes and with registers only."""
     monkeypatch.setenv("LLAMA_DIRECT", "2")
+    monkeypatch.setenv("LLAMA_DIRECT_ASYNC", use_async)
     schema = W.SCHEMAS[schema_name]
     names = ["aos", "aos_aligned", "soa_mb", "soa_sb", "soa_sb_aligned"]
     for a in names:
