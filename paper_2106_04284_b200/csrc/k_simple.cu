@@ -142,6 +142,16 @@ __device__ __forceinline__ uint64_t tile_leaf_offset(uint64_t f, uint64_t q, uin
   return l.base + q * l.B + l.F + r * l.size;
 }
 
+// Per-CTA table of a linear side's leaves (built once per CTA in shared
+// memory: one 16-byte load per leaf instead of the descriptor's fields from
+// parameter space): element of record f at g + f * m, tile at tbz & 0xFFFFFF,
+// leaf size tbz >> 24.
+struct __align__(16) LinEnt {
+  uint8_t* g;
+  uint32_t m;
+  uint32_t tbz;
+};
+
 // kLinear sides (every leaf either L = 1 or one block holding all records,
 // fewer than 2^32 records): leaf element of record f at g + f * m (m = B for
 // L = 1, the leaf size for one block); one 32-bit multiply-add into a 64-bit
@@ -188,9 +198,8 @@ __device__ __forceinline__ void lin_leaf(uint8_t* t, uint8_t* g, uint32_t m, uin
 // aligned size T: two leaves x four records per pass, so eight loads of a
 // thread are in flight before the first is consumed (one leaf per pass: the
 // shared store waits on its load before the next leaf's loads issue).
-template <typename T>
-__device__ __forceinline__ void lin_load_fixed(uint8_t* tsm, const uint32_t* tbase, const DevLeaf* leaves,
-                                               const uint8_t* const* blobs, int K, const uint32_t (&f)[4],
+template <typename T, typename Get>
+__device__ __forceinline__ void lin_load_fixed(uint8_t* tsm, const Get& get, int K, const uint32_t (&f)[4],
                                                const uint32_t (&e)[4], const bool (&ok)[4]) {
   constexpr int U = 2;
   for (int k0 = 0; k0 < K; k0 += U) {
@@ -198,17 +207,15 @@ __device__ __forceinline__ void lin_load_fixed(uint8_t* tsm, const uint32_t* tba
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k0 + u < K) {
-        const DevLeaf& l = leaves[k0 + u];
-        const uint8_t* g = blobs[l.blob] + l.base + l.F;
-        const uint32_t m = l.L == 1 ? (uint32_t)l.B : (uint32_t)sizeof(T);
+        const LinEnt l = get(k0 + u);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (ok[j]) v[u][j] = *reinterpret_cast<const T*>(g + (uint64_t)f[j] * m);
+          if (ok[j]) v[u][j] = *reinterpret_cast<const T*>(l.g + (uint64_t)f[j] * l.m);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k0 + u < K) {
-        T* t = reinterpret_cast<T*>(tsm + tbase[k0 + u]);
+        T* t = reinterpret_cast<T*>(tsm + (get(k0 + u).tbz & 0xFFFFFFu));
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (ok[j]) t[e[j]] = v[u][j];
@@ -246,6 +253,20 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
   extern __shared__ __align__(16) uint8_t tsm[];
   const uint64_t tiles_x = (p.W + 31) / 32, n_tiles = tiles_x * ((p.H + 31) / 32);
   uint8_t* raw = tsm + p.rawoff;
+  // kLin: the leaf table, [0, K) source, [K, 2K) destination; in shared
+  // memory when p.linoff != 0 (not with a raw side: its 56 KB of tile + raw
+  // buffer for Particle7 fill a quarter SM exactly), else from parameters
+  LinEnt* lt = reinterpret_cast<LinEnt*>(tsm + p.linoff);
+  auto ent = [&](int i) -> LinEnt {
+    const int k = i < p.K ? i : i - p.K;
+    const DevLeaf& l = i < p.K ? p.sl[k] : p.dl[k];
+    uint8_t* b = i < p.K ? const_cast<uint8_t*>(p.sb[l.blob]) : p.db[l.blob];
+    return LinEnt{b + l.base + l.F, l.L == 1 ? (uint32_t)l.B : l.size, p.tbase[k] | (l.size << 24)};
+  };
+  if (kLin && p.linoff) {
+    for (int i = threadIdx.x; i < 2 * p.K; i += kThreads) lt[i] = ent(i);
+    __syncthreads();
+  }
   for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const uint64_t y0 = (t / tiles_x) * 32, x0 = (t % tiles_x) * 32;
     const bool full = y0 + 32 <= p.H && x0 + 32 <= p.W;
@@ -292,18 +313,18 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
       uint32_t fl[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
+      auto get = [&](int k) { return p.linoff ? lt[k] : ent(k); };
       if (kLin == 4)
-        lin_load_fixed<uint32_t>(tsm, p.tbase, p.sl, p.sb, p.K, fl, e, ok);
+        lin_load_fixed<uint32_t>(tsm, get, p.K, fl, e, ok);
       else
-        lin_load_fixed<uint64_t>(tsm, p.tbase, p.sl, p.sb, p.K, fl, e, ok);
+        lin_load_fixed<uint64_t>(tsm, get, p.K, fl, e, ok);
     } else if (kLin) {
       uint32_t fl[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
       for (int k = 0; k < p.K; ++k) {
-        const DevLeaf& l = p.sl[k];
-        lin_leaf<kAligned, true>(tsm + p.tbase[k], const_cast<uint8_t*>(p.sb[l.blob]) + l.base + l.F,
-                                 l.L == 1 ? (uint32_t)l.B : l.size, l.size, fl, e, ok);
+        const LinEnt l = p.linoff ? lt[k] : ent(k);
+        lin_leaf<kAligned, true>(tsm + (l.tbz & 0xFFFFFFu), l.g, l.m, l.tbz >> 24, fl, e, ok);
       }
     } else
     for (int k = 0; k < p.K; ++k) {
@@ -359,9 +380,8 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
 #pragma unroll
       for (int j = 0; j < 4; ++j) fl[j] = (uint32_t)f[j];
       for (int k = 0; k < p.K; ++k) {
-        const DevLeaf& l = p.dl[k];
-        lin_leaf<kAligned, false>(tsm + p.tbase[k], p.db[l.blob] + l.base + l.F, l.L == 1 ? (uint32_t)l.B : l.size,
-                                  l.size, fl, e, ok);
+        const LinEnt l = p.linoff ? lt[p.K + k] : ent(p.K + k);
+        lin_leaf<kAligned, false>(tsm + (l.tbz & 0xFFFFFFu), l.g, l.m, l.tbz >> 24, fl, e, ok);
       }
     } else
     for (int k = 0; k < p.K; ++k) {

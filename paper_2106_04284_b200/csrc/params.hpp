@@ -75,6 +75,7 @@ struct NaiveParams {
   uint32_t rawoff;             // TRANSPOSE: shared-memory offset of the raw record buffer
   uint32_t sS, dS;             // TRANSPOSE: record strides of the raw sides
   uint32_t dpad;               // TRANSPOSE: the raw destination has padding bytes (zero the buffer)
+  uint32_t linoff;             // TRANSPOSE, linear sides: shared-memory offset of the per-CTA leaf table
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];

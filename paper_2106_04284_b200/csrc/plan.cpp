@@ -154,6 +154,15 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
     }
     n.tsmem = (uint32_t)smem;
   }
+  // per-CTA leaf table of both sides (k_simple.cu LinEnt, 16 B per leaf);
+  // not next to a raw buffer (Particle7: 56 KB of tile + raw buffer fill a
+  // quarter SM exactly, the table would cost a CTA per SM: -17%)
+  if (n.tlinear && !n.sraw && !n.draw && env_u64("LLAMA_TRANSPOSE_TABLE", 1)) {
+    smem = (smem + 15) & ~15ull;
+    n.linoff = (uint32_t)smem;
+    smem += 2ull * 16 * s.K();
+    n.tsmem = (uint32_t)smem;
+  }
   n.taligned = 1;  // blobs are 16-B aligned: check the normal forms
   for (const Mapping* m : {&s, &d})
     for (int k = 0; k < m->K(); ++k) {
