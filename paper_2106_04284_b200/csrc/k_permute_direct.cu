@@ -19,6 +19,19 @@ constexpr int kCons = 256;  // consumer threads
 constexpr int kBars = 128;  // 2 rings x <= 8 stages x 8 B
 }  // namespace
 
+// Per-CTA leaf table in class order (after the ring and its 16-byte slack):
+// one 16-byte shared load per leaf visit instead of a dependent chain of
+// parameter-space loads (order[i], then the descriptor's fields).
+struct __align__(16) DTab {
+  uint8_t* gptr;
+  uint32_t F;
+  uint32_t a_img;  // bits 0-7; bits 8-31: staging offset (DirectLeaf::stg)
+};
+extern __shared__ __align__(128) uint8_t dsmem[];
+__device__ __forceinline__ const DTab* dtab(const DirectParams& p) {
+  return reinterpret_cast<const DTab*>(dsmem + kBars + (size_t)p.ns * p.stage + 16);
+}
+
 // An element of `s` bytes at a shared-memory address aligned to `a`.
 __device__ __forceinline__ uint64_t sm_gather(const uint8_t* p, uint32_t s, uint32_t a) {
   if (a >= s) {
@@ -43,6 +56,45 @@ __device__ __forceinline__ uint64_t sm_gather(const uint8_t* p, uint32_t s, uint
   const uint32_t hi = __funnelshift_r(w1, w[2], sh);
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
+
+// The same for an element whose address is 4-byte aligned minus LO2 bytes
+// at every record (record stride a multiple of 4: the word phase is a
+// per-leaf constant), shifts fixed at compile time.
+template <uint32_t SZ, uint32_t LO2>
+__device__ __forceinline__ uint64_t sm_gather_ph(const uint8_t* p) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(p - LO2);
+  if (SZ == 8) {
+    if (LO2 == 0) return (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+    const uint32_t w1 = w[1];
+    return (uint64_t)__funnelshift_r(w[0], w1, 8 * LO2) | ((uint64_t)__funnelshift_r(w1, w[2], 8 * LO2) << 32);
+  }
+  if (SZ == 4) return LO2 == 0 ? w[0] : __funnelshift_r(w[0], w[1], 8 * LO2);
+  if (SZ == 2) return LO2 < 3 ? (w[0] >> (8 * LO2)) & 0xFFFFu : __funnelshift_r(w[0], w[1], 24) & 0xFFFFu;
+  return (w[0] >> (8 * LO2)) & 0xFFu;
+}
+
+// Store an element whose first byte sits LO2 bytes past a 4-byte boundary
+// (fixed per leaf when the record stride is a multiple of 4): the widest
+// naturally aligned pieces, chosen at compile time (never touching the
+// neighbouring leaves' bytes).
+template <uint32_t SZ, uint32_t LO2, uint32_t OFF>
+struct ScatterPh {
+  static __device__ __forceinline__ void run(uint8_t* p, uint64_t v) {
+    constexpr uint32_t a = LO2 + OFF, rem = SZ - OFF;
+    constexpr uint32_t w = (a % 4 == 0 && rem >= 4) ? 4 : ((a % 2 == 0 && rem >= 2) ? 2 : 1);
+    if (w == 4)
+      *reinterpret_cast<uint32_t*>(p + OFF) = (uint32_t)(v >> (8 * OFF));
+    else if (w == 2)
+      *reinterpret_cast<uint16_t*>(p + OFF) = (uint16_t)(v >> (8 * OFF));
+    else
+      p[OFF] = (uint8_t)(v >> (8 * OFF));
+    ScatterPh<SZ, LO2, OFF + w>::run(p, v);
+  }
+};
+template <uint32_t SZ, uint32_t LO2>
+struct ScatterPh<SZ, LO2, SZ> {
+  static __device__ __forceinline__ void run(uint8_t*, uint64_t) {}
+};
 
 __device__ __forceinline__ void sm_scatter(uint8_t* p, uint64_t v, uint32_t s, uint32_t a) {
   if (a >= s) {
@@ -101,7 +153,7 @@ template <> struct UT<8> { typedef unsigned long long T; };
 // One class of leaves (equal size, alignment classes) for the tile's records
 // lane and lane + 32: warps take the class's leaves in turn, kU at a time, so
 // each lane has 2 * kU independent accesses in flight.
-template <bool kA2S, uint32_t SZ, bool kImgA, bool kGlobA, bool kFull>
+template <bool kA2S, uint32_t SZ, bool kImgA, bool kGlobA, bool kFull, int kPh = -1>
 __device__ __forceinline__ void direct_class(const DirectParams& p, const DirectClass& c, uint8_t* img,
                                              uint64_t t0, uint32_t nrec, int warp, int lane) {
   typedef typename UT<SZ>::T U;
@@ -114,15 +166,18 @@ __device__ __forceinline__ void direct_class(const DirectParams& p, const Direct
     for (int u = 0; u < kU; ++u) {
       const uint32_t i = i0 + u * (kCons / 32);
       const bool has = i < c.k1;
-      const DirectLeaf& l = p.leaf[p.order[has ? i : c.k0]];
+      const DTab l = dtab(p)[has ? i : c.k0];
       const bool ok0 = has && ok0r, ok1 = has && ok1r;
       if (kA2S) {
         if (kImgA) {
           v[u][0] = ok0 ? *reinterpret_cast<const U*>(img + r0 + l.F) : U(0);
           v[u][1] = ok1 ? *reinterpret_cast<const U*>(img + r1 + l.F) : U(0);
+        } else if (kPh >= 0) {
+          v[u][0] = ok0 ? (U)sm_gather_ph<SZ, (kPh < 0 ? 0u : (uint32_t)kPh)>(img + r0 + l.F) : U(0);
+          v[u][1] = ok1 ? (U)sm_gather_ph<SZ, (kPh < 0 ? 0u : (uint32_t)kPh)>(img + r1 + l.F) : U(0);
         } else {
-          v[u][0] = ok0 ? (U)sm_gather(img + r0 + l.F, SZ, l.a_img) : U(0);
-          v[u][1] = ok1 ? (U)sm_gather(img + r1 + l.F, SZ, l.a_img) : U(0);
+          v[u][0] = ok0 ? (U)sm_gather(img + r0 + l.F, SZ, l.a_img & 0xFFu) : U(0);
+          v[u][1] = ok1 ? (U)sm_gather(img + r1 + l.F, SZ, l.a_img & 0xFFu) : U(0);
         }
       } else {
         const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
@@ -139,7 +194,7 @@ __device__ __forceinline__ void direct_class(const DirectParams& p, const Direct
     for (int u = 0; u < kU; ++u) {
       const uint32_t i = i0 + u * (kCons / 32);
       const bool has = i < c.k1;
-      const DirectLeaf& l = p.leaf[p.order[has ? i : c.k0]];
+      const DTab l = dtab(p)[has ? i : c.k0];
       const bool ok0 = has && ok0r, ok1 = has && ok1r;
       if (kA2S) {
         U* g = reinterpret_cast<U*>(l.gptr) + t0;
@@ -154,9 +209,13 @@ __device__ __forceinline__ void direct_class(const DirectParams& p, const Direct
         if (kImgA) {
           if (ok0) *reinterpret_cast<U*>(img + r0 + l.F) = v[u][0];
           if (ok1) *reinterpret_cast<U*>(img + r1 + l.F) = v[u][1];
+        } else if (kPh >= 0) {
+          constexpr uint32_t ph = kPh < 0 ? 0u : (uint32_t)kPh;
+          if (ok0) ScatterPh<SZ, ph, 0>::run(img + r0 + l.F, v[u][0]);
+          if (ok1) ScatterPh<SZ, ph, 0>::run(img + r1 + l.F, v[u][1]);
         } else {
-          if (ok0) sm_scatter(img + r0 + l.F, v[u][0], SZ, l.a_img);
-          if (ok1) sm_scatter(img + r1 + l.F, v[u][1], SZ, l.a_img);
+          if (ok0) sm_scatter(img + r0 + l.F, v[u][0], SZ, l.a_img & 0xFFu);
+          if (ok1) sm_scatter(img + r1 + l.F, v[u][1], SZ, l.a_img & 0xFFu);
         }
       }
     }
@@ -222,7 +281,7 @@ __device__ __forceinline__ void direct_class_async(const DirectParams& p, const 
     for (uint32_t g0 = c.k0 + 4 * warp; g0 < c.k1; g0 += 4 * (kCons / 32)) {
       const uint32_t i = g0 + sub;
       if (i >= c.k1) continue;
-      const DirectLeaf& l = p.leaf[p.order[i]];
+      const DTab l = dtab(p)[i];
       const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -236,7 +295,7 @@ __device__ __forceinline__ void direct_class_async(const DirectParams& p, const 
     return;
   }
   for (uint32_t i = c.k0 + warp; i < c.k1; i += kCons / 32) {
-    const DirectLeaf& l = p.leaf[p.order[i]];
+    const DTab l = dtab(p)[i];
     const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -253,6 +312,65 @@ __device__ __forceinline__ bool async_class(const DirectParams& p, const DirectC
   return p.async && (c.kind & 48) == 48 && (z == 4 || z == 8);
 }
 
+// SoA -> AoS, a misaligned 4- / 8-byte class of a fixed word phase: its
+// elements land by cp.async in an aligned staging area (T per leaf, after
+// the leaf table), and after the tile's wait they are scattered from there
+// into the image in compile-time pieces -- no register round trip through
+// global latency for them.
+__device__ __forceinline__ bool stage_class(const DirectParams& p, const DirectClass& c) {
+  const uint32_t z = c.kind & 15;
+  return p.stg_bytes && (c.kind & 96) == 96 && (z == 4 || z == 8);
+}
+
+__device__ __forceinline__ uint8_t* dstage(const DirectParams& p) {
+  return dsmem + kBars + (size_t)p.ns * p.stage + 16 + 16 * (size_t)p.K;
+}
+
+template <uint32_t SZ, bool kFull>
+__device__ __forceinline__ void direct_stage_in(const DirectParams& p, const DirectClass& c, uint64_t t0,
+                                                uint32_t nrec, int warp, int lane) {
+  typedef typename UT<SZ>::T U;
+  const uint32_t base = smem_u32(dstage(p));
+  for (uint32_t i = c.k0 + warp; i < c.k1; i += kCons / 32) {
+    const DTab l = dtab(p)[i];
+    const U* g = reinterpret_cast<const U*>(l.gptr) + t0;
+    const uint32_t st = base + (l.a_img >> 8);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t r = (uint32_t)lane + 32 * h;
+      if (kFull || r < nrec)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(st + r * SZ), "l"(g + r), "n"(SZ) : "memory");
+    }
+  }
+}
+
+template <uint32_t SZ, uint32_t PH, bool kFull>
+__device__ __forceinline__ void direct_stage_out(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                                 uint32_t nrec, int warp, int lane) {
+  typedef typename UT<SZ>::T U;
+  const uint8_t* stg = dstage(p);
+  for (uint32_t i = c.k0 + warp; i < c.k1; i += kCons / 32) {
+    const DTab l = dtab(p)[i];
+    const U* st = reinterpret_cast<const U*>(stg + (l.a_img >> 8));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t r = (uint32_t)lane + 32 * h;
+      if (kFull || r < nrec) ScatterPh<SZ, PH, 0>::run(img + r * p.S + l.F, st[r]);
+    }
+  }
+}
+
+template <uint32_t SZ, bool kFull>
+__device__ __forceinline__ void direct_stage_out_c(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                                   uint32_t nrec, int warp, int lane) {
+  switch ((c.kind >> 7) & 3) {
+    case 0: direct_stage_out<SZ, 0, kFull>(p, c, img, nrec, warp, lane); break;
+    case 1: direct_stage_out<SZ, 1, kFull>(p, c, img, nrec, warp, lane); break;
+    case 2: direct_stage_out<SZ, 2, kFull>(p, c, img, nrec, warp, lane); break;
+    default: direct_stage_out<SZ, 3, kFull>(p, c, img, nrec, warp, lane); break;
+  }
+}
+
 template <bool kA2S, uint32_t SZ, bool kFull>
 __device__ __forceinline__ void direct_class_a(const DirectParams& p, const DirectClass& c, uint8_t* img, uint64_t t0,
                                                uint32_t nrec, int warp, int lane) {
@@ -262,6 +380,14 @@ __device__ __forceinline__ void direct_class_a(const DirectParams& p, const Dire
     else
       direct_class_mix<kA2S, SZ, false, kFull>(p, c, img, t0, nrec, warp, lane);
     return;
+  }
+  if ((c.kind & 64) && (c.kind & 32)) {  // misaligned image leaf of a fixed word phase
+    switch ((c.kind >> 7) & 3) {
+      case 0: direct_class<kA2S, SZ, false, true, kFull, 0>(p, c, img, t0, nrec, warp, lane); return;
+      case 1: direct_class<kA2S, SZ, false, true, kFull, 1>(p, c, img, t0, nrec, warp, lane); return;
+      case 2: direct_class<kA2S, SZ, false, true, kFull, 2>(p, c, img, t0, nrec, warp, lane); return;
+      default: direct_class<kA2S, SZ, false, true, kFull, 3>(p, c, img, t0, nrec, warp, lane); return;
+    }
   }
   switch (c.kind & 48) {
     case 48: direct_class<kA2S, SZ, true, true, kFull>(p, c, img, t0, nrec, warp, lane); break;
@@ -278,6 +404,13 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
   if (!kA2S && p.async) {  // the cp.async classes first, then the register classes overlap them
     for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
       const DirectClass c = p.cls[ci];
+      if (stage_class(p, c)) {
+        if ((c.kind & 15) == 8)
+          direct_stage_in<8, kFull>(p, c, t0, nrec, warp, lane);
+        else
+          direct_stage_in<4, kFull>(p, c, t0, nrec, warp, lane);
+        continue;
+      }
       if (!async_class(p, c)) continue;
       if ((c.kind & 15) == 8)
         direct_class_async<8, kFull>(p, c, img, t0, nrec, warp, lane);
@@ -288,7 +421,7 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
   }
   for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
     const DirectClass c = p.cls[ci];
-    if (!kA2S && async_class(p, c)) continue;
+    if (!kA2S && (async_class(p, c) || stage_class(p, c))) continue;
     switch (c.kind & 15) {
       case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
       case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
@@ -296,11 +429,23 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
       default: direct_class_a<kA2S, 1, kFull>(p, c, img, t0, nrec, warp, lane); break;
     }
   }
+  if (!kA2S && p.stg_bytes) {  // the staged classes: wait for the tile's cp.asyncs, then scatter
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    cons_sync();
+    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
+      const DirectClass c = p.cls[ci];
+      if (!stage_class(p, c)) continue;
+      if ((c.kind & 15) == 8)
+        direct_stage_out_c<8, kFull>(p, c, img, nrec, warp, lane);
+      else
+        direct_stage_out_c<4, kFull>(p, c, img, nrec, warp, lane);
+    }
+  }
 }
 
 template <bool kA2S>
 __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_constant__ DirectParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* smem = dsmem;
   uint64_t* ready = reinterpret_cast<uint64_t*>(smem);  // A2S: full; S2A: dfull
   uint64_t* freed = ready + 8;                         // A2S: empty; S2A: dempty
   uint8_t* ring = smem + kBars;
@@ -308,6 +453,10 @@ __global__ void __launch_bounds__(kCons + 32, 3) k_permute_direct(const __grid_c
   if (!kA2S)  // destination padding bytes are never written: zero the ring once
     for (uint32_t o = 16 * tid; o < p.ns * p.stage; o += 16 * (kCons + 32))
       *reinterpret_cast<uint4*>(ring + o) = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = tid; i < p.K; i += kCons + 32) {
+    const DirectLeaf& l = p.leaf[p.order[i]];
+    const_cast<DTab*>(dtab(p))[i] = DTab{l.gptr, l.F, l.a_img | (l.stg << 8)};
+  }
   if (tid == 0) {
     for (uint32_t s = 0; s < p.ns; ++s) {
       mbar_init(&ready[s], 1);
@@ -402,7 +551,8 @@ int launch_permute_direct(const DirectParams& p, void* stream) {
   static LaunchCache cache[2][64];
   int dev = 0, per_sm = 1, sms = 148;
   cudaGetDevice(&dev);
-  const int smem = kBars + (int)(p.ns * p.stage) + 16;  // + slack: funnel reads of the last element
+  // + slack (funnel reads of the last element) + the leaf table + staging
+  const int smem = kBars + (int)(p.ns * p.stage) + 16 + 16 * (int)p.K + (int)p.stg_bytes;
   auto kern = p.a2s ? k_permute_direct<true> : k_permute_direct<false>;
   int e = prepare_kernel(kern, kCons + 32, smem, &cache[p.a2s ? 1 : 0][dev & 63], &per_sm);
   if (e) return e;

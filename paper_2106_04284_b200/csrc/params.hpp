@@ -270,7 +270,7 @@ struct DirectLeaf {
   uint16_t size;
   uint8_t a_img;     // alignment of every (r * S + F) in the AoS image (1, 2, 4, 8)
   uint8_t a_glob;    // alignment of every SoA element address
-  uint32_t pad_;
+  uint32_t stg;      // SoA -> AoS, staged class: offset of the leaf's T elements in the staging area
 };
 
 // Leaves of equal size and alignment classes, handled by one specialised loop:
@@ -287,7 +287,7 @@ struct DirectParams {
   uint32_t ns, stage;
   uint32_t mix;      // 1: aligned-image classes use the 4-leaves x 8-records warp mapping
   uint32_t async;    // SoA -> AoS: 4- / 8-byte classes aligned on both sides land by cp.async
-  uint32_t pad_;
+  uint32_t stg_bytes; // SoA -> AoS with async: staging area of the misaligned 4- / 8-byte (phase) classes
   uint64_t abase;    // AoS side: byte offset of record 0 in blob `ablob`
   uint32_t ablob;
   uint32_t n_gaps;   // AoS -> aligned SoA SB: padding between sub-arrays, zeroed by CTA 0

@@ -259,10 +259,15 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   const uint64_t S = A.B;
   if (S == 0 || A.L != 1) { *why = "AoS stride"; return false; }
   // measured on HEP100: AoS -> SoA wins for packed and aligned records (2.8 ->
-  // 3.5 TB/s; misaligned leaves are funnel-shifted out of aligned words);
-  // SoA -> AoS only for naturally aligned records (misaligned leaves would be
-  // scattered into shared memory in 1-2 byte pieces: 2.9 -> 2.0 TB/s)
-  if (mode != 2 && s2a)
+  // 5.2 TB/s packed; misaligned leaves are funnel-shifted out of aligned
+  // words); SoA -> AoS for naturally aligned records, and for packed ones
+  // only with the staged misaligned classes (2.92 -> 3.18 TB/s; scattered from
+  // registers in 1-2 byte pieces they lost: 2.9 -> 2.0)
+  // (with a record stride that is a multiple of 4 the misaligned 4- / 8-byte
+  // leaves are staged by cp.async and scattered in compile-time pieces)
+  const bool staging = s2a && S % 4 == 0 && env_u64("LLAMA_DIRECT_ASYNC", 1) && env_u64("LLAMA_DIRECT_PHASE", 1) &&
+                       env_u64("LLAMA_DIRECT_STAGING", 1);
+  if (mode != 2 && s2a && !staging)
     for (int k = 0; k < A.K(); ++k)
       if (A.F[k] % A.sizes[k] || S % A.sizes[k]) { *why = "packed AoS: the tile permute"; return false; }
   // T = 64 records per tile (two per lane); stages measured on HEP100: AoS ->
@@ -305,7 +310,12 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
     for (int k = 0; k < s.K(); ++k) idx[k] = k;
     auto kind = [&](int k) {
       const DirectLeaf& l = dp.leaf[k];
-      return (uint32_t)l.size | (l.a_img >= l.size ? 16u : 0u) | (l.a_glob >= l.size ? 32u : 0u);
+      uint32_t kd = (uint32_t)l.size | (l.a_img >= l.size ? 16u : 0u) | (l.a_glob >= l.size ? 32u : 0u);
+      // record stride a multiple of 4: a misaligned leaf sits at the same
+      // word phase F % 4 in every record (compile-time funnel shifts / pieces)
+      if (S % 4 == 0 && l.a_img < l.size && l.size >= 2 && env_u64("LLAMA_DIRECT_PHASE", 1))
+        kd |= 64u | ((l.F & 3u) << 7);
+      return kd;
     };
     std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return kind(x) < kind(y); });
     for (int i = 0; i < s.K(); ++i) {
@@ -317,6 +327,19 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
         dp.cls[dp.n_cls - 1].k1 = (uint16_t)(i + 1);
       }
     }
+  }
+  if (staging) {  // staging area of the misaligned (phase) 4- / 8-byte classes, T elements per leaf
+    uint64_t off = 0;
+    for (uint32_t ci = 0; ci < dp.n_cls; ++ci) {
+      const DirectClass& c = dp.cls[ci];
+      const uint32_t z = c.kind & 15;
+      if ((c.kind & 96) != 96 || (z != 4 && z != 8)) continue;
+      for (uint32_t i = c.k0; i < c.k1; ++i) {
+        dp.leaf[dp.order[i]].stg = (uint32_t)off;
+        off += align16(T * z);
+      }
+    }
+    dp.stg_bytes = (uint32_t)off;
   }
   if (a2s && d.has_padding()) {  // aligned SoA SB: the gaps between sub-arrays
     if (d.kind != LLAMA_SOA_SINGLE_BLOB) { *why = "padded destination"; return false; }
@@ -332,7 +355,7 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
     }
   }
   p->path = LLAMA_PATH_PERMUTE;
-  p->smem_bytes = (int)(128 + ns * stage + 16);
+  p->smem_bytes = (int)(128 + ns * stage + 16 + 16 * s.K() + dp.stg_bytes);
   return true;
 }
 

@@ -382,14 +382,16 @@ def test_one_and_mapping_c_sources(llama, oracle_mod, n):
 # ------------------------------------------------ direct AoS <-> SoA variant
 @pytest.mark.parametrize("schema_name", ["listing1", "particle7", "hep100"])
 @pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097])
-@pytest.mark.parametrize("use_async", ["1", "0"])
+@pytest.mark.parametrize("use_async", ["1", "0", "nostage"])
 def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async, monkeypatch):
     """The direct permute (AoS side through TMA, SoA side element-wise) for
     every AoS <-> SoA pair, forced for few-leaf records too (LLAMA_DIRECT=2):
     odd record strides exercise the byte-wise shared-memory accesses; SoA ->
-    AoS with the cp.async classes and with registers only."""
+    AoS with the cp.async classes (with and without the staged misaligned
+    classes) and with registers only."""
     monkeypatch.setenv("LLAMA_DIRECT", "2")
-    monkeypatch.setenv("LLAMA_DIRECT_ASYNC", use_async)
+    monkeypatch.setenv("LLAMA_DIRECT_ASYNC", "0" if use_async == "0" else "1")
+    monkeypatch.setenv("LLAMA_DIRECT_STAGING", "0" if use_async == "nostage" else "1")
     schema = W.SCHEMAS[schema_name]
     names = ["aos", "aos_aligned", "soa_mb", "soa_sb", "soa_sb_aligned"]
     for a in names:
@@ -407,7 +409,7 @@ def test_direct_chosen_for_hep(llama):
     assert llama.plan(m["aos_aligned"], m["soa_mb"])["direct"]
     assert llama.plan(m["soa_mb"], m["aos_aligned"])["direct"]
     assert llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: funnel-shifted gathers
-    assert not llama.plan(m["soa_mb"], m["aos"])["direct"]  # packed destination: the tile permute
+    assert llama.plan(m["soa_mb"], m["aos"])["direct"]  # packed destination: staged misaligned classes
     assert not llama.plan(m["aos"], m["aos_aligned"])["direct"]
 
 
