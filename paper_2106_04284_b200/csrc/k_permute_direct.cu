@@ -360,6 +360,43 @@ __device__ __forceinline__ void direct_stage_out(const DirectParams& p, const Di
   }
 }
 
+// SoA -> AoS, an image-aligned class of 1- / 2-byte leaves whose SoA runs
+// start 16-byte aligned (full tiles): each leaf's T * SZ-byte run lands in the
+// staging area as 16-byte cp.async chunks ((leaf, chunk) pairs spread over
+// all consumer threads), then moves into the image element by element.
+__device__ __forceinline__ bool chunk_class(const DirectParams& p, const DirectClass& c) {
+  return p.stg_bytes && (c.kind & 512);
+}
+
+template <uint32_t SZ>
+__device__ __forceinline__ void direct_chunk_in(const DirectParams& p, const DirectClass& c, uint64_t t0, int tid) {
+  constexpr uint32_t kCh = 64 * SZ / 16;  // chunks per leaf (T = 64)
+  const uint32_t base = smem_u32(dstage(p));
+  for (uint32_t x = tid; x < (c.k1 - c.k0) * kCh; x += kCons) {
+    const uint32_t i = c.k0 + x / kCh, ch = x % kCh;
+    const DTab l = dtab(p)[i];
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + (l.a_img >> 8) + 16 * ch),
+                 "l"(l.gptr + t0 * SZ + 16 * ch)
+                 : "memory");
+  }
+}
+
+template <uint32_t SZ>
+__device__ __forceinline__ void direct_chunk_out(const DirectParams& p, const DirectClass& c, uint8_t* img, int warp,
+                                                 int lane) {
+  typedef typename UT<SZ>::T U;
+  const uint8_t* stg = dstage(p);
+  for (uint32_t i = c.k0 + warp; i < c.k1; i += kCons / 32) {
+    const DTab l = dtab(p)[i];
+    const U* st = reinterpret_cast<const U*>(stg + (l.a_img >> 8));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t r = (uint32_t)lane + 32 * h;
+      *reinterpret_cast<U*>(img + r * p.S + l.F) = st[r];
+    }
+  }
+}
+
 template <uint32_t SZ, bool kFull>
 __device__ __forceinline__ void direct_stage_out_c(const DirectParams& p, const DirectClass& c, uint8_t* img,
                                                    uint32_t nrec, int warp, int lane) {
@@ -404,6 +441,13 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
   if (!kA2S && p.async) {  // the cp.async classes first, then the register classes overlap them
     for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
       const DirectClass c = p.cls[ci];
+      if (kFull && chunk_class(p, c)) {
+        if ((c.kind & 15) == 2)
+          direct_chunk_in<2>(p, c, t0, warp * 32 + lane);
+        else
+          direct_chunk_in<1>(p, c, t0, warp * 32 + lane);
+        continue;
+      }
       if (stage_class(p, c)) {
         if ((c.kind & 15) == 8)
           direct_stage_in<8, kFull>(p, c, t0, nrec, warp, lane);
@@ -421,7 +465,7 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
   }
   for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
     const DirectClass c = p.cls[ci];
-    if (!kA2S && (async_class(p, c) || stage_class(p, c))) continue;
+    if (!kA2S && (async_class(p, c) || stage_class(p, c) || (kFull && chunk_class(p, c)))) continue;
     switch (c.kind & 15) {
       case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
       case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
@@ -434,6 +478,13 @@ __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img,
     cons_sync();
     for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
       const DirectClass c = p.cls[ci];
+      if (kFull && chunk_class(p, c)) {
+        if ((c.kind & 15) == 2)
+          direct_chunk_out<2>(p, c, img, warp, lane);
+        else
+          direct_chunk_out<1>(p, c, img, warp, lane);
+        continue;
+      }
       if (!stage_class(p, c)) continue;
       if ((c.kind & 15) == 8)
         direct_stage_out_c<8, kFull>(p, c, img, nrec, warp, lane);

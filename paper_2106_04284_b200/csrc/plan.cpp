@@ -315,6 +315,13 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
       // word phase F % 4 in every record (compile-time funnel shifts / pieces)
       if (S % 4 == 0 && l.a_img < l.size && l.size >= 2 && env_u64("LLAMA_DIRECT_PHASE", 1))
         kd |= 64u | ((l.F & 3u) << 7);
+      // SoA -> AoS, image-aligned 1- / 2-byte leaf with 16-byte aligned SoA
+      // runs: staged as 16-byte cp.async chunks (full tiles)
+      // (measured: chunk-staging the aligned 4- / 8-byte classes too, instead
+      // of their element cp.asyncs into the image, lost 2-33%)
+      if (staging && l.size <= 2 && l.a_img >= l.size && l.gbase % 16 == 0 && (T * l.size) % 16 == 0 &&
+          env_u64("LLAMA_DIRECT_CHUNKS", 1))
+        kd |= 512u;
       return kd;
     };
     std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return kind(x) < kind(y); });
@@ -333,7 +340,7 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
     for (uint32_t ci = 0; ci < dp.n_cls; ++ci) {
       const DirectClass& c = dp.cls[ci];
       const uint32_t z = c.kind & 15;
-      if ((c.kind & 96) != 96 || (z != 4 && z != 8)) continue;
+      if (!(c.kind & 512) && ((c.kind & 96) != 96 || (z != 4 && z != 8))) continue;
       for (uint32_t i = c.k0; i < c.k1; ++i) {
         dp.leaf[dp.order[i]].stg = (uint32_t)off;
         off += align16(T * z);

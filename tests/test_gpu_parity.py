@@ -382,16 +382,18 @@ def test_one_and_mapping_c_sources(llama, oracle_mod, n):
 # ------------------------------------------------ direct AoS <-> SoA variant
 @pytest.mark.parametrize("schema_name", ["listing1", "particle7", "hep100"])
 @pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097])
-@pytest.mark.parametrize("use_async", ["1", "0", "nostage"])
+@pytest.mark.parametrize("use_async", ["1", "0", "nostage", "nochunk"])
 def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async, monkeypatch):
     """The direct permute (AoS side through TMA, SoA side element-wise) for
     every AoS <-> SoA pair, forced for few-leaf records too (LLAMA_DIRECT=2):
     odd record strides exercise the byte-wise shared-memory accesses; SoA ->
     AoS with the cp.async classes (with and without the staged misaligned
-    classes) and with registers only."""
+    classes and the 16-byte chunk-staged 1- / 2-byte classes) and with
+    registers only."""
     monkeypatch.setenv("LLAMA_DIRECT", "2")
     monkeypatch.setenv("LLAMA_DIRECT_ASYNC", "0" if use_async == "0" else "1")
     monkeypatch.setenv("LLAMA_DIRECT_STAGING", "0" if use_async == "nostage" else "1")
+    monkeypatch.setenv("LLAMA_DIRECT_CHUNKS", "0" if use_async == "nochunk" else "1")
     schema = W.SCHEMAS[schema_name]
     names = ["aos", "aos_aligned", "soa_mb", "soa_sb", "soa_sb_aligned"]
     for a in names:
