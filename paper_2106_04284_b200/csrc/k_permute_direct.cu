@@ -307,20 +307,12 @@ __device__ __forceinline__ void direct_class_async(const DirectParams& p, const 
   }
 }
 
-__device__ __forceinline__ bool async_class(const DirectParams& p, const DirectClass& c) {
-  const uint32_t z = c.kind & 15;
-  return p.async && (c.kind & 48) == 48 && (z == 4 || z == 8);
-}
 
 // SoA -> AoS, a misaligned 4- / 8-byte class of a fixed word phase: its
 // elements land by cp.async in an aligned staging area (T per leaf, after
 // the leaf table), and after the tile's wait they are scattered from there
 // into the image in compile-time pieces -- no register round trip through
 // global latency for them.
-__device__ __forceinline__ bool stage_class(const DirectParams& p, const DirectClass& c) {
-  const uint32_t z = c.kind & 15;
-  return p.stg_bytes && (c.kind & 96) == 96 && (z == 4 || z == 8);
-}
 
 __device__ __forceinline__ uint8_t* dstage(const DirectParams& p) {
   return dsmem + kBars + (size_t)p.ns * p.stage + 16 + 16 * (size_t)p.K;
@@ -364,9 +356,6 @@ __device__ __forceinline__ void direct_stage_out(const DirectParams& p, const Di
 // start 16-byte aligned (full tiles): each leaf's T * SZ-byte run lands in the
 // staging area as 16-byte cp.async chunks ((leaf, chunk) pairs spread over
 // all consumer threads), then moves into the image element by element.
-__device__ __forceinline__ bool chunk_class(const DirectParams& p, const DirectClass& c) {
-  return p.stg_bytes && (c.kind & 512);
-}
 
 template <uint32_t SZ>
 __device__ __forceinline__ void direct_chunk_in(const DirectParams& p, const DirectClass& c, uint64_t t0, int tid) {
@@ -434,58 +423,74 @@ __device__ __forceinline__ void direct_class_a(const DirectParams& p, const Dire
   }
 }
 
-// full tiles (every record present) and the partial last tile
+// one class through registers (the size-specialised loops above)
+template <bool kA2S, bool kFull>
+__device__ __forceinline__ void direct_class_regs(const DirectParams& p, const DirectClass& c, uint8_t* img,
+                                                  uint64_t t0, uint32_t nrec, int warp, int lane) {
+  switch (c.kind & 15) {
+    case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    case 2: direct_class_a<kA2S, 2, kFull>(p, c, img, t0, nrec, warp, lane); break;
+    default: direct_class_a<kA2S, 1, kFull>(p, c, img, t0, nrec, warp, lane); break;
+  }
+}
+
+// full tiles (every record present) and the partial last tile.  SoA -> AoS
+// with cp.async: the planner orders the classes [0, e0) chunk-staged, [e0, e1)
+// staged, [e1, e2) cp.async into the image, [e2, n) registers (partial tiles
+// move the chunk-staged classes through registers: their runs would overrun).
 template <bool kA2S, bool kFull>
 __device__ __forceinline__ void direct_tile(const DirectParams& p, uint8_t* img, uint64_t t0, uint32_t nrec, int warp,
                                             int lane) {
-  if (!kA2S && p.async) {  // the cp.async classes first, then the register classes overlap them
-    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
-      const DirectClass c = p.cls[ci];
-      if (kFull && chunk_class(p, c)) {
+  const bool as = !kA2S && p.async;
+  const uint32_t e0 = as ? p.cat_end[0] : 0, e1 = as ? p.cat_end[1] : 0, e2 = as ? p.cat_end[2] : 0;
+  if (as) {  // the cp.async classes first, then the register classes overlap them
+    if (kFull)
+      for (uint32_t ci = 0; ci < e0; ++ci) {
+        const DirectClass c = p.cls[ci];
         if ((c.kind & 15) == 2)
           direct_chunk_in<2>(p, c, t0, warp * 32 + lane);
         else
           direct_chunk_in<1>(p, c, t0, warp * 32 + lane);
-        continue;
       }
-      if (stage_class(p, c)) {
-        if ((c.kind & 15) == 8)
-          direct_stage_in<8, kFull>(p, c, t0, nrec, warp, lane);
-        else
-          direct_stage_in<4, kFull>(p, c, t0, nrec, warp, lane);
-        continue;
-      }
-      if (!async_class(p, c)) continue;
+    for (uint32_t ci = e0; ci < e1; ++ci) {
+      const DirectClass c = p.cls[ci];
+      if ((c.kind & 15) == 8)
+        direct_stage_in<8, kFull>(p, c, t0, nrec, warp, lane);
+      else
+        direct_stage_in<4, kFull>(p, c, t0, nrec, warp, lane);
+    }
+    for (uint32_t ci = e1; ci < e2; ++ci) {
+      const DirectClass c = p.cls[ci];
       if ((c.kind & 15) == 8)
         direct_class_async<8, kFull>(p, c, img, t0, nrec, warp, lane);
       else
         direct_class_async<4, kFull>(p, c, img, t0, nrec, warp, lane);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+    if (!kFull)
+      for (uint32_t ci = 0; ci < e0; ++ci) {
+        const DirectClass c = p.cls[ci];  // (a copy: its fields stay in registers)
+        direct_class_regs<kA2S, kFull>(p, c, img, t0, nrec, warp, lane);
+      }
   }
-  for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
+  for (uint32_t ci = e2; ci < p.n_cls; ++ci) {
     const DirectClass c = p.cls[ci];
-    if (!kA2S && (async_class(p, c) || stage_class(p, c) || (kFull && chunk_class(p, c)))) continue;
-    switch (c.kind & 15) {
-      case 8: direct_class_a<kA2S, 8, kFull>(p, c, img, t0, nrec, warp, lane); break;
-      case 4: direct_class_a<kA2S, 4, kFull>(p, c, img, t0, nrec, warp, lane); break;
-      case 2: direct_class_a<kA2S, 2, kFull>(p, c, img, t0, nrec, warp, lane); break;
-      default: direct_class_a<kA2S, 1, kFull>(p, c, img, t0, nrec, warp, lane); break;
-    }
+    direct_class_regs<kA2S, kFull>(p, c, img, t0, nrec, warp, lane);
   }
-  if (!kA2S && p.stg_bytes) {  // the staged classes: wait for the tile's cp.asyncs, then scatter
+  if (as && e1 > 0) {  // the staged classes: wait for the tile's cp.asyncs, then copy out
     asm volatile("cp.async.wait_all;" ::: "memory");
     cons_sync();
-    for (uint32_t ci = 0; ci < p.n_cls; ++ci) {
-      const DirectClass c = p.cls[ci];
-      if (kFull && chunk_class(p, c)) {
+    if (kFull)
+      for (uint32_t ci = 0; ci < e0; ++ci) {
+        const DirectClass c = p.cls[ci];
         if ((c.kind & 15) == 2)
           direct_chunk_out<2>(p, c, img, warp, lane);
         else
           direct_chunk_out<1>(p, c, img, warp, lane);
-        continue;
       }
-      if (!stage_class(p, c)) continue;
+    for (uint32_t ci = e0; ci < e1; ++ci) {
+      const DirectClass c = p.cls[ci];
       if ((c.kind & 15) == 8)
         direct_stage_out_c<8, kFull>(p, c, img, nrec, warp, lane);
       else

@@ -296,6 +296,7 @@ struct DirectParams {
   uint64_t gap_off[kMaxLeaves];
   DirectLeaf leaf[kMaxLeaves];
   uint32_t n_cls;
+  uint32_t cat_end[3];  // SoA -> AoS with async: class ranges [0, e0) chunk-staged, [e0, e1) staged, [e1, e2) cp.async
   DirectClass cls[16];
   uint16_t order[kMaxLeaves];  // leaf ids grouped by class
   uint8_t* blobs[2][kMaxBlobs];

@@ -324,7 +324,21 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
         kd |= 512u;
       return kd;
     };
-    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return kind(x) < kind(y); });
+    // SoA -> AoS with cp.async: classes ordered by how the kernel moves them
+    // (k_permute_direct.cu direct_tile): 0 chunk-staged, 1 staged, 2 cp.async
+    // into the image, 3 registers; each pass walks its own class range
+    const bool use_async = !a2s && env_u64("LLAMA_DIRECT_ASYNC", 1);
+    auto cat = [&](int k) -> uint32_t {
+      const uint32_t kd = kind(k), z = kd & 15;
+      if (!use_async) return 3;
+      if (kd & 512) return 0;
+      if (staging && (kd & 96) == 96 && (z == 4 || z == 8)) return 1;
+      if ((kd & 48) == 48 && (z == 4 || z == 8)) return 2;
+      return 3;
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) {
+      return cat(x) != cat(y) ? cat(x) < cat(y) : kind(x) < kind(y);
+    });
     for (int i = 0; i < s.K(); ++i) {
       dp.order[i] = (uint16_t)idx[i];
       if (i == 0 || kind(idx[i]) != kind(idx[i - 1])) {
@@ -333,6 +347,11 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
       } else {
         dp.cls[dp.n_cls - 1].k1 = (uint16_t)(i + 1);
       }
+    }
+    for (uint32_t c = 0; c < 3; ++c) {
+      dp.cat_end[c] = 0;
+      for (uint32_t ci = 0; ci < dp.n_cls; ++ci)
+        if (cat(idx[dp.cls[ci].k0]) <= c) dp.cat_end[c] = ci + 1;
     }
   }
   if (staging) {  // staging area of the misaligned (phase) 4- / 8-byte classes, T elements per leaf
