@@ -287,6 +287,17 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
         e[j] = tile_slot(dy, dx);
         f[j] = (uint64_t)q * p.sS;
       }
+      if (kAligned && kLin && p.tlinear == 4 && p.raw_typed) {  // one 4-byte size: typed, 32-bit offsets
+        uint32_t fr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fr[j] = (uint32_t)f[j];
+        for (int k = 0; k < p.K; ++k) {
+          const uint32_t F = (uint32_t)p.sl[k].F;
+          uint32_t* tk = reinterpret_cast<uint32_t*>(tsm + p.tbase[k]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tk[e[j]] = *reinterpret_cast<const uint32_t*>(raw + fr[j] + F);
+        }
+      } else
       for (int k = 0; k < p.K; ++k) {
         const uint32_t size = p.sl[k].size, F = (uint32_t)p.sl[k].F;
         uint8_t* tk = tsm + p.tbase[k];
@@ -351,6 +362,17 @@ __global__ void __launch_bounds__(kThreads) k_transpose2d(const __grid_constant_
         e[j] = tile_slot(dy, dx);
         f[j] = (uint64_t)q * p.dS;
       }
+      if (kAligned && kLin && p.tlinear == 4 && p.raw_typed) {
+        uint32_t fr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fr[j] = (uint32_t)f[j];
+        for (int k = 0; k < p.K; ++k) {
+          const uint32_t F = (uint32_t)p.dl[k].F;
+          const uint32_t* tk = reinterpret_cast<const uint32_t*>(tsm + p.tbase[k]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) *reinterpret_cast<uint32_t*>(raw + fr[j] + F) = tk[e[j]];
+        }
+      } else
       for (int k = 0; k < p.K; ++k) {
         const uint32_t size = p.dl[k].size, F = (uint32_t)p.dl[k].F;
         const uint8_t* tk = tsm + p.tbase[k];

@@ -76,6 +76,7 @@ struct NaiveParams {
   uint32_t sS, dS;             // TRANSPOSE: record strides of the raw sides
   uint32_t dpad;               // TRANSPOSE: the raw destination has padding bytes (zero the buffer)
   uint32_t linoff;             // TRANSPOSE, linear sides: shared-memory offset of the per-CTA leaf table
+  uint32_t raw_typed;          // TRANSPOSE: raw passes as typed 4-byte moves when every leaf is 4 bytes
   DevLeaf sl[kMaxLeaves];
   DevLeaf dl[kMaxLeaves];
   const uint8_t* sb[kMaxBlobs];

@@ -115,6 +115,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
     for (int k = 0; k < m->K(); ++k)
       if (!((m->Lk[k] == 1 && m->Bk[k] < (1ull << 32)) || m->Lk[k] >= m->N)) n.tlinear = 0;
   if (!env_u64("LLAMA_TRANSPOSE_LINEAR", 1)) n.tlinear = 0;
+  n.raw_typed = (uint32_t)env_u64("LLAMA_TRANSPOSE_RAW_TYPED", 1);
   if (n.tlinear) {  // one leaf size of 4 or 8 bytes: the two-leaf pass (k_simple.cu lin_tile_fixed)
     const uint64_t z = s.sizes[0];
     bool same = (z == 4 || z == 8) && env_u64("LLAMA_TRANSPOSE_FIXED", 1);

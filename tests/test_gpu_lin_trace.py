@@ -136,6 +136,7 @@ def test_raw_aos_tiles(llama, oracle_mod, lins):
 
 @pytest.mark.parametrize("knobs", [{"LLAMA_TRANSPOSE_LINEAR": "0"}, {"LLAMA_TRANSPOSE_RAW1": "0"},
                                    {"LLAMA_TRANSPOSE_FIXED": "0"}, {"LLAMA_TRANSPOSE_TABLE": "0"},
+                                   {"LLAMA_TRANSPOSE_RAW_TYPED": "0"},
                                    {"LLAMA_TRANSPOSE_RAW": "0"}, {}])
 def test_transpose_variants(llama, oracle_mod, monkeypatch, knobs):
     """Every k_transpose2d instantiation: linear sides (one multiply-add per
