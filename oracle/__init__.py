@@ -31,7 +31,7 @@ def build(force=False):
         return _LIB
     tmp = _LIB + f".tmp{os.getpid()}"
     subprocess.check_call(["gcc", "-O3", "-std=c11", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
-                           "-Wall", "-Wextra", "-o", tmp, _SRC])
+                           "-Wall", "-Wextra", "-o", tmp, _SRC, "-lm"])
     os.replace(tmp, _LIB)
     return _LIB
 
@@ -262,7 +262,7 @@ def copy_range(src, src_blobs, src_base, dst, dst_blobs, dst_base, i0, i1):
 
 def nbody_move(m, blobs, dt, pos=(0, 1, 2), vel=(3, 4, 5), i0=0, i1=None):
     """n-body move (Listing P:643-645) in place on m's blobs: Pos += Vel * dt
-    in f32 (two roundings).  Default leaves: Particle7's Pos.X..Z, Vel.X..Z."""
+    in f32 (one rounding: fmaf, reading #25).  Default leaves: Particle7's Pos.X..Z, Vel.X..Z."""
     if i1 is None:
         i1 = m.record_count
     p3 = (ctypes.c_int32 * 3)(*pos)

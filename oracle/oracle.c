@@ -4,6 +4,7 @@
  */
 #include "oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -452,9 +453,12 @@ int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
 }
 
 /* Listing P:643-645: particles(i)(Pos{}) += particles(i)(Vel{}) * TIMESTEP, per
- * component, FP = float.  Two roundings: t = v * dt, then p + t
- * (reading #25; the library builds this file with -ffp-contract=off so the
- * compiler cannot fuse them). */
+ * component, FP = float.  ONE rounding: p + v * dt as a fused
+ * multiply-add (reading #25): the paper built its CPU n-body with -ffast-math
+ * -mfma and its GPU n-body with nvcc --use_fast_math, both of
+ * which contract the multiply-add.  C99 fmaf is correctly rounded on every
+ * host (the file is built with -ffp-contract=off, so no other expression is
+ * fused). */
 int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int32_t* pos, const int32_t* vel,
                       float dt, int64_t i0, int64_t i1) {
   if (oracle_validate(m)) return -1;
@@ -475,8 +479,7 @@ int oracle_nbody_move(const oracle_mapping* m, uint8_t* const* blobs, const int3
       float p, v;
       memcpy(&p, blobs[bp] + op, 4);
       memcpy(&v, blobs[bv] + ov, 4);
-      float t = v * dt;
-      p = p + t;
+      p = fmaf(v, dt, p);
       memcpy(blobs[bp] + op, &p, 4);
     }
   }

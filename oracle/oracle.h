@@ -119,7 +119,7 @@ int oracle_copy(const oracle_mapping* src, const uint8_t* const* src_blobs,
 /* n-body move (Listing P:643-645, §4.1), FP = float
  * (P:618): for every particle i in [i0, i1) and c in {X, Y, Z}
  *   Pos_c(i) = Pos_c(i) + Vel_c(i) * dt
- * in f32 with two roundings (the product, then the sum; DESIGN.md reading
+ * in f32 with one rounding (a fused multiply-add, fmaf; DESIGN.md reading
  * #25), reading and writing through the oracle's own address function.
  * pos[3] / vel[3] are the leaf indices of Pos.{X,Y,Z} / Vel.{X,Y,Z}; those
  * leaves must be 4 bytes.  Every other byte is left as it is.

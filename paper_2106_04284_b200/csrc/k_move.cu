@@ -1,6 +1,7 @@
 // k_move.cu -- the n-body move (Listing P:643-645):
-//   Pos_c(i) = Pos_c(i) + Vel_c(i) * dt,  c in {X, Y, Z}, f32, two roundings
-// (reading #25: __fmul_rn / __fadd_rn keep nvcc from fusing them).
+//   Pos_c(i) = Pos_c(i) + Vel_c(i) * dt,  c in {X, Y, Z}, f32, one rounding
+// (reading #25: a fused multiply-add, __fmaf_rn, as the paper's builds with
+// -ffast-math -mfma / nvcc --use_fast_math contracted it).
 //
 // Kernels, one per layout family:
 //   k_move_generic  thread per particle through the per-leaf normal form (any mapping)
@@ -20,7 +21,7 @@ namespace llb {
 namespace {
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ float move1(float x, float v, float dt) { return __fadd_rn(x, __fmul_rn(v, dt)); }
+__device__ __forceinline__ float move1(float x, float v, float dt) { return __fmaf_rn(v, dt, x); }
 
 __device__ __forceinline__ float load_f32(const uint8_t* a, bool aligned) {
   if (aligned) return *reinterpret_cast<const float*>(a);

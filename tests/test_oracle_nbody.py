@@ -1,6 +1,10 @@
-"""Pins of the oracle's n-body move (Listing P:643-645): numpy's own
-f32 arithmetic on the columns, closed forms, the two-roundings reading (#25),
-untouched bytes, and layout commutation."""
+"""Pins of the oracle's n-body move (Listing P:643-645): the exact
+value p + v*dt rounded ONCE to f32 (reading #25: the paper's builds contract
+the multiply-add, -ffast-math -mfma P:593, nvcc --use_fast_math P:597),
+computed here in exact rational arithmetic; closed forms, untouched bytes,
+and layout commutation."""
+from fractions import Fraction
+
 import numpy as np
 import pytest
 
@@ -22,22 +26,53 @@ def _values(oracle, m, blobs):
     return np.frombuffer(oracle.copy(m, blobs, aos)[0].tobytes(), np.float32).reshape(-1, 7)
 
 
+def round_f32(q):
+    """The f32 nearest to the rational q, ties to even (IEEE 754 round to
+    nearest), decided exactly: candidates around float(q), compared as
+    Fractions."""
+    f = np.float32(float(q))
+    cands = {f, np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))}
+    cands = [c for c in cands if np.isfinite(c)]
+    best = min(abs(Fraction(float(c)) - q) for c in cands)
+    near = [c for c in cands if abs(Fraction(float(c)) - q) == best]
+    if len(near) > 1:  # a tie: the even significand
+        near = [c for c in near if (int(np.array(c, np.float32).view(np.uint32)) & 1) == 0]
+    return np.float32(near[0])
+
+
+def fused_ref(p, v, dt):
+    """p + v*dt, exact, then one rounding to f32."""
+    return round_f32(Fraction(float(p)) + Fraction(float(v)) * Fraction(float(dt)))
+
+
+def test_round_f32_helper():
+    # exact values stay; halfway cases go to the even neighbour
+    assert round_f32(Fraction(3, 4)) == np.float32(0.75)
+    one_up = np.nextafter(np.float32(1), np.float32(2))
+    assert round_f32(Fraction(1) + Fraction(1, 2 ** 24)) == np.float32(1)  # tie -> even (1.0)
+    assert round_f32(Fraction(1) + Fraction(3, 2 ** 24)) == np.nextafter(one_up, np.float32(2))  # tie -> even
+    assert round_f32(Fraction(1) + Fraction(1, 2 ** 23) - Fraction(1, 2 ** 40)) == one_up
+
+
 @pytest.mark.parametrize("name", SPECS)
 @pytest.mark.parametrize("n", [1, 33, 1000])
-def test_move_equals_numpy_f32(oracle_mod, name, n):
+def test_move_equals_exact_single_rounding(oracle_mod, name, n):
     vals = W.particle_values(n, seed=42)
     m, blobs = _view(oracle_mod, name, n, vals)
     oracle_mod.nbody_move(m, blobs, float(DT))
     got = _values(oracle_mod, m, blobs)
     exp = vals.copy()
-    exp[:, 0:3] = vals[:, 0:3] + vals[:, 3:6] * DT  # numpy f32: product rounded, then the sum
+    for i in range(n):
+        for c in range(3):
+            exp[i, c] = fused_ref(vals[i, c], vals[i, 3 + c], DT)
     assert got.tobytes() == exp.tobytes()
 
 
-def test_two_roundings_reading(oracle_mod):
-    """Reading #25: t = v*dt rounded to f32, then p + t rounded; a fused
-    multiply-add would keep the 2^-24 term: (1 + 2^-12)^2 - 1 = 2^-11 + 2^-24
-    exactly, and the product alone rounds (tie to even) to 1 + 2^-11."""
+def test_single_rounding_reading(oracle_mod):
+    """Reading #25: one rounding (fused multiply-add, P:593 -ffast-math -mfma,
+    P:597 --use_fast_math).  (1 + 2^-12)^2 - 1 = 2^-11 + 2^-24 exactly and is
+    representable; two roundings would lose the 2^-24 term (the product alone
+    rounds, tie to even, to 1 + 2^-11)."""
     e = np.float32(1 + 2.0 ** -12)
     vals = np.zeros((1, 7), np.float32)
     vals[0, 0] = -1.0
@@ -45,9 +80,9 @@ def test_two_roundings_reading(oracle_mod):
     m, blobs = _view(oracle_mod, "soa_mb", 1, vals)
     oracle_mod.nbody_move(m, blobs, float(e))
     got = _values(oracle_mod, m, blobs)[0, 0]
-    assert got == np.float32(2.0 ** -11)                 # two roundings
-    assert got != np.float32(2.0 ** -11 + 2.0 ** -24)    # what fmaf would give (representable)
     assert float(np.float32(2.0 ** -11 + 2.0 ** -24)) == 2.0 ** -11 + 2.0 ** -24
+    assert got == np.float32(2.0 ** -11 + 2.0 ** -24)    # one rounding (exact here)
+    assert got != np.float32(2.0 ** -11)                 # what two roundings would give
 
 
 def test_closed_forms(oracle_mod):
