@@ -11,8 +11,10 @@
  * reference texts of the paper).
  *
  * Conventions for every function:
- *   - Thread safety: all functions are thread-safe. Mappings are immutable
- *     after creation and may be shared between threads and devices.
+ *   - Thread safety: all functions are thread-safe (plan and launch caches
+ *     are mutex-protected), except that one llama_stager runs one staged call
+ *     at a time.  Mappings are immutable after creation and may be shared
+ *     between threads and devices.
  *   - Ownership: the library owns llama_mapping objects (create/destroy).  The
  *     caller owns all blob memory ("LLAMA ... function[s] orthogonally to
  *     memory allocation"); the library never allocates or frees blobs.  Arrays
@@ -212,9 +214,44 @@ typedef enum {
                               shared memory, read in source and written in destination storage order */
 } llama_path;
 
+/* Tuning knobs: explicit overrides of the planner's measured defaults (for
+ * sweeps and ablations).  The library never reads
+ * the environment: a plan depends only on the two mappings and the options,
+ * and the plan cache keys on every knob value. */
+typedef enum {
+  LLAMA_KNOB_TILE_BYTES = 0,   /* PERMUTE: src + dst image bytes per tile (64 KB small records, 48 KB wide) */
+  LLAMA_KNOB_SMEM_BUDGET,      /* PERMUTE: shared memory per CTA the ring may use (230 KB / 112 KB) */
+  LLAMA_KNOB_STAGES,           /* PERMUTE: source stages 2..4 (4 small records, 2 wide) */
+  LLAMA_KNOB_DST_BUFS,         /* PERMUTE: destination buffers 2..4 (3 small records, 2 wide) */
+  LLAMA_KNOB_WS_ORDER,         /* PERMUTE: producer order 0 stores first / 1 release first / 2 refill first (2) */
+  LLAMA_KNOB_NO_TMA,           /* PERMUTE: 1 = LSU segment copies (0) */
+  LLAMA_KNOB_PERMUTE_V1,       /* PERMUTE: 1 = barrier-synchronised kernel (0) */
+  LLAMA_KNOB_NO_PDL,           /* PERMUTE: 1 = no programmatic dependent launch (0) */
+  LLAMA_KNOB_WORD_MODE,        /* PERMUTE: AoS <-> AoS word mode for wide records (1) */
+  LLAMA_KNOB_DIRECT,           /* PERMUTE: direct AoS <-> SoA variant: 0 off, 1 many leaves, 2 any leaf count (1) */
+  LLAMA_KNOB_DIRECT_STAGES,    /* direct: ring stages (3 AoS -> SoA, 2 SoA -> AoS) */
+  LLAMA_KNOB_DIRECT_ASYNC,     /* direct SoA -> AoS: aligned 4- / 8-byte classes by cp.async (1) */
+  LLAMA_KNOB_DIRECT_PHASE,     /* direct: compile-time word phases of misaligned classes (1) */
+  LLAMA_KNOB_DIRECT_STAGING,   /* direct SoA -> AoS: misaligned 4- / 8-byte classes staged by cp.async (1) */
+  LLAMA_KNOB_DIRECT_CHUNKS,    /* direct SoA -> AoS: 1- / 2-byte classes staged as 16-byte chunks (1) */
+  LLAMA_KNOB_DIRECT_MIX,       /* direct: 4 leaves x 8 records per warp access for even word strides (1) */
+  LLAMA_KNOB_BULK_CHUNK,       /* BLOBCOPY: TMA chunk bytes (65536) */
+  LLAMA_KNOB_BULK_STAGES,      /* BLOBCOPY: TMA ring stages (3) */
+  LLAMA_KNOB_BLOBCOPY_LSU,     /* BLOBCOPY: 1 = 16-byte LSU vector copy instead of TMA (0) */
+  LLAMA_KNOB_TRANSPOSE_RAW,    /* TRANSPOSE: raw 16-byte AoS tiles (1) */
+  LLAMA_KNOB_TRANSPOSE_LINEAR, /* TRANSPOSE: linear-side element addressing (1) */
+  LLAMA_KNOB_TRANSPOSE_RAW1,   /* TRANSPOSE: one raw AoS side next to an element-wise side (1) */
+  LLAMA_KNOB_TRANSPOSE_FIXED,  /* TRANSPOSE: two-leaf load pass for one 4- / 8-byte leaf size (1) */
+  LLAMA_KNOB_TRANSPOSE_TABLE,  /* TRANSPOSE: per-CTA shared-memory leaf table (1) */
+  LLAMA_KNOB_TRANSPOSE_RAW_TYPED, /* TRANSPOSE: typed 4-byte raw passes (1) */
+  LLAMA_KNOB_COUNT
+} llama_knob;
+
 typedef struct {
   llama_path path;      /* forced path; UNSUPPORTED if not applicable to the pair */
   int32_t tile_records; /* PERMUTE only: records per tile, 0 = planner's choice */
+  const int64_t* knobs; /* NULL = all defaults, else LLAMA_KNOB_COUNT values (< 0 = that knob's default);
+                           read during the call only */
 } llama_copy_options;
 
 /* llama_copy with options (NULL = defaults = llama_copy). */
@@ -289,7 +326,9 @@ llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llam
  * n-body move (Listing P:643-645, §4.1, §4.2
  * P:698-743): in place on one view, for every particle i and c in {X,Y,Z}
  *     Pos_c(i) = Pos_c(i) + Vel_c(i) * dt
- * in f32 with two roundings (product, then sum; reading #25).
+ * in f32 with one rounding (fused multiply-add, as the paper's -ffast-math
+ * -mfma / --use_fast_math builds contracted it; DESIGN.md
+ * reading #25).
  * pos_leaves[3] / vel_leaves[3]: leaf indices (DFS order) of Pos.{X,Y,Z} and
  * Vel.{X,Y,Z}; all six must be 4-byte leaves (f32).  Only Pos bytes change
  * value (the AoS kernel rewrites whole records with their own bytes).
@@ -303,7 +342,10 @@ llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llam
  * Errors: INVALID_ARGUMENT (NULL, bad leaf index, non-4-byte leaf, a leaf
  * listed twice), UNSUPPORTED (forced path not applicable; a mapping that maps
  * several particles onto one place), ALIGNMENT, CUDA. */
-typedef enum { LLAMA_MOVE_AUTO = 0, LLAMA_MOVE_GENERIC = 1, LLAMA_MOVE_RUNS = 2, LLAMA_MOVE_AOS = 3 } llama_move_path;
+typedef enum {
+  LLAMA_MOVE_AUTO = 0, LLAMA_MOVE_GENERIC = 1, LLAMA_MOVE_RUNS = 2, LLAMA_MOVE_AOS = 3,
+  LLAMA_MOVE_AOS_LSU = 4 /* as AOS, through the warp-staged LSU kernel instead of the TMA ring (comparison) */
+} llama_move_path;
 llama_status llama_nbody_move(const llama_mapping* m, void* const* blobs, const int32_t* pos_leaves,
                               const int32_t* vel_leaves, float dt, void* stream);
 /* The same with a forced path (AUTO = planner's choice); *path_used (may be

@@ -41,7 +41,7 @@ EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_ma
            "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_copy_staged_batch",
            "llama_nbody_move_staged", "llama_nbody_move",
            "llama_nbody_move_ex"]
-MOVE_PATHS = {"auto": 0, "generic": 1, "runs": 2, "aos": 3}
+MOVE_PATHS = {"auto": 0, "generic": 1, "runs": 2, "aos": 3, "aos_lsu": 4}
 MOVE_PATH_NAMES = {v: k for k, v in MOVE_PATHS.items()}
 
 
@@ -59,7 +59,15 @@ class _Desc(ctypes.Structure):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32)]
+    _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32),
+                ("knobs", ctypes.POINTER(ctypes.c_int64))]
+
+
+# llama_knob (include/llama_b200.h): explicit overrides of the planner's defaults
+KNOBS = ["tile_bytes", "smem_budget", "stages", "dst_bufs", "ws_order", "no_tma", "permute_v1", "no_pdl",
+         "word_mode", "direct", "direct_stages", "direct_async", "direct_phase", "direct_staging",
+         "direct_chunks", "direct_mix", "bulk_chunk", "bulk_stages", "blobcopy_lsu", "transpose_raw",
+         "transpose_linear", "transpose_raw1", "transpose_fixed", "transpose_table", "transpose_raw_typed"]
 
 
 class _PlanInfo(ctypes.Structure):
@@ -70,8 +78,8 @@ class _PlanInfo(ctypes.Structure):
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
-        from . import _build
+    from . import _build
+    if not _build.up_to_date():  # missing, or built from other sources: rebuild (fails loudly)
         _build.build()
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.POINTER
@@ -331,16 +339,24 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _options(path, tile_records):
-    return _Options(PATHS[path or "auto"], int(tile_records))
+def _options(path, tile_records, knobs=None):
+    opt = _Options(PATHS[path or "auto"], int(tile_records), None)
+    if knobs:
+        vals = [-1] * len(KNOBS)
+        for k, v in knobs.items():
+            vals[KNOBS.index(k)] = int(v)
+        opt._keep = (ctypes.c_int64 * len(KNOBS))(*vals)
+        opt.knobs = opt._keep
+    return opt
 
 
-def copy(src_map, src_blobs, dst_map, dst_blobs, stream=None, path=None, tile_records=0):
+def copy(src_map, src_blobs, dst_map, dst_blobs, stream=None, path=None, tile_records=0, knobs=None):
     """The layout-aware copy (llama_copy / llama_copy_ex), enqueued on `stream`
-    (default: torch's current stream)."""
+    (default: torch's current stream).  knobs: {name: value} overrides of the
+    planner's tuning defaults (KNOBS)."""
     s = _ptrs(src_blobs, src_map.blob_sizes(), "src_blobs")
     d = _ptrs(dst_blobs, dst_map.blob_sizes(), "dst_blobs")
-    opt = _options(path, tile_records)
+    opt = _options(path, tile_records, knobs)
     _check(_lib.llama_copy_ex(src_map.handle, s, dst_map.handle, d, _stream(stream), ctypes.byref(opt)))
 
 
@@ -366,10 +382,10 @@ def copy_staged_batch(stager, copies, stream=None):
     db = (vp * n)(*[ctypes.cast(k[1], vp) for k in keep])
     _check(_lib.llama_copy_staged_batch(stager.handle, n, sm, sb, dm, db, _stream(stream)))
 
-def plan(src_map, dst_map, path=None, tile_records=0):
+def plan(src_map, dst_map, path=None, tile_records=0, knobs=None):
     """The planner's decision for a pair (no device work)."""
     info = _PlanInfo()
-    opt = _options(path, tile_records)
+    opt = _options(path, tile_records, knobs)
     _check(_lib.llama_plan(src_map.handle, dst_map.handle, ctypes.byref(opt), ctypes.byref(info)))
     return {"path": PATH_NAMES[info.path], "tile_records": info.tile_records, "smem_bytes": info.smem_bytes,
             "moves": info.moves, "tma": bool(info.tma), "src_bytes": int(info.src_bytes),

@@ -2,15 +2,18 @@
 extension machinery): every .cu/.cpp under csrc/ -> one shared library with a
 plain C ABI (include/llama_b200.h)."""
 import glob
+import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libllama_b200.so")
+STAMP = LIB + ".stamp"  # content hash of the sources + flags the library was built from
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -26,25 +29,43 @@ def _deps():
                                + [os.path.join(ROOT, "include", "llama_b200.h")])
 
 
+def source_hash():
+    h = hashlib.sha256(" ".join(ARCH + FLAGS[:3]).encode())
+    for f in _deps():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def up_to_date():
-    if not os.path.exists(LIB):
+    """True when the library exists and was built from the current sources
+    (content hash, not mtimes: a snapshot copied to another box keeps it)."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(f) <= t for f in _deps())
+    with open(STAMP) as f:
+        return f.read().strip() == source_hash()
 
 
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    log = []
-    for src in _sources():
+    digest = source_hash()
+
+    def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, r
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, _sources()))
+    objs = []
+    log = []
+    for src, obj, cmd, r in results:
         log.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -57,6 +78,8 @@ def build(force=False, verbose=False):
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
     with open(os.path.join(BUILD, "build.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:

@@ -7,6 +7,7 @@
 #include <new>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "capi_internal.hpp"
 #include "launch.hpp"
@@ -21,13 +22,16 @@ llama_status fail(llama_status s, const std::string& msg) {
   return s;
 }
 
-using PlanKey = std::tuple<uint64_t, uint64_t, int, int>;
+using PlanKey = std::tuple<uint64_t, uint64_t, int, int, std::vector<int64_t>>;
 std::mutex g_mu;
 std::map<PlanKey, std::shared_ptr<llb::Plan>> g_plans;
 
-llama_status get_plan(const llb::Mapping& s, const llb::Mapping& d, llama_path path, int tile,
+llama_status get_plan(const llb::Mapping& s, const llb::Mapping& d, const llama_copy_options* options,
                       std::shared_ptr<llb::Plan>* out) {
-  PlanKey key{s.id, d.id, (int)path, tile};
+  const llama_path path = options ? options->path : LLAMA_PATH_AUTO;
+  const int tile = options ? options->tile_records : 0;
+  const llb::Knobs kn(options ? options->knobs : nullptr);
+  PlanKey key{s.id, d.id, (int)path, tile, std::vector<int64_t>(kn.v, kn.v + LLAMA_KNOB_COUNT)};
   {
     std::lock_guard<std::mutex> g(g_mu);
     auto it = g_plans.find(key);
@@ -35,7 +39,7 @@ llama_status get_plan(const llb::Mapping& s, const llb::Mapping& d, llama_path p
   }
   auto plan = std::make_shared<llb::Plan>();
   std::string err;
-  llama_status st = llb::make_plan(s, d, path, tile, plan.get(), &err);
+  llama_status st = llb::make_plan(s, d, path, tile, kn, plan.get(), &err);
   if (st != LLAMA_OK) return fail(st, err);
   std::lock_guard<std::mutex> g(g_mu);
   g_plans[key] = plan;
@@ -187,10 +191,8 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
                         const llama_copy_options* options, llama_plan_info* out) {
   if (!src_map || !dst_map || !out) return fail(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
   try {
-    llama_path path = options ? options->path : LLAMA_PATH_AUTO;
-    int tile = options ? options->tile_records : 0;
     std::shared_ptr<llb::Plan> plan;
-    llama_status st = get_plan(src_map->m, dst_map->m, path, tile, &plan);
+    llama_status st = get_plan(src_map->m, dst_map->m, options, &plan);
     if (st != LLAMA_OK) return st;
     *out = llama_plan_info{};
     out->path = plan->path;
@@ -246,10 +248,8 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
           return fail(LLAMA_ERR_OVERLAP, "dst blobs " + std::to_string(i) + " and " + std::to_string(j) + " overlap");
       }
     }
-    llama_path path = options ? options->path : LLAMA_PATH_AUTO;
-    int tile = options ? options->tile_records : 0;
     std::shared_ptr<llb::Plan> plan;
-    if ((st = get_plan(s, d, path, tile, &plan)) != LLAMA_OK) return st;
+    if ((st = get_plan(s, d, options, &plan)) != LLAMA_OK) return st;
     if (plan->empty) return LLAMA_OK;
 
     int e = 0;
@@ -305,7 +305,7 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
         llb::PermParams p = *plan->perm;
         for (int b = 0; b < s.nblobs(); ++b) p.blobs[0][b] = static_cast<uint8_t*>(const_cast<void*>(src_blobs[b]));
         for (int b = 0; b < d.nblobs(); ++b) p.blobs[1][b] = static_cast<uint8_t*>(dst_blobs[b]);
-        e = llb::launch_permute(p, plan->smem_bytes, stream);
+        e = llb::launch_permute(p, plan->smem_bytes, plan->permute_v1, plan->pdl, stream);
         break;
       }
       default:

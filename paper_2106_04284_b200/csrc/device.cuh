@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "params.hpp"
 
 namespace llb {
@@ -166,26 +168,43 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Host side: per-device cache of the dynamic-smem attribute and occupancy of
-// a kernel for the last shared-memory size it was launched with (these driver
+// Host side: per-device cache of a kernel's launch setup (these driver
 // queries cost tens of microseconds; a copy should not pay them every launch).
+// Thread-safe: the dynamic-smem limit is raised ONCE per kernel and device to
+// the device's opt-in maximum (so no thread ever lowers it under another's
+// launch), and the occupancy per shared-memory size is memoised under a mutex.
 struct LaunchCache {
-  int smem = -1;
-  int per_sm = 1;
+  std::mutex mu;
+  bool attr_set = false;
+  int n = 0;            // valid entries of smem / per_sm (ring replacement)
+  int smem[8] = {};
+  int per_sm[8] = {};
 };
+
+int max_optin_smem(int* bytes);  // k_simple.cu
 
 template <typename K>
 inline int prepare_kernel(K kernel, int threads, int smem_bytes, LaunchCache* cache, int* per_sm) {
-  if (cache->smem != smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    if (e != cudaSuccess) return (int)e;
+  std::lock_guard<std::mutex> g(cache->mu);
+  if (!cache->attr_set) {
+    int mx = 0;
+    int e = max_optin_smem(&mx);
+    if (e) return e;
+    cudaError_t ce = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (ce != cudaSuccess) return (int)ce;
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem_bytes);
-    cache->per_sm = n < 1 ? 1 : n;
-    cache->smem = smem_bytes;
+    cache->attr_set = true;
   }
-  *per_sm = cache->per_sm;
+  const int used = cache->n < 8 ? cache->n : 8;
+  for (int j = 0; j < used; ++j)
+    if (cache->smem[j] == smem_bytes) { *per_sm = cache->per_sm[j]; return 0; }
+  int n = 1;
+  cudaError_t ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem_bytes);
+  if (ce != cudaSuccess) return (int)ce;
+  const int slot = cache->n++ % 8;
+  cache->smem[slot] = smem_bytes;
+  cache->per_sm[slot] = n < 1 ? 1 : n;
+  *per_sm = cache->per_sm[slot];
   return 0;
 }
 

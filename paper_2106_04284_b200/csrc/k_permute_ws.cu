@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NC + 32, NC == 256 ? 3 : 1) k_permute_ws(const
   }
 }
 
-int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
+int launch_permute_ws(const PermParams& p, int smem_bytes, bool pdl, void* stream) {
   // 8 consumer warps (measured: 16 in one CTA are no faster for small
   // records and halve the speed of wide ones, which lose their 2 CTAs per SM)
   static LaunchCache cache[2][64];
@@ -215,27 +215,19 @@ int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream) {
   cfg.blockDim = dim3(kThreadsWS);
   cfg.dynamicSmemBytes = (size_t)smem_bytes;
   cfg.stream = (cudaStream_t)stream;
-  static const bool no_pdl = [] {
-    const char* e = std::getenv("LLAMA_NO_PDL");
-    return e && *e == '1';
-  }();
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, p);
   count_launch();
   return le != cudaSuccess ? (int)le : (int)cudaGetLastError();
 }
 
-int launch_permute(const PermParams& p, int smem_bytes, void* stream) {
+int launch_permute(const PermParams& p, int smem_bytes, bool v1, bool pdl, void* stream) {
   if (p.n_tiles == 0) return 0;
-  static const bool v1 = [] {
-    const char* e = std::getenv("LLAMA_PERMUTE_V1");
-    return e && *e == '1';
-  }();
-  if (p.tma && p.ns <= 4 && !v1) return launch_permute_ws(p, smem_bytes, stream);
+  if (p.tma && p.ns <= 4 && !v1) return launch_permute_ws(p, smem_bytes, pdl, stream);
   return launch_permute_v1(p, smem_bytes, stream);
 }
 

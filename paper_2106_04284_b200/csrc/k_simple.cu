@@ -28,15 +28,18 @@ void count_launch() { g_launches.fetch_add(1); }
 const char* cuda_error_string(int err) { return cudaGetErrorString((cudaError_t)err); }
 
 int current_device_sms(int* sms) {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];  // zero-initialised (static storage)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return (int)e;
-  if (dev >= 0 && dev < 64 && cache[dev] > 0) { *sms = cache[dev]; return 0; }
+  if (dev >= 0 && dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) { *sms = c; return 0; }
+  }
   int v = 0;
   e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return (int)e;
-  if (dev >= 0 && dev < 64) cache[dev] = v;
+  if (dev >= 0 && dev < 64) cache[dev].store(v, std::memory_order_relaxed);
   *sms = v;
   return 0;
 }

@@ -12,9 +12,10 @@ int launch_fill(const FillParams& p, void* stream);
 int launch_blobcopy(const BlobCopyParams& p, void* stream);
 int launch_bulkcopy(const BulkCopyParams& p, void* stream);
 int launch_run(const RunParams& p, void* stream);
-int launch_permute(const PermParams& p, int smem_bytes, void* stream);     // chooses v1 / warp-specialised
+// chooses v1 (barrier-synchronised) / warp-specialised; pdl: programmatic dependent launch
+int launch_permute(const PermParams& p, int smem_bytes, bool v1, bool pdl, void* stream);
 int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream);
-int launch_permute_ws(const PermParams& p, int smem_bytes, void* stream);
+int launch_permute_ws(const PermParams& p, int smem_bytes, bool pdl, void* stream);
 int launch_permute_direct(const DirectParams& p, void* stream);
 
 int launch_move_generic(const MoveParams& p, void* stream);

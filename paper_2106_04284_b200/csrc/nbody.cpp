@@ -108,12 +108,11 @@ llama_status llama_nbody_move_ex(const llama_mapping* mh, void* const* blobs, co
         }
         // TMA ring: tiles of T records (a multiple of 256, ~32 KB, T*S a
         // 16-byte multiple since S % 4 == 0 and T % 4 == 0), up to 8 stages
-        // in ~200 KB of shared memory; LLAMA_MOVE_AOS_LSU=1 selects the
-        // warp-staged LSU kernel instead
-        const char* lsu = std::getenv("LLAMA_MOVE_AOS_LSU");
+        // in ~200 KB of shared memory; the AOS_LSU path selects the
+        // warp-staged LSU kernel instead (measured slower: 5.2 vs 6.3 TB/s)
         const uint64_t T = std::max<uint64_t>(256, (32768 / S) / 256 * 256);
         const uint64_t ns = std::min<uint64_t>(8, (200 * 1024) / (T * S));
-        if (!(lsu && *lsu == '1') && ns >= 2 && T * S <= 64 * 1024) {
+        if (path != LLAMA_MOVE_AOS_LSU && ns >= 2 && T * S <= 64 * 1024) {
           p.tile = (uint32_t)T;
           p.ns = (uint32_t)ns;
         }
@@ -124,13 +123,13 @@ llama_status llama_nbody_move_ex(const llama_mapping* mh, void* const* blobs, co
     if (use == LLAMA_MOVE_AUTO) use = runs ? LLAMA_MOVE_RUNS : aos ? LLAMA_MOVE_AOS : LLAMA_MOVE_GENERIC;
     if (use == LLAMA_MOVE_RUNS && !runs)
       return llb::set_error(LLAMA_ERR_UNSUPPORTED, "RUNS needs 16-byte aligned runs of >= 4 particles per leaf");
-    if (use == LLAMA_MOVE_AOS && !aos)
+    if ((use == LLAMA_MOVE_AOS || use == LLAMA_MOVE_AOS_LSU) && !aos)
       return llb::set_error(LLAMA_ERR_UNSUPPORTED, "AOS needs Pos / Vel in one AoS part with 4-byte aligned fields");
-    if (use < LLAMA_MOVE_AUTO || use > LLAMA_MOVE_AOS) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "bad path");
+    if (use < LLAMA_MOVE_AUTO || use > LLAMA_MOVE_AOS_LSU) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "bad path");
     if (path_used) *path_used = use;
     if (m.N == 0) return LLAMA_OK;
     int e = use == LLAMA_MOVE_RUNS ? llb::launch_move_runs(p, stream)
-            : use == LLAMA_MOVE_AOS ? llb::launch_move_aos(p, stream)
+            : (use == LLAMA_MOVE_AOS || use == LLAMA_MOVE_AOS_LSU) ? llb::launch_move_aos(p, stream)
                                     : llb::launch_move_generic(p, stream);
     if (e) return llb::set_error(LLAMA_ERR_CUDA, std::string("move launch: ") + llb::cuda_error_string(e));
     return LLAMA_OK;

@@ -13,14 +13,10 @@ namespace {
 constexpr uint64_t kAosLikeMaxBlock = 16384;  // larger AoSoA blocks are tiled inside a block
 constexpr int kBarBytes = 128;
 
-// Tuning knobs (defaults measured on B200; env overrides for sweeps):
-//   LLAMA_TILE_BYTES  src + dst image bytes per tile
-//   LLAMA_SMEM_BUDGET shared memory per CTA the stage count may use
-//   LLAMA_STAGES      source stages (2..4); LLAMA_NO_TMA=1 forces LSU copies
-uint64_t env_u64(const char* name, uint64_t def) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::strtoull(v, nullptr, 10) : def;
-}
+// Tuning knobs (llama_knob, include/llama_b200.h): the defaults written at
+// each use below are the measured choices on B200; a caller overrides them
+// only explicitly through llama_copy_options.knobs (the plan cache keys on
+// the values), never through the environment.
 
 uint64_t gcd64(uint64_t a, uint64_t b) {
   while (b) { uint64_t t = a % b; a = b; b = t; }
@@ -88,7 +84,7 @@ void plan_naive(const Mapping& s, const Mapping& d, Plan* p) {
 
 // 2-d views of different linearisations, records small enough for 32x32
 // tiles in <= 48 KB of shared memory, not traced.
-bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
+bool plan_transpose(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
   if (s.trace || d.trace) { *why = "traced views count through the naive kernel"; return false; }
   if (s.lin == d.lin) { *why = "equal linearisations"; return false; }
   if (s.extents.size() != 2) { *why = "TRANSPOSE is for 2-d views"; return false; }
@@ -114,11 +110,11 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   for (const Mapping* m : {&s, &d})
     for (int k = 0; k < m->K(); ++k)
       if (!((m->Lk[k] == 1 && m->Bk[k] < (1ull << 32)) || m->Lk[k] >= m->N)) n.tlinear = 0;
-  if (!env_u64("LLAMA_TRANSPOSE_LINEAR", 1)) n.tlinear = 0;
-  n.raw_typed = (uint32_t)env_u64("LLAMA_TRANSPOSE_RAW_TYPED", 1);
+  if (!kn.get(LLAMA_KNOB_TRANSPOSE_LINEAR, 1)) n.tlinear = 0;
+  n.raw_typed = (uint32_t)kn.get(LLAMA_KNOB_TRANSPOSE_RAW_TYPED, 1);
   if (n.tlinear) {  // one leaf size of 4 or 8 bytes: the two-leaf pass (k_simple.cu lin_tile_fixed)
     const uint64_t z = s.sizes[0];
-    bool same = (z == 4 || z == 8) && env_u64("LLAMA_TRANSPOSE_FIXED", 1);
+    bool same = (z == 4 || z == 8) && kn.get(LLAMA_KNOB_TRANSPOSE_FIXED, 1);
     for (int k = 0; k < s.K(); ++k) same = same && s.sizes[k] == z;
     n.tlinear = same ? (uint32_t)z : 1;
   }
@@ -130,7 +126,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
     const Mapping& m = X == 0 ? s : d;
     const uint64_t S = m.B;
     bool ok = m.uniform && m.kind == LLAMA_AOS && m.L == 1 && m.base[0] % 16 == 0 && (32 * S) % 16 == 0 &&
-              env_u64("LLAMA_TRANSPOSE_RAW", 1);
+              kn.get(LLAMA_KNOB_TRANSPOSE_RAW, 1);
     if (m.lin == LLAMA_ROW_MAJOR) ok = ok && ((uint64_t)m.extents[1] * S) % 16 == 0;
     if (m.lin == LLAMA_COL_MAJOR) ok = ok && ((uint64_t)m.extents[0] * S) % 16 == 0;
     if (ok) {
@@ -143,7 +139,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   // measured (4096^2 Particle7): raw on both sides 1.54 -> 2.37 TB/s; one
   // raw side next to an element-wise SoA side is slower than element-wise
   // on both (2.52 -> 2.22 TB/s: the raw code's registers cost occupancy)
-  if (!(n.sraw && n.draw) && !(n.tlinear && env_u64("LLAMA_TRANSPOSE_RAW1", 1))) n.sraw = n.draw = 0, raw_bytes = 0;
+  if (!(n.sraw && n.draw) && !(n.tlinear && kn.get(LLAMA_KNOB_TRANSPOSE_RAW1, 1))) n.sraw = n.draw = 0, raw_bytes = 0;
   if (raw_bytes) {
     smem = (smem + 15) & ~15ull;
     n.rawoff = (uint32_t)smem;
@@ -158,7 +154,7 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   // per-CTA leaf table of both sides (k_simple.cu LinEnt, 16 B per leaf);
   // not next to a raw buffer (Particle7: 56 KB of tile + raw buffer fill a
   // quarter SM exactly, the table would cost a CTA per SM: -17%)
-  if (n.tlinear && !n.sraw && !n.draw && env_u64("LLAMA_TRANSPOSE_TABLE", 1)) {
+  if (n.tlinear && !n.sraw && !n.draw && kn.get(LLAMA_KNOB_TRANSPOSE_TABLE, 1)) {
     smem = (smem + 15) & ~15ull;
     n.linoff = (uint32_t)smem;
     smem += 2ull * 16 * s.K();
@@ -174,11 +170,11 @@ bool plan_transpose(const Mapping& s, const Mapping& d, Plan* p, std::string* wh
   return true;
 }
 
-bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
+bool plan_blobcopy(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
   if (!same_layout(s, d)) { *why = "layouts differ"; return false; }
   if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
   p->path = LLAMA_PATH_BLOBCOPY;
-  if (env_u64("LLAMA_BLOBCOPY_LSU", 0)) {  // thread (LDG/STG) variant, for comparison
+  if (kn.get(LLAMA_KNOB_BLOBCOPY_LSU, 0)) {  // thread (LDG/STG) variant, for comparison
     p->blobcopy.reset(new BlobCopyParams);
     BlobCopyParams& b = *p->blobcopy;
     std::memset(&b, 0, sizeof(b));
@@ -193,8 +189,8 @@ bool plan_blobcopy(const Mapping& s, const Mapping& d, Plan* p, std::string* why
   BulkCopyParams& b = *p->bulkcopy;
   std::memset(&b, 0, sizeof(b));
   b.nb = d.nblobs();
-  b.CH = (uint32_t)env_u64("LLAMA_BULK_CHUNK", 65536) & ~15u;  // 64 KB x 3 stages: measured best on B200
-  b.NS = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, env_u64("LLAMA_BULK_STAGES", 3)));
+  b.CH = (uint32_t)kn.get(LLAMA_KNOB_BULK_CHUNK, 65536) & ~15u;  // 64 KB x 3 stages: measured best on B200
+  b.NS = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_BULK_STAGES, 3)));
   for (int j = 0; j < b.nb; ++j) {
     b.bytes[j] = d.blob_sizes[j];
     b.cstart[j + 1] = b.cstart[j] + ceil_div(d.blob_sizes[j], b.CH);
@@ -247,8 +243,8 @@ bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why) {
 
 // AoS <-> SoA with many leaves (measured on HEP100): the AoS side
 // through a TMA ring, the SoA side element-wise with coalesced accesses.
-bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
-  const uint64_t mode = env_u64("LLAMA_DIRECT", 1);  // 0: off; 2: any leaf count (tests)
+bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why) {
+  const uint64_t mode = kn.get(LLAMA_KNOB_DIRECT, 1);  // 0: off; 2: any leaf count (tests)
   if (mode == 0) { *why = "disabled"; return false; }
   if (!s.uniform || !d.uniform) { *why = "split"; return false; }
   const bool a2s = s.kind == LLAMA_AOS && d.soa();
@@ -266,8 +262,8 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   // registers in 1-2 byte pieces they lost: 2.9 -> 2.0)
   // (with a record stride that is a multiple of 4 the misaligned 4- / 8-byte
   // leaves are staged by cp.async and scattered in compile-time pieces)
-  const bool staging = s2a && S % 4 == 0 && env_u64("LLAMA_DIRECT_ASYNC", 1) && env_u64("LLAMA_DIRECT_PHASE", 1) &&
-                       env_u64("LLAMA_DIRECT_STAGING", 1);
+  const bool staging = s2a && S % 4 == 0 && kn.get(LLAMA_KNOB_DIRECT_ASYNC, 1) && kn.get(LLAMA_KNOB_DIRECT_PHASE, 1) &&
+                       kn.get(LLAMA_KNOB_DIRECT_STAGING, 1);
   if (mode != 2 && s2a && !staging)
     for (int k = 0; k < A.K(); ++k)
       if (A.F[k] % A.sizes[k] || S % A.sizes[k]) { *why = "packed AoS: the tile permute"; return false; }
@@ -276,7 +272,7 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   const uint64_t T = 64;
   if (tile_records > 0 && tile_records != 64) { *why = "the direct variant uses 64-record tiles"; return false; }
   const uint64_t stage = align16(T * S);
-  const uint64_t ns = std::min<uint64_t>(8, std::max<uint64_t>(2, env_u64("LLAMA_DIRECT_STAGES", a2s ? 3 : 2)));
+  const uint64_t ns = std::min<uint64_t>(8, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_DIRECT_STAGES, a2s ? 3 : 2)));
   if (ns * stage > 200 * 1024) { *why = "record too wide"; return false; }
   p->direct.reset(new DirectParams);
   DirectParams& dp = *p->direct;
@@ -290,9 +286,9 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   dp.stage = (uint32_t)stage;
   dp.n_tiles = ceil_div(s.N, T);
   // an even record stride in words puts one leaf of 32 records on few banks
-  dp.mix = ((S / 4) % 2 == 0 && S % 4 == 0 && env_u64("LLAMA_DIRECT_MIX", 1)) ? 1 : 0;
+  dp.mix = ((S / 4) % 2 == 0 && S % 4 == 0 && kn.get(LLAMA_KNOB_DIRECT_MIX, 1)) ? 1 : 0;
   // SoA -> AoS: aligned 4- / 8-byte elements land in the image by cp.async
-  dp.async = (!a2s && env_u64("LLAMA_DIRECT_ASYNC", 1)) ? 1 : 0;
+  dp.async = (!a2s && kn.get(LLAMA_KNOB_DIRECT_ASYNC, 1)) ? 1 : 0;
   dp.abase = A.base[0];
   dp.ablob = A.blob[0];
   auto lb = [](uint64_t x) { return x ? (x & (~x + 1)) : 16ull; };
@@ -314,21 +310,21 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
       uint32_t kd = (uint32_t)l.size | (l.a_img >= l.size ? 16u : 0u) | (l.a_glob >= l.size ? 32u : 0u);
       // record stride a multiple of 4: a misaligned leaf sits at the same
       // word phase F % 4 in every record (compile-time funnel shifts / pieces)
-      if (S % 4 == 0 && l.a_img < l.size && l.size >= 2 && env_u64("LLAMA_DIRECT_PHASE", 1))
+      if (S % 4 == 0 && l.a_img < l.size && l.size >= 2 && kn.get(LLAMA_KNOB_DIRECT_PHASE, 1))
         kd |= 64u | ((l.F & 3u) << 7);
       // SoA -> AoS, image-aligned 1- / 2-byte leaf with 16-byte aligned SoA
       // runs: staged as 16-byte cp.async chunks (full tiles)
       // (measured: chunk-staging the aligned 4- / 8-byte classes too, instead
       // of their element cp.asyncs into the image, lost 2-33%)
       if (staging && l.size <= 2 && l.a_img >= l.size && l.gbase % 16 == 0 && (T * l.size) % 16 == 0 &&
-          env_u64("LLAMA_DIRECT_CHUNKS", 1))
+          kn.get(LLAMA_KNOB_DIRECT_CHUNKS, 1))
         kd |= 512u;
       return kd;
     };
     // SoA -> AoS with cp.async: classes ordered by how the kernel moves them
     // (k_permute_direct.cu direct_tile): 0 chunk-staged, 1 staged, 2 cp.async
     // into the image, 3 registers; each pass walks its own class range
-    const bool use_async = !a2s && env_u64("LLAMA_DIRECT_ASYNC", 1);
+    const bool use_async = !a2s && kn.get(LLAMA_KNOB_DIRECT_ASYNC, 1);
     auto cat = [&](int k) -> uint32_t {
       const uint32_t kd = kind(k), z = kd & 15;
       if (!use_async) return 3;
@@ -386,7 +382,7 @@ bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, Plan* p, 
   return true;
 }
 
-bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p, std::string* why) {
+bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why) {
   // every part must spread its records over its blobs (not One)
   for (const Mapping* m : {&s, &d}) {
     if ((int)m->parts.size() > kMaxParts) { *why = "too many split parts"; return false; }
@@ -434,7 +430,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     // CTAs per SM (budget below)
     const uint64_t per = rec_img[0] + rec_img[1];
     const uint64_t def_tile = per <= 128 ? 64 * 1024 : 48 * 1024;
-    uint64_t c = std::max<uint64_t>(1, env_u64("LLAMA_TILE_BYTES", def_tile) / (per * Tmult));
+    uint64_t c = std::max<uint64_t>(1, kn.get(LLAMA_KNOB_TILE_BYTES, def_tile) / (per * Tmult));
     const uint64_t cmax = std::max<uint64_t>(1, ceil_div(R, Tmult));
     c = std::min(c, cmax);
     T = 0;
@@ -448,7 +444,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
       // wide records: the tile must leave room for two CTAs per SM with two
       // source stages (measured: one CTA per SM starves the permute of warps)
       const uint64_t est = 256 + 64ull * s.K() + 2 * (t * rec_img[0] + 16ull * s.K()) + 2 * (t * rec_img[1] + 16ull * s.K());
-      if (per > 128 && c > 1 && est > env_u64("LLAMA_SMEM_BUDGET", 112 * 1000)) ok = false;
+      if (per > 128 && c > 1 && est > kn.get(LLAMA_KNOB_SMEM_BUDGET, 112 * 1000)) ok = false;
       if (ok) { T = t; break; }
     }
     if (!T) { *why = "no tile size divides the AoSoA lane count"; return false; }
@@ -527,7 +523,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
     ps.n_segs = ns;
     ps.img_bytes = (uint32_t)align16(off);
   }
-  if (env_u64("LLAMA_NO_TMA", 0)) tma = false;
+  if (kn.get(LLAMA_KNOB_NO_TMA, 0)) tma = false;
   pp.tma = tma ? 1 : 0;
   pp.src_tile_tma = (uint32_t)full_src;
   pp.src_stage = (uint32_t)align16(pp.side[0].img_bytes);
@@ -585,7 +581,7 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   pp.n_wmoves = 0;
   if (s.parts.size() == 1 && d.parts.size() == 1 && !soa_like[0][0] && !soa_like[1][0] && s.L == 1 &&
       d.L == 1 && s.B % 4 == 0 && d.B % 4 == 0 &&
-      env_u64("LLAMA_WORD_MODE", 1)) {
+      kn.get(LLAMA_KNOB_WORD_MODE, 1)) {
     std::vector<int64_t> src_of(d.B, -1);
     for (int k = 0; k < s.K(); ++k)
       for (uint32_t b = 0; b < s.sizes[k]; ++b) src_of[d.F[k] + b] = (int64_t)(s.F[k] + b);
@@ -619,26 +615,26 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   pp.nd = 2;
   uint64_t smem = 0;
   const uint64_t per_rec = rec_img[0] + rec_img[1];
-  const uint64_t budget = env_u64("LLAMA_SMEM_BUDGET", per_rec <= 128 ? 230 * 1000 : 112 * 1000);
+  const uint64_t budget = kn.get(LLAMA_KNOB_SMEM_BUDGET, per_rec <= 128 ? 230 * 1000 : 112 * 1000);
   // small records: a deep (4-stage) ring; wide records: 2 stages, so more CTAs fit per SM
   const uint32_t ns_max =
-      (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_STAGES", per_rec <= 128 ? 4 : 2)));
+      (uint32_t)std::min<uint64_t>(4, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_STAGES, per_rec <= 128 ? 4 : 2)));
   for (uint32_t ns = ns_max; ns >= 2; --ns) {
     smem = kBarBytes + pp.tab_bytes + (uint64_t)ns * pp.src_stage + 2ull * pp.dst_stage;
     pp.ns = ns;
     // measured on B200: one CTA with 116-160 KB of shared memory runs far
     // slower than both 108 KB and 172 KB (C4: 3.5 vs 6.0 TB/s); skip the window
-    const bool window = smem > 116 * 1024 && smem < 160 * 1024 && !std::getenv("LLAMA_STAGES");
+    const bool window = smem > 116 * 1024 && smem < 160 * 1024 && !kn.given(LLAMA_KNOB_STAGES);
     if (smem <= budget && !(window && ns > 2)) break;
   }
   if (smem > 227 * 1024) { *why = "tile images exceed shared memory"; return false; }
-  pp.order = (uint32_t)env_u64("LLAMA_WS_ORDER", 2);
+  pp.order = (uint32_t)kn.get(LLAMA_KNOB_WS_ORDER, 2);
   // a third destination buffer keeps one tile's store in flight while the
   // consumers fill the next (warp-specialised kernel only; measured on B200:
   // +2-5% for small records, C2 6.44 -> 6.57 TB/s; slower for wide records
   // with two CTAs per SM, and never into the 116-160 KB window above)
   const uint64_t nd_req =
-      std::min<uint64_t>(4, std::max<uint64_t>(2, env_u64("LLAMA_DST_BUFS", per_rec <= 128 ? 3 : 2)));
+      std::min<uint64_t>(4, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_DST_BUFS, per_rec <= 128 ? 3 : 2)));
   while (pp.tma && pp.nd < nd_req && smem + pp.dst_stage <= std::min<uint64_t>(budget, 227 * 1024) &&
          !(smem + pp.dst_stage > 116 * 1024 && smem + pp.dst_stage < 160 * 1024)) {
     smem += pp.dst_stage;
@@ -674,8 +670,10 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, Plan* p,
   return true;
 }
 
-llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int tile_records, Plan* out,
-                       std::string* err) {
+llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int tile_records, const Knobs& kn,
+                       Plan* out, std::string* err) {
+  out->permute_v1 = kn.get(LLAMA_KNOB_PERMUTE_V1, 0) != 0;
+  out->pdl = kn.get(LLAMA_KNOB_NO_PDL, 0) == 0;
   llama_status st = check_compatible(s, d, err);
   if (st != LLAMA_OK) return st;
   if (d.collides()) {  // the copy's result would depend on the order of the writes
@@ -693,7 +691,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   // record (index) -> record (index) across storage orders, or counting every
   // address resolution (Trace / Heatmap): the element-wise kernel only
   if (s.lin != d.lin || s.trace || d.trace) {
-    if ((path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) && plan_transpose(s, d, out, &why))
+    if ((path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) && plan_transpose(s, d, kn, out, &why))
       return LLAMA_OK;
     if (path != LLAMA_PATH_AUTO && path != LLAMA_PATH_NAIVE) {
       *err = "path not applicable to this mapping pair: linearised differently or traced: " + why;
@@ -713,10 +711,10 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       // bulk blob copy) and run pairs (SoA <-> AoSoA) included
       // identities of SoA layouts with many leaves (many blobs / segments): the bulk blob copy
       // (HEP SoA MB: 6.4 TB/s vs 1.8 for 200 TMA segment ops per tile)
-      if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
-      if (plan_direct(s, d, tile_records, out, &why)) return LLAMA_OK;
-      if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
-      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
+      if (plan_direct(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
+      if (plan_permute(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
+      if (plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
       plan_naive(s, d, out);
       return LLAMA_OK;
@@ -724,14 +722,14 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       plan_naive(s, d, out);
       return LLAMA_OK;
     case LLAMA_PATH_BLOBCOPY:
-      if (plan_blobcopy(s, d, out, &why)) return LLAMA_OK;
+      if (plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
       break;
     case LLAMA_PATH_RUN:
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
       break;
     case LLAMA_PATH_PERMUTE:
-      if (plan_direct(s, d, tile_records, out, &why)) return LLAMA_OK;
-      if (plan_permute(s, d, tile_records, out, &why)) return LLAMA_OK;
+      if (plan_direct(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
+      if (plan_permute(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       break;
     default:
       *err = "bad path";

@@ -65,6 +65,10 @@ struct llama_stager {
   uint8_t* zero = nullptr;  // 4 KB of device zeros (gap fills)
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t e_in[kNB] = {}, e_comp[kNB] = {}, e_out[kNB] = {}, e_start = nullptr, e_done = nullptr;
+  // slabs enqueued over the stager's lifetime: slab c uses buffer c % kNB and
+  // waits for the previous user of that buffer (slab c - kNB, possibly of an
+  // earlier call on another stream) to have gone back out
+  uint64_t slabs = 0;
   std::map<std::tuple<uint64_t, uint64_t>, llama_mapping*> local;  // (parent id, records) -> 1-D view
   ~llama_stager() {
     if (h2d) cudaStreamSynchronize(h2d);
@@ -211,8 +215,9 @@ llama_status prepare_job(llama_stager* st, StagedJob* jb) {
   return LLAMA_OK;
 }
 
-// Enqueues the slabs of one job; c counts slabs over the whole batch, so the
-// three buffers keep rotating from one job into the next (no drain between).
+// Enqueues the slabs of one job; c counts slabs over the stager's lifetime, so
+// the three buffers keep rotating from one job (and call) into the next (no
+// drain between), and every reuse of a buffer waits for its previous slab.
 llama_status enqueue_job(llama_stager* st, const StagedJob& jb, uint64_t* c) {
   const llb::Mapping& s = jb.sm->m;
   const llb::Mapping& d = jb.dm->m;
@@ -295,9 +300,8 @@ llama_status llama_copy_staged_batch(llama_stager* st, int32_t count, const llam
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->comp, st->e_start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->d2h, st->e_start, 0);
     if (e != cudaSuccess) return cuda_err(e, "stream ordering");
-    uint64_t c = 0;
     for (const StagedJob& jb : jobs) {
-      llama_status s = enqueue_job(st, jb, &c);
+      llama_status s = enqueue_job(st, jb, &st->slabs);
       if (s != LLAMA_OK) return s;
     }
     if ((e = cudaEventRecord(st->e_done, st->d2h)) != cudaSuccess) return cuda_err(e, "done event");
@@ -335,8 +339,7 @@ llama_status llama_nbody_move_staged(llama_stager* st, const llama_mapping* m, v
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->comp, st->e_start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st->d2h, st->e_start, 0);
     if (e != cudaSuccess) return cuda_err(e, "stream ordering");
-    uint64_t c = 0;
-    if ((s = enqueue_job(st, jb, &c)) != LLAMA_OK) return s;
+    if ((s = enqueue_job(st, jb, &st->slabs)) != LLAMA_OK) return s;
     if ((e = cudaEventRecord(st->e_done, st->d2h)) != cudaSuccess) return cuda_err(e, "done event");
     if ((e = cudaStreamWaitEvent((cudaStream_t)stream, st->e_done, 0)) != cudaSuccess) return cuda_err(e, "join");
     return LLAMA_OK;

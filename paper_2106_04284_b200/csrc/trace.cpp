@@ -31,6 +31,23 @@ DevTrace dev_trace(const Mapping& m) {
 
 }  // namespace llb
 
+namespace {
+
+// Counters are read after ALL work on the counters' device: a traced copy may
+// sit on a non-blocking stream (torch's streams, a stager's), which the
+// legacy-stream cudaMemcpy below would not wait for.
+cudaError_t sync_trace_device(const llb::TraceBuffers& t) {
+  int cur = 0;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return e;
+  if (cur != t.device && (e = cudaSetDevice(t.device)) != cudaSuccess) return e;
+  e = cudaDeviceSynchronize();
+  if (cur != t.device) cudaSetDevice(cur);
+  return e;
+}
+
+}  // namespace
+
 extern "C" {
 
 llama_status llama_mapping_create_traced(const llama_mapping* inner, int32_t kinds, llama_mapping** out) {
@@ -72,7 +89,8 @@ llama_status llama_trace_field_hits(const llama_mapping* m, uint64_t* hits, int3
   if (!m->m.trace || !m->m.trace->hits) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "mapping not traced with FIELDS");
   const int n = std::min(capacity, m->m.K());
   if (n <= 0) return LLAMA_OK;
-  cudaError_t e = cudaMemcpy(hits, m->m.trace->hits, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost);
+  cudaError_t e = sync_trace_device(*m->m.trace);
+  if (e == cudaSuccess) e = cudaMemcpy(hits, m->m.trace->hits, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? LLAMA_OK : llb::set_error(LLAMA_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -83,7 +101,8 @@ llama_status llama_trace_byte_hits(const llama_mapping* m, int32_t blob, uint32_
   const uint64_t n = m->m.blob_sizes[blob];
   if (capacity < n) return llb::set_error(LLAMA_ERR_INVALID_ARGUMENT, "capacity below the blob size");
   if (n == 0) return LLAMA_OK;
-  cudaError_t e = cudaMemcpy(hits, m->m.trace->heat + m->m.trace->heat_base[blob], sizeof(uint32_t) * n,
+  cudaError_t e = sync_trace_device(*m->m.trace);
+  if (e == cudaSuccess) e = cudaMemcpy(hits, m->m.trace->heat + m->m.trace->heat_base[blob], sizeof(uint32_t) * n,
                              cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? LLAMA_OK : llb::set_error(LLAMA_ERR_CUDA, cudaGetErrorString(e));
 }

@@ -17,7 +17,7 @@ def llama():
     return m
 
 
-def _pair(llama, oracle, schema, ext, sspec, slin, dspec, dlin, seed=3, paths=("auto",)):
+def _pair(llama, oracle, schema, ext, sspec, slin, dspec, dlin, seed=3, paths=("auto",), knobs=None):
     sm = llama.Mapping.from_spec(schema, ext, sspec, lin=slin)
     dm = llama.Mapping.from_spec(schema, ext, dspec, lin=dlin)
     so = oracle.mapping_from_spec(schema, ext, sspec, lin=slin)
@@ -30,13 +30,13 @@ def _pair(llama, oracle, schema, ext, sspec, slin, dspec, dlin, seed=3, paths=("
     exp = oracle.copy(so, src, do)
     for path in paths:
         try:
-            llama.plan(sm, dm, path=path)
+            llama.plan(sm, dm, path=path, knobs=knobs)
         except llama.LlamaError:
             continue
         db = dm.alloc("cuda")
         for t in db:
             t.fill_(0x5A)
-        llama.copy(sm, sb, dm, db, path=path)
+        llama.copy(sm, sb, dm, db, path=path, knobs=knobs)
         torch.cuda.synchronize()
         for j, t in enumerate(db):
             assert np.array_equal(t.cpu().numpy(), exp[j]), (sspec, slin, dspec, dlin, path, j)
@@ -134,21 +134,20 @@ def test_raw_aos_tiles(llama, oracle_mod, lins):
             _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "naive"))
 
 
-@pytest.mark.parametrize("knobs", [{"LLAMA_TRANSPOSE_LINEAR": "0"}, {"LLAMA_TRANSPOSE_RAW1": "0"},
-                                   {"LLAMA_TRANSPOSE_FIXED": "0"}, {"LLAMA_TRANSPOSE_TABLE": "0"},
-                                   {"LLAMA_TRANSPOSE_RAW_TYPED": "0"},
-                                   {"LLAMA_TRANSPOSE_RAW": "0"}, {}])
-def test_transpose_variants(llama, oracle_mod, monkeypatch, knobs):
+@pytest.mark.parametrize("knobs", [{"transpose_linear": 0}, {"transpose_raw1": 0},
+                                   {"transpose_fixed": 0}, {"transpose_table": 0},
+                                   {"transpose_raw_typed": 0},
+                                   {"transpose_raw": 0}, {}])
+def test_transpose_variants(llama, oracle_mod, knobs):
     """Every k_transpose2d instantiation: linear sides (one multiply-add per
     element) or the block / lane split, a raw AoS side next to an element-wise
     side, raw on both sides or none, the two-leaf pass for one 4-byte leaf
     size; full and ragged tiles, 4- and mixed-size leaves, AoSoA sides (not
     linear)."""
-    for k, v in knobs.items():
-        monkeypatch.setenv(k, v)
     for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [70, 45]), (W.PARTICLE7, [64, 64])):
         for sk, dk in ((("soa_mb", 1, False), ("aos", 1, False)), (("aos", 1, True), ("soa_sb", 1, True)),
                        (("aos", 1, False), ("aos", 1, True)), (("aosoa", 8, False), ("aos", 1, False)),
                        (("one", 1, True), ("soa_mb", 1, False))):
             for lins in (("morton", "col") if ext[0] == ext[1] else ("row", "col"), ("col", "row")):
-                _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "transpose"))
+                _pair(llama, oracle_mod, schema, ext, sk, lins[0], dk, lins[1], paths=("auto", "transpose"),
+                      knobs=knobs)

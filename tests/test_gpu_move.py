@@ -147,14 +147,13 @@ def test_move_full_size_sampled(llama, oracle_mod, full_aos, name):
 
 
 @pytest.mark.parametrize("n", [127, 128 * 37 + 5, 300_001])
-def test_move_aos_lsu_variant(llama, oracle_mod, n, monkeypatch):
-    """The warp-staged LSU AoS kernel (LLAMA_MOVE_AOS_LSU=1) against the oracle."""
-    monkeypatch.setenv("LLAMA_MOVE_AOS_LSU", "1")
+def test_move_aos_lsu_variant(llama, oracle_mod, n):
+    """The warp-staged LSU AoS kernel (path AOS_LSU) against the oracle."""
     vals = W.particle_values(n, seed=8)
     om = oracle_mod.Mapping(W.PARTICLE7, [n], "aos")
     exp = oracle_mod.nbody_move(om, [np.frombuffer(vals.tobytes(), np.uint8).copy()], DT)
     dm, db, _, _ = _device_view(llama, oracle_mod, "aos", n, vals)
-    assert llama.nbody_move(dm, db, DT, path="aos") == "aos"
+    assert llama.nbody_move(dm, db, DT, path="aos_lsu") == "aos_lsu"
     torch.cuda.synchronize()
     assert np.array_equal(db[0].cpu().numpy(), exp[0])
 

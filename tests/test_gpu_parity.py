@@ -39,7 +39,7 @@ def _host(t):
     return t.cpu().numpy()
 
 
-def run_case(llama, oracle, schema, ext, sk, dk, seed=42, paths=("auto",), pad=0xCD, check_src=True):
+def run_case(llama, oracle, schema, ext, sk, dk, seed=42, paths=("auto",), pad=0xCD, check_src=True, knobs=None):
     sm = llama.Mapping(schema, ext, *sk)
     dm = llama.Mapping(schema, ext, *dk)
     so = oracle.Mapping(schema, ext, *sk)
@@ -54,19 +54,19 @@ def run_case(llama, oracle, schema, ext, sk, dk, seed=42, paths=("auto",), pad=0
     for path in paths:
         if path != "auto":
             try:
-                llama.plan(sm, dm, path=path)
+                llama.plan(sm, dm, path=path, knobs=knobs)
             except llama.LlamaError:
                 continue  # path not applicable to this pair
         db = dm.alloc("cuda")
         for t in db:
             t.fill_(0x5A)
-        llama.copy(sm, sb, dm, db, path=path)
+        llama.copy(sm, sb, dm, db, path=path, knobs=knobs)
         torch.cuda.synchronize()
         for j, t in enumerate(db):
             got = _host(t)
             if not np.array_equal(got, exp[j]):
                 bad = np.nonzero(got != exp[j])[0]
-                raise AssertionError(f"{sk}->{dk} ext={ext} path={path} plan={llama.plan(sm, dm, path=path)}: "
+                raise AssertionError(f"{sk}->{dk} ext={ext} path={path} plan={llama.plan(sm, dm, path=path, knobs=knobs)}: "
                                      f"blob {j}: {bad.size} bytes differ, first at {bad[:8]}")
 
 
@@ -383,17 +383,16 @@ def test_one_and_mapping_c_sources(llama, oracle_mod, n):
 @pytest.mark.parametrize("schema_name", ["listing1", "particle7", "hep100"])
 @pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097])
 @pytest.mark.parametrize("use_async", ["1", "0", "nostage", "nochunk"])
-def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async, monkeypatch):
+def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async):
     """The direct permute (AoS side through TMA, SoA side element-wise) for
-    every AoS <-> SoA pair, forced for few-leaf records too (LLAMA_DIRECT=2):
+    every AoS <-> SoA pair, forced for few-leaf records too (knob direct=2):
     odd record strides exercise the byte-wise shared-memory accesses; SoA ->
     AoS with the cp.async classes (with and without the staged misaligned
     classes and the 16-byte chunk-staged 1- / 2-byte classes) and with
     registers only."""
-    monkeypatch.setenv("LLAMA_DIRECT", "2")
-    monkeypatch.setenv("LLAMA_DIRECT_ASYNC", "0" if use_async == "0" else "1")
-    monkeypatch.setenv("LLAMA_DIRECT_STAGING", "0" if use_async == "nostage" else "1")
-    monkeypatch.setenv("LLAMA_DIRECT_CHUNKS", "0" if use_async == "nochunk" else "1")
+    knobs = {"direct": 2, "direct_async": 0 if use_async == "0" else 1,
+             "direct_staging": 0 if use_async == "nostage" else 1,
+             "direct_chunks": 0 if use_async == "nochunk" else 1}
     schema = W.SCHEMAS[schema_name]
     names = ["aos", "aos_aligned", "soa_mb", "soa_sb", "soa_sb_aligned"]
     for a in names:
@@ -402,8 +401,8 @@ def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async, mon
                 continue
             sm = llama.Mapping(schema, [n], *KINDS[a])
             dm = llama.Mapping(schema, [n], *KINDS[b])
-            assert llama.plan(sm, dm)["direct"], (a, b)
-            run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b])
+            assert llama.plan(sm, dm, knobs=knobs)["direct"], (a, b)
+            run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b], knobs=knobs)
 
 
 def test_direct_chosen_for_hep(llama):

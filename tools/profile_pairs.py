@@ -2,6 +2,7 @@
 """Runs selected mapping pairs of a BASELINE config a few times (for ncu
 captures and quick timing).  Usage:
     python tools/profile_pairs.py --config C2 --pairs aos:soa_mb,aosoa8:soa_mb --iters 3 [--path permute]
+        [--knobs stages=3,dst_bufs=2]   (llama_knob overrides, paper_2106_04284_b200.KNOBS)
 """
 import argparse
 import os
@@ -22,7 +23,9 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--path", default=None)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--records", type=int, default=0)
+ap.add_argument("--knobs", default="")
 a = ap.parse_args()
+knobs = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)} or None
 cfg = W.CONFIGS[a.config]
 schema = W.SCHEMAS[cfg["schema"]]
 ext = [a.records] if a.records else list(cfg["extents"])
@@ -34,14 +37,14 @@ for pair in a.pairs.split(","):
     llama.generate(sm, sb, 42)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile)
+    llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile, knobs=knobs)
     e0.record()
     for _ in range(a.iters):
-        llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile)
+        llama.copy(sm, sb, dm, db, path=a.path, tile_records=a.tile, knobs=knobs)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.iters
     nbytes = sm.footprint() + dm.footprint()
-    print(f"{s:>12} -> {d:<12} {llama.plan(sm, dm, path=a.path, tile_records=a.tile)} {ms:.3f} ms "
+    print(f"{s:>12} -> {d:<12} {llama.plan(sm, dm, path=a.path, tile_records=a.tile, knobs=knobs)} {ms:.3f} ms "
           f"{nbytes / ms / 1e6:.0f} GB/s", flush=True)
     del sb, db
