@@ -444,8 +444,16 @@ def roundtrip_check(ctx, maps, src, dst, pairs):
         if a != b:
             llama.copy(maps[b], dst[b], maps[a], dst[a], stream=ctx.stream, path="naive")
         torch.cuda.synchronize()
-        ok = ok and all(torch.equal(x, y) for x, y in zip(dst[a], src[a]))
+        ok = ok and all(blobs_equal(torch, x, y) for x, y in zip(dst[a], src[a]))
     return bool(ctx.min_over_ranks(1.0 if ok else 0.0) > 0.5)
+
+
+def blobs_equal(torch, x, y, chunk=1 << 30):
+    """Byte equality of two device blobs in 1 GiB chunks (C3's views leave no
+    room for a full-size comparison temporary)."""
+    if x.numel() != y.numel():
+        return False
+    return all(torch.equal(x[i:i + chunk], y[i:i + chunk]) for i in range(0, x.numel(), chunk))
 
 
 def measure_config(ctx, name, steps, warmup, headline=False):
@@ -752,7 +760,7 @@ def run_c5(args, world, rank, local):
         back = sm.alloc("cuda")
         llama.copy(dm, mine, sm, back, path="naive")
         torch.cuda.synchronize()
-        ok = torch.equal(back[0], ref[0])
+        ok = blobs_equal(torch, back[0], ref[0])
         for t in mine:
             t.fill_(0x5A)
         del ref, back
