@@ -34,9 +34,11 @@ MAPPINGS = {
     "aos_aligned": ("aos", 1, True),     # aligned AoS
     "soa_mb": ("soa_mb", 1, False),      # SoA multi-blob (reading #10: "SoA" := MB)
     "soa_sb": ("soa_sb", 1, False),      # SoA single-blob
+    "soa_sb_aligned": ("soa_sb", 1, True),  # sub-array starts rounded up to the leaf size (reading #9)
     "aosoa4": ("aosoa", 4, False),
     "aosoa8": ("aosoa", 8, False),
     "aosoa32": ("aosoa", 32, False),
+    "aosoa4_aligned": ("aosoa", 4, True),  # aligned offsets x L, aligned record size (reading #6)
     "one": ("one", 1, True),             # One: always the aligned record
 }
 
