@@ -50,7 +50,8 @@ TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 NOMINAL_HBM_GBS = 8000.0
 METRIC = "layout-copy GB/s (read+write) per mapping pair vs 8 TB/s HBM, 1/2/4/8 B200"
-KERNEL = {"permute": "k_permute_ws", "permute_direct": "k_permute_direct", "blobcopy": "k_bulkcopy",
+KERNEL = {"permute": "k_permute_ws", "permute_direct": "k_permute_direct", "permute_jit": "llb_jit_permute",
+          "blobcopy": "k_bulkcopy",
           "run": "k_run", "naive": "k_naive", "transpose": "k_transpose2d"}
 DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C4"
 
@@ -505,7 +506,7 @@ def measure_config(ctx, name, steps, warmup, headline=False):
     per_pair = []
     for j, (a, b) in enumerate(pairs):
         t = statistics.median(ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(steps))
-        path = plans[j]["path"] + ("_direct" if plans[j].get("direct") else "")
+        path = plans[j]["path"] + ("_direct" if plans[j].get("direct") else "") + ("_jit" if plans[j].get("jit") else "")
         per_pair.append({"src": a, "dst": b, "path": path, "kernel": KERNEL.get(path, path), "bytes": pair_bytes[j],
                          "ms": t, "gbs": pair_bytes[j] / (t * 1e6), "frac": pair_bytes[j] / (t * 1e6) / peak})
 

@@ -244,6 +244,13 @@ typedef enum {
   LLAMA_KNOB_TRANSPOSE_FIXED,  /* TRANSPOSE: two-leaf load pass for one 4- / 8-byte leaf size (1) */
   LLAMA_KNOB_TRANSPOSE_TABLE,  /* TRANSPOSE: per-CTA shared-memory leaf table (1) */
   LLAMA_KNOB_TRANSPOSE_RAW_TYPED, /* TRANSPOSE: typed 4-byte raw passes (1) */
+  LLAMA_KNOB_JIT,              /* PERMUTE: plan-time specialised kernel (NVRTC): 0 off, 1 wide records (> 16
+                                  leaves) and splits, 2 every eligible pair (1) */
+  LLAMA_KNOB_JIT_TILE,         /* JIT: records per tile, 32 / 64 / 128 / 256 / 512 (~12 KB SoA source tiles,
+                                  else ~64 KB of images per tile) */
+  LLAMA_KNOB_JIT_STAGES,       /* JIT: source stages 2..6 (SoA source: 2; else 3 while <= 180 KB, else 2) */
+  LLAMA_KNOB_JIT_DST_BUFS,     /* JIT: destination image buffers 2..4 (3 while <= 180 KB, else 2) */
+  LLAMA_KNOB_JIT_RESERVED,     /* reserved (no effect) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 
@@ -270,10 +277,19 @@ typedef struct {
   uint64_t dst_bytes;       /* sum of destination blob sizes */
   int32_t word_moves;       /* PERMUTE: > 0 if AoS <-> AoS word mode is used (words per record) */
   int32_t direct;           /* PERMUTE: 1 = direct variant (AoS side through TMA, SoA side element-wise) */
+  int32_t jit;              /* PERMUTE: 1 = plan-time specialised kernel (NVRTC-compiled move program) */
 } llama_plan_info;
 
 llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_map,
                         const llama_copy_options* options, llama_plan_info* out);
+
+/* The generated CUDA source of the plan-time specialised kernel the planner
+ * chose for a pair (llama_plan_info.jit == 1), for inspection and tests: the
+ * NUL-terminated text is copied into buf (truncated to capacity - 1 bytes);
+ * *length (may be NULL) receives the full length.  INVALID_ARGUMENT when the
+ * plan is not a JIT plan.  No device work. */
+llama_status llama_plan_source(const llama_mapping* src_map, const llama_mapping* dst_map,
+                               const llama_copy_options* options, char* buf, uint64_t capacity, uint64_t* length);
 
 /* Seeded synthetic input (an input recipe, not the method): fills every blob
  * byte with pad_byte, then writes byte b of leaf k of record i as byte b

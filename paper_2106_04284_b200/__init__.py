@@ -36,7 +36,8 @@ EXPORTS = ["llama_mapping_create", "llama_mapping_create_from_schema", "llama_ma
            "llama_trace_byte_hits", "llama_trace_reset",
            "llama_mapping_destroy",
            "llama_blob_count", "llama_blob_sizes", "llama_record_count", "llama_leaf_types",
-           "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_generate",
+           "llama_blob_nr_and_offset", "llama_copy", "llama_copy_ex", "llama_plan", "llama_plan_source",
+           "llama_generate",
            "llama_launch_count", "llama_status_string", "llama_last_error_message", "llama_version",
            "llama_stager_create", "llama_stager_destroy", "llama_copy_staged", "llama_copy_staged_batch",
            "llama_nbody_move_staged", "llama_nbody_move",
@@ -67,14 +68,15 @@ class _Options(ctypes.Structure):
 KNOBS = ["tile_bytes", "smem_budget", "stages", "dst_bufs", "ws_order", "no_tma", "permute_v1", "no_pdl",
          "word_mode", "direct", "direct_stages", "direct_async", "direct_phase", "direct_staging",
          "direct_chunks", "direct_mix", "bulk_chunk", "bulk_stages", "blobcopy_lsu", "transpose_raw",
-         "transpose_linear", "transpose_raw1", "transpose_fixed", "transpose_table", "transpose_raw_typed"]
+         "transpose_linear", "transpose_raw1", "transpose_fixed", "transpose_table", "transpose_raw_typed",
+         "jit", "jit_tile", "jit_stages", "jit_dst_bufs", "jit_reserved"]
 
 
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("moves", ctypes.c_int32), ("tma", ctypes.c_int32), ("src_bytes", ctypes.c_uint64),
                 ("dst_bytes", ctypes.c_uint64), ("word_moves", ctypes.c_int32),
-                ("direct", ctypes.c_int32)]
+                ("direct", ctypes.c_int32), ("jit", ctypes.c_int32)]
 
 
 def _load():
@@ -107,6 +109,8 @@ def _load():
     lib.llama_copy.argtypes = [ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p]
     lib.llama_copy_ex.argtypes = [ctypes.c_void_p, vpp, ctypes.c_void_p, vpp, ctypes.c_void_p, P(_Options)]
     lib.llama_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(_Options), P(_PlanInfo)]
+    lib.llama_plan_source.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(_Options), ctypes.c_char_p, ctypes.c_uint64,
+                                      P(ctypes.c_uint64)]
     lib.llama_generate.argtypes = [ctypes.c_void_p, vpp, ctypes.c_uint64, ctypes.c_uint8, ctypes.c_void_p]
     lib.llama_stager_create.argtypes = [ctypes.c_uint64, P(ctypes.c_void_p)]
     lib.llama_stager_destroy.argtypes = [ctypes.c_void_p]
@@ -389,7 +393,18 @@ def plan(src_map, dst_map, path=None, tile_records=0, knobs=None):
     _check(_lib.llama_plan(src_map.handle, dst_map.handle, ctypes.byref(opt), ctypes.byref(info)))
     return {"path": PATH_NAMES[info.path], "tile_records": info.tile_records, "smem_bytes": info.smem_bytes,
             "moves": info.moves, "tma": bool(info.tma), "src_bytes": int(info.src_bytes),
-            "dst_bytes": int(info.dst_bytes), "word_moves": int(info.word_moves), "direct": bool(info.direct)}
+            "dst_bytes": int(info.dst_bytes), "word_moves": int(info.word_moves), "direct": bool(info.direct),
+            "jit": bool(info.jit)}
+
+
+def plan_source(src_map, dst_map, path=None, tile_records=0, knobs=None):
+    """The generated CUDA source of the pair's plan-time specialised kernel."""
+    opt = _options(path, tile_records, knobs)
+    n = ctypes.c_uint64(0)
+    _check(_lib.llama_plan_source(src_map.handle, dst_map.handle, ctypes.byref(opt), None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(_lib.llama_plan_source(src_map.handle, dst_map.handle, ctypes.byref(opt), buf, n.value + 1, None))
+    return buf.value.decode()
 
 
 def generate(m, blobs, seed=42, pad_byte=0, stream=None):

@@ -17,7 +17,27 @@ STAMP = LIB + ".stamp"  # content hash of the sources + flags the library was bu
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + BUILD, "-I/usr/local/cuda/include"]
+
+
+# device sources compiled at plan time by NVRTC (jit.cpp), embedded as strings
+JIT_EMBED = [("kJitParamsSrc", "jit_params.h"), ("kJitKernelSrc", "jit_kernel.cuh")]
+
+
+def _write_embed():
+    """build/jit_embed.inc: the NVRTC-compiled device sources as C++ raw strings."""
+    os.makedirs(BUILD, exist_ok=True)
+    out = []
+    for name, fn in JIT_EMBED:
+        with open(os.path.join(CSRC, fn)) as f:
+            text = f.read()
+        assert ')LLBJIT"' not in text
+        out.append(f'static const char {name}[] = R"LLBJIT({text})LLBJIT";\n')
+    path = os.path.join(BUILD, "jit_embed.inc")
+    data = "".join(out)
+    if not os.path.exists(path) or open(path).read() != data:
+        with open(path, "w") as f:
+            f.write(data)
 
 
 def _sources():
@@ -52,6 +72,7 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     digest = source_hash()
+    _write_embed()
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
@@ -72,7 +93,7 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1,5 +1,6 @@
 // capi.cpp -- the C ABI (include/llama_b200.h): validation, plan cache,
 // launches.  No C++ exception crosses this boundary.
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -205,12 +206,40 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
       out->tma = (int32_t)plan->perm->tma;
       out->word_moves = (int32_t)plan->perm->n_wmoves;
     }
+    if (plan->jit) {
+      out->tile_records = (int32_t)plan->jit->T;
+      out->smem_bytes = plan->smem_bytes;
+      out->moves = (int32_t)plan->jit->parts;
+      out->tma = 1;
+      out->jit = 1;
+    }
     if (plan->direct) {
       out->tile_records = (int32_t)plan->direct->T;
       out->smem_bytes = plan->smem_bytes;
       out->moves = (int32_t)plan->direct->K;
       out->tma = 1;
       out->direct = 1;
+    }
+    return LLAMA_OK;
+  } catch (...) {
+    return fail(LLAMA_ERR_OOM, "planning failed");
+  }
+}
+
+llama_status llama_plan_source(const llama_mapping* src_map, const llama_mapping* dst_map,
+                               const llama_copy_options* options, char* buf, uint64_t capacity, uint64_t* length) {
+  if (!src_map || !dst_map) return fail(LLAMA_ERR_INVALID_ARGUMENT, "NULL argument");
+  try {
+    std::shared_ptr<llb::Plan> plan;
+    llama_status st = get_plan(src_map->m, dst_map->m, options, &plan);
+    if (st != LLAMA_OK) return st;
+    if (!plan->jit) return fail(LLAMA_ERR_INVALID_ARGUMENT, "the plan is not a plan-time specialised kernel");
+    const std::string& src = plan->jit->source;
+    if (length) *length = src.size();
+    if (buf && capacity) {
+      const size_t n = std::min<size_t>(src.size(), capacity - 1);
+      std::memcpy(buf, src.data(), n);
+      buf[n] = '\0';
     }
     return LLAMA_OK;
   } catch (...) {
@@ -293,6 +322,10 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
         break;
       }
       case LLAMA_PATH_PERMUTE: {
+        if (plan->jit) {
+          e = llb::launch_jit(*plan->jit, s, src_blobs, d, dst_blobs, plan->pdl, stream);
+          break;
+        }
         if (plan->direct) {
           llb::DirectParams q = *plan->direct;
           for (int b = 0; b < s.nblobs(); ++b) q.blobs[0][b] = static_cast<uint8_t*>(const_cast<void*>(src_blobs[b]));

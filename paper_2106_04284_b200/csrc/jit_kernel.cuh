@@ -1,0 +1,201 @@
+// jit_kernel.cuh -- device skeleton of the plan-time specialised permute
+// (DESIGN.md "k_jit_permute").  NOT compiled by nvcc: _build.py embeds this
+// file (and jit_params.h) as strings into the library, and jit.cpp compiles
+// them with NVRTC for sm_100a together with the code it generates for one
+// mapping pair: the tile geometry as macros, the TMA segment list of the
+// AoS-like parts, the cp.async chunk table of the SoA source leaves, and the
+// per-record move program llb_permute (straight-line loads / byte permutes /
+// stores with compile-time offsets -- the paper's compile-time specialised
+// copies, specialised at plan time instead).
+//
+// Generated: the macros LLB_T, LLB_NS, LLB_ND, LLB_SSTAGE, LLB_DSTAGE,
+// LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_P (before this file) and, at the
+// LLB_GENERATED marker, llb_ctab[] (SoA source chunks: smem offset | log2 s_k
+// << 18 | leaf << 20), llb_src_tma(), llb_dst_tma(), llb_permute().
+//
+// Roles (warp-specialised like k_permute_ws):
+//   producer warp  source tile i+NS: TMA bulk loads of the AoS-like parts
+//                  (lane 0, expect_tx) and 16-byte cp.async chunks of every
+//                  SoA leaf's T * s_k run (all 32 lanes; completion counted on
+//                  the same mbarrier with cp.async.mbarrier.arrive.noinc);
+//                  destination tile i: TMA bulk stores of the AoS-like parts.
+//   8 consumer warps  wait for the source stage, run llb_permute for their
+//                  records (lane = record) and program part (warp % P), hand
+//                  the stage back; SoA destination leaves are stored straight
+//                  to global memory by llb_permute (coalesced: lane = record).
+// The last partial tile (and AoSoA tail lanes) is moved element-wise through
+// the normal form by the consumers of the last CTA.
+
+#define LLB_CONS 256
+
+extern __shared__ __align__(128) uint8_t llb_smem[];
+
+__device__ __forceinline__ uint32_t llb_sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void llb_mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(llb_sa(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void llb_mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nLLBW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra LLBW_%=;\n}" ::"r"(
+          llb_sa(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void llb_mbar_wait_sleep(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nLLBS_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t@!p bra LLBS_%=;\n}" ::"r"(
+          llb_sa(b)),
+      "r"(ph), "r"(20000)
+      : "memory");
+}
+__device__ __forceinline__ void llb_mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(llb_sa(b)) : "memory");
+}
+__device__ __forceinline__ void llb_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(llb_sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void llb_g2s(void* s, const void* g, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(llb_sa(s)),
+               "l"(g), "r"(bytes), "r"(llb_sa(b))
+               : "memory");
+}
+__device__ __forceinline__ void llb_s2g(void* g, const void* s, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(llb_sa(s)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void llb_cp16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(llb_sa(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void llb_cp_arrive_noinc(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(llb_sa(b)) : "memory");
+}
+__device__ __forceinline__ void llb_cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(LLB_CONS) : "memory"); }
+
+// streaming global stores of the SoA destination elements (written once)
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint8_t v) { asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint16_t v) { asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint32_t v) { asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint64_t v) { asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory"); }
+
+__device__ __forceinline__ uint64_t llb_nf(const LlbJitLeaf& l, uint64_t i) {
+  const uint64_t q = i / l.L;
+  return l.base + q * l.B + l.F + (i - q * l.L) * l.size;
+}
+
+// ==== LLB_GENERATED ====
+
+extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_permute(const __grid_constant__ LlbJitParams p) {
+  uint64_t* full = reinterpret_cast<uint64_t*>(llb_smem);
+  uint64_t* empty = full + 8;
+  uint64_t* dfull = full + 16;
+  uint64_t* dempty = full + 24;
+  uint8_t* sring = llb_smem + 256;
+  uint8_t* dring = sring + LLB_NS * LLB_SSTAGE;
+  // per leaf: the SoA source element-0 pointer minus the leaf's segment offset
+  // in the stage, so a chunk's global address is sgs[k] + soff + (t0 << lg)
+  const uint8_t** sgs = reinterpret_cast<const uint8_t**>(dring + LLB_ND * LLB_DSTAGE);
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(sgs + LLB_JIT_MAX_LEAVES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < LLB_NS; ++s) {
+      llb_mbar_init(&full[s], 32);  // the producer lanes' cp.async arrivals (+ TMA bytes)
+      llb_mbar_init(&empty[s], 1);
+    }
+    for (int d = 0; d < (LLB_ND > 0 ? LLB_ND : 1); ++d) {
+      llb_mbar_init(&dfull[d], 1);
+      llb_mbar_init(&dempty[d], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // destination images: padding bytes are never written by the program, so
+  // they stay 0 (reading #12)
+  for (uint32_t o = 16 * tid; o < LLB_ND * LLB_DSTAGE; o += 16 * (LLB_CONS + 32))
+    *reinterpret_cast<uint4*>(dring + o) = make_uint4(0, 0, 0, 0);
+  for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
+  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) sgs[k] = p.sg[k] - llb_seg[k];
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (blockIdx.x == 0 && warp < LLB_CONS / 32)
+    for (uint32_t g = 0; g < p.n_gaps; ++g)
+      for (uint32_t o = tid; o < p.gap_len[g]; o += LLB_CONS) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
+
+  const uint64_t first = blockIdx.x, stride = gridDim.x;
+  const uint32_t n_my = first < p.n_full ? (uint32_t)((p.n_full - first + stride - 1) / stride) : 0;
+
+  if (warp == LLB_CONS / 32) {  // ------------------------------------ producer
+    auto issue = [&](uint32_t i, uint32_t s) {
+      const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
+      uint8_t* stage = sring + s * LLB_SSTAGE;
+      if (LLB_SRC_TMA > 0 && lane == 0) {
+        llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
+        llb_src_tma(p, stage, t0, &full[s]);
+      }
+      for (uint32_t c = lane; c < LLB_NCHUNK; c += 32) {
+        const uint32_t e = ctab[c], so = e & 0x3FFFFu;
+        llb_cp16(stage + so, sgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)));
+      }
+      llb_cp_arrive_noinc(&full[s]);
+    };
+    for (uint32_t i = 0; i < LLB_NS && i < n_my; ++i) issue(i, i);
+    uint32_t s = 0, sph = 0, d = 0, dph = 0;
+    for (uint32_t i = 0; i < n_my; ++i) {
+      llb_mbar_wait_sleep(&empty[s], sph);
+      if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
+      if (LLB_ND > 0) {
+        if (lane == 0) {
+          const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
+          llb_mbar_wait_sleep(&dfull[d], dph);
+          llb_dst_tma(p, dring + d * LLB_DSTAGE, t0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          llb_mbar_arrive(&dempty[d]);
+        }
+        if (++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
+      }
+      if (++s == LLB_NS) { s = 0; sph ^= 1; }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
+  // ------------------------------------------------------------- consumers
+  const uint32_t part = (uint32_t)warp % LLB_P, grp = (uint32_t)warp / LLB_P;
+  uint32_t s = 0, sph = 0, d = 0, dph = 0;
+  for (uint32_t i = 0; i < n_my; ++i) {
+    const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
+    if (tid == 0) {
+      llb_mbar_wait(&full[s], sph);
+      if (LLB_ND > 0 && i >= (uint32_t)LLB_ND) llb_mbar_wait(&dempty[d], dph ^ 1);
+    }
+    llb_cons_sync();
+    const uint8_t* sim = sring + s * LLB_SSTAGE;
+    uint8_t* dim = dring + d * LLB_DSTAGE;
+    for (uint32_t r = grp * 32 + lane; r < LLB_T; r += (LLB_CONS / LLB_P)) llb_permute(p, sim, dim, t0, part, r);
+    if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    llb_cons_sync();
+    if (tid == 0) {
+      llb_mbar_arrive(&empty[s]);
+      if (LLB_ND > 0) llb_mbar_arrive(&dfull[d]);
+    }
+    if (++s == LLB_NS) { s = 0; sph ^= 1; }
+    if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
+  }
+  // --------------------------------------- the last partial tile (element-wise)
+  const uint64_t t_tail = p.n_full * LLB_T;
+  if (blockIdx.x == gridDim.x - 1 && t_tail < p.N) {
+    for (uint32_t z = 0; z < p.n_zero; ++z)
+      for (uint64_t o = tid; o < p.zero_len[z]; o += LLB_CONS) p.blobs[1][p.zero_blob[z]][p.zero_off[z] + o] = 0;
+    llb_cons_sync();
+    const uint64_t n = (p.N - t_tail) * p.K;
+    for (uint64_t x = tid; x < n; x += LLB_CONS) {
+      const uint64_t i = t_tail + x / p.K;
+      const uint32_t k = (uint32_t)(x % p.K);
+      const LlbJitLeaf& a = p.leaf[0][k];
+      const LlbJitLeaf& b = p.leaf[1][k];
+      const uint8_t* sp = p.blobs[0][a.blob] + llb_nf(a, i);
+      uint8_t* dp = p.blobs[1][b.blob] + llb_nf(b, i);
+      for (uint32_t j = 0; j < a.size; ++j) dp[j] = sp[j];
+    }
+  }
+}

@@ -670,6 +670,16 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, const Kn
   return true;
 }
 
+// The plan-time specialised permute (jit.cpp) for wide records and splits.
+bool plan_jit_path(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why) {
+  std::unique_ptr<JitPlan> jp(new JitPlan);
+  if (!plan_jit(s, d, tile_records, kn, jp.get(), why)) return false;
+  p->path = LLAMA_PATH_PERMUTE;
+  p->smem_bytes = (int)jp->smem;
+  p->jit = std::move(jp);
+  return true;
+}
+
 llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int tile_records, const Knobs& kn,
                        Plan* out, std::string* err) {
   out->permute_v1 = kn.get(LLAMA_KNOB_PERMUTE_V1, 0) != 0;
@@ -712,6 +722,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       // identities of SoA layouts with many leaves (many blobs / segments): the bulk blob copy
       // (HEP SoA MB: 6.4 TB/s vs 1.8 for 200 TMA segment ops per tile)
       if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
+      if (plan_jit_path(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_direct(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
@@ -728,6 +739,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       if (plan_run(s, d, out, &why)) return LLAMA_OK;
       break;
     case LLAMA_PATH_PERMUTE:
+      if (plan_jit_path(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_direct(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       break;

@@ -6,6 +6,7 @@
 #include <memory>
 #include <string>
 
+#include "jit.hpp"
 #include "mapping.hpp"
 #include "params.hpp"
 
@@ -40,6 +41,7 @@ struct Plan {
   std::unique_ptr<RunParams> run;
   std::unique_ptr<PermParams> perm;
   std::unique_ptr<DirectParams> direct;  // PERMUTE path, direct variant (AoS <-> SoA, many leaves)
+  std::unique_ptr<JitPlan> jit;          // PERMUTE path, plan-time specialised kernel (wide records, splits)
 };
 
 // Checks S:484-486 (same leaf types, same extents).

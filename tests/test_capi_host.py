@@ -62,8 +62,9 @@ def test_knobs_change_the_plan_and_key_the_cache():
     assert not llama.plan(a, b, knobs={"no_tma": 1})["tma"]
     h = llama.Mapping(W.HEP100, [4096], "aos", 1, True)
     hs = llama.Mapping(W.HEP100, [4096], "soa_mb")
-    assert llama.plan(h, hs)["direct"]
-    assert not llama.plan(h, hs, knobs={"direct": 0})["direct"]
+    assert llama.plan(h, hs)["jit"]
+    assert llama.plan(h, hs, knobs={"jit": 0})["direct"]
+    assert not llama.plan(h, hs, knobs={"jit": 0, "direct": 0})["direct"]
 
 
 def test_library_is_sm100a_only():
@@ -297,3 +298,29 @@ def test_linearizer_errors_and_plans():
     b = llama.Mapping(sizes[2:], [4], "aos")
     with pytest.raises(llama.LlamaError, match="INVALID_ARGUMENT"):
         llama.Mapping.split(a, b, [0, 1])
+
+
+def test_jit_plans_compile_without_spills():
+    """The plan-time specialised kernels of the C3 pairs compile on the host
+    (NVRTC needs no GPU) and their generated source, compiled again by ptxas,
+    spills nothing."""
+    import subprocess
+    import tempfile
+    m = {k: llama.Mapping(W.HEP100, [1 << 20], *W.MAPPINGS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
+    with tempfile.TemporaryDirectory() as tmp:
+        for a in m:
+            for b in m:
+                if a == b:
+                    continue
+                pl = llama.plan(m[a], m[b])
+                assert pl["jit"] and pl["path"] == "permute", (a, b, pl)
+                src = llama.plan_source(m[a], m[b])
+                assert "llb_jit_permute" in src
+                fn = os.path.join(tmp, f"{a}_{b}.cu")
+                with open(fn, "w") as f:
+                    f.write(src)
+                r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin",
+                                    "-std=c++17", "-Xptxas", "-v", "-o", fn + ".cubin", fn],
+                                   capture_output=True, text=True)
+                assert r.returncode == 0, r.stderr[-2000:]
+                assert "0 bytes spill stores, 0 bytes spill loads" in r.stderr, (a, b, r.stderr[-600:])

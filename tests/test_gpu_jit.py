@@ -1,0 +1,81 @@
+"""GPU parity of the plan-time specialised permute (k_jit_permute: a move
+program generated per mapping pair and compiled with NVRTC), byte
+for byte against the oracle: every ordered pair of the HEP100 kinds (the
+paper's 100-leaf event records), ragged extents (full tiles, a partial
+last tile, fewer records than a tile, AoSoA tail lanes), small records forced
+onto it (knob jit=2), splits, every tile size and stage count."""
+import numpy as np
+import pytest
+
+import workloads as W
+from test_gpu_parity import KINDS, run_case, run_spec_case
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def llama():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_04284_b200 as m
+    return m
+
+
+HEP_KINDS = ["aos", "aos_aligned", "soa_mb", "soa_sb", "aosoa8", "aosoa32", "aosoa8_aligned"]
+
+
+@pytest.mark.parametrize("n", [1, 31, 64, 65, 1000, 4097, 100_003])
+def test_hep100_pairs_jit(llama, oracle_mod, n):
+    for a in HEP_KINDS:
+        for b in HEP_KINDS:
+            if a == b:
+                continue
+            sm = llama.Mapping(W.HEP100, [n], *KINDS[a])
+            dm = llama.Mapping(W.HEP100, [n], *KINDS[b])
+            pl = llama.plan(sm, dm, path="permute", knobs={"jit": 2})
+            if "soa_sb" not in (a, b):  # SB sub-arrays of N * s_k bytes start 16-byte aligned only for some N
+                assert pl["jit"], (a, b, pl)
+            run_case(llama, oracle_mod, W.HEP100, [n], KINDS[a], KINDS[b], seed=3 + n, paths=("permute",),
+                     knobs={"jit": 2})
+
+
+@pytest.mark.parametrize("schema_name", ["particle7", "listing1"])
+@pytest.mark.parametrize("n", [1, 33, 4097, 70_001])
+def test_small_records_forced_jit(llama, oracle_mod, schema_name, n):
+    """Small records through the JIT kernel (knob jit=2): every eligible pair
+    of the 11 kinds; ineligible pairs fall back to the other kernels."""
+    schema = W.SCHEMAS[schema_name]
+    for a in KINDS:
+        for b in KINDS:
+            run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b], seed=5 + n, paths=("permute",),
+                     knobs={"jit": 2})
+
+
+@pytest.mark.parametrize("knobs", [{"jit_tile": 32}, {"jit_tile": 64}, {"jit_tile": 128}, {"jit_stages": 3},
+                                   {"jit_stages": 4, "jit_dst_bufs": 3}, {"jit_tile": 256}, {"jit_stages": 2, "jit_dst_bufs": 2}])
+def test_jit_geometry_knobs(llama, oracle_mod, knobs):
+    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos_aligned"), ("aos", "aos_aligned"), ("soa_sb", "aosoa8")]:
+        run_case(llama, oracle_mod, W.HEP100, [20_011], KINDS[a], KINDS[b], seed=9, paths=("permute",),
+                 knobs=dict(knobs, jit=2))
+
+
+@pytest.mark.parametrize("n", [100, 4097, 50_000])
+def test_splits_jit(llama, oracle_mod, n):
+    """Split mappings through the JIT kernel: the parts' images side
+    by side, AoS-like parts by TMA, SoA leaves by cp.async chunks / direct stores."""
+    cases = [("hep100", "aos", "split_hep"), ("hep100", "split_hep", "soa_mb"), ("hep100", "split_hep", "aos"),
+             ("particle7", "aos", "split_p7"), ("particle7", "split_p7", "soa_mb"), ("listing1", "split_pos", "aos_aligned")]
+    for schema_name, a, b in cases:
+        schema = W.SCHEMAS[schema_name]
+        run_spec_case(llama, oracle_mod, schema, [n], W.resolve_spec(a), W.resolve_spec(b), seed=n,
+                      knobs={"jit": 2}, paths=("permute",))
+
+
+def test_jit_chosen_for_wide_records(llama):
+    m = {k: llama.Mapping(W.HEP100, [1 << 16], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
+    for a in m:
+        for b in m:
+            if a != b:
+                assert llama.plan(m[a], m[b])["jit"], (a, b)

@@ -263,7 +263,7 @@ def test_staged_copy_batch(llama, oracle_mod, cap):
 
 
 # ------------------------------------------------------------ One / Split (f1)
-def run_spec_case(llama, oracle, schema, ext, s_spec, d_spec, seed=7, pad=0xCD):
+def run_spec_case(llama, oracle, schema, ext, s_spec, d_spec, seed=7, pad=0xCD, knobs=None, paths=None):
     """run_case for workloads spec trees (MAPPINGS tuples or split trees)."""
     sm = llama.Mapping.from_spec(schema, ext, s_spec)
     dm = llama.Mapping.from_spec(schema, ext, d_spec)
@@ -275,16 +275,16 @@ def run_spec_case(llama, oracle, schema, ext, s_spec, d_spec, seed=7, pad=0xCD):
     for j, t in enumerate(sb):
         assert np.array_equal(_host(t), src_host[j]), f"generated source differs in blob {j}"
     exp = oracle.copy(so, src_host, do)
-    for path in ALL_PATHS:
+    for path in (paths or ALL_PATHS):
         if path != "auto":
             try:
-                llama.plan(sm, dm, path=path)
+                llama.plan(sm, dm, path=path, knobs=knobs)
             except llama.LlamaError:
                 continue
         db = dm.alloc("cuda")
         for t in db:
             t.fill_(0x5A)
-        llama.copy(sm, sb, dm, db, path=path)
+        llama.copy(sm, sb, dm, db, path=path, knobs=knobs)
         torch.cuda.synchronize()
         for j, t in enumerate(db):
             got = _host(t)
@@ -340,7 +340,7 @@ def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async):
     AoS with the cp.async classes (with and without the staged misaligned
     classes and the 16-byte chunk-staged 1- / 2-byte classes) and with
     registers only."""
-    knobs = {"direct": 2, "direct_async": 0 if use_async == "0" else 1,
+    knobs = {"jit": 0, "direct": 2, "direct_async": 0 if use_async == "0" else 1,
              "direct_staging": 0 if use_async == "nostage" else 1,
              "direct_chunks": 0 if use_async == "nochunk" else 1}
     schema = W.SCHEMAS[schema_name]
@@ -355,13 +355,14 @@ def test_direct_variant_forced(llama, oracle_mod, schema_name, n, use_async):
             run_case(llama, oracle_mod, schema, [n], KINDS[a], KINDS[b], knobs=knobs)
 
 
-def test_direct_chosen_for_hep(llama):
+def test_direct_chosen_for_hep_without_jit(llama):
     m = {k: llama.Mapping(W.HEP100, [4096], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
-    assert llama.plan(m["aos_aligned"], m["soa_mb"])["direct"]
-    assert llama.plan(m["soa_mb"], m["aos_aligned"])["direct"]
-    assert llama.plan(m["aos"], m["soa_mb"])["direct"]  # packed: funnel-shifted gathers
-    assert llama.plan(m["soa_mb"], m["aos"])["direct"]  # packed destination: staged misaligned classes
-    assert not llama.plan(m["aos"], m["aos_aligned"])["direct"]
+    kn = {"jit": 0}
+    assert llama.plan(m["aos_aligned"], m["soa_mb"], knobs=kn)["direct"]
+    assert llama.plan(m["soa_mb"], m["aos_aligned"], knobs=kn)["direct"]
+    assert llama.plan(m["aos"], m["soa_mb"], knobs=kn)["direct"]  # packed: funnel-shifted gathers
+    assert llama.plan(m["soa_mb"], m["aos"], knobs=kn)["direct"]  # packed destination: staged misaligned classes
+    assert not llama.plan(m["aos"], m["aos_aligned"], knobs=kn)["direct"]
 
 
 def test_c5_symmetric_memory_path_one_rank(llama):
