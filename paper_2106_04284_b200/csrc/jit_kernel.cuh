@@ -9,7 +9,7 @@
 // copies, specialised at plan time instead).
 //
 // Generated: the macros LLB_T, LLB_NS, LLB_ND, LLB_SSTAGE, LLB_DSTAGE,
-// LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_P (before this file) and, at the
+// LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_P, LLB_G (before this file) and, at the
 // LLB_GENERATED marker, llb_ctab[] (SoA source chunks: smem offset | log2 s_k
 // << 18 | leaf << 20), llb_src_tma(), llb_dst_tma(), llb_permute().
 //
@@ -171,7 +171,8 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
     llb_cons_sync();
     const uint8_t* sim = sring + s * LLB_SSTAGE;
     uint8_t* dim = dring + d * LLB_DSTAGE;
-    for (uint32_t r = grp * 32 + lane; r < LLB_T; r += (LLB_CONS / LLB_P)) llb_permute(p, sim, dim, t0, part, r);
+    // r = a group of LLB_G consecutive records (lane = group)
+    for (uint32_t r = grp * 32 + lane; r < LLB_T / LLB_G; r += (LLB_CONS / LLB_P)) llb_permute(p, sim, dim, t0, part, r);
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     llb_cons_sync();
     if (tid == 0) {

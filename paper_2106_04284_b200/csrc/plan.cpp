@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 namespace llb {
@@ -673,7 +674,12 @@ bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, const Kn
 // The plan-time specialised permute (jit.cpp) for wide records and splits.
 bool plan_jit_path(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why) {
   std::unique_ptr<JitPlan> jp(new JitPlan);
-  if (!plan_jit(s, d, tile_records, kn, jp.get(), why)) return false;
+  if (!plan_jit(s, d, tile_records, kn, jp.get(), why)) {
+#ifdef LLB_DEBUG_JIT
+    std::fprintf(stderr, "plan_jit: %s\n", why->c_str());
+#endif
+    return false;
+  }
   p->path = LLAMA_PATH_PERMUTE;
   p->smem_bytes = (int)jp->smem;
   p->jit = std::move(jp);

@@ -300,27 +300,36 @@ def test_linearizer_errors_and_plans():
         llama.Mapping.split(a, b, [0, 1])
 
 
+def _jit_cases():
+    m = {k: llama.Mapping(W.HEP100, [1 << 20], *W.MAPPINGS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
+    cases = [(f"hep_{a}_{b}", m[a], m[b], None) for a in m for b in m if a != b]
+    l1 = {k: llama.Mapping(W.LISTING1, [1 << 20], *W.MAPPINGS[k]) for k in ("aos", "soa_mb", "aosoa32", "soa_sb")}
+    cases += [(f"l1_{a}_{b}", l1[a], l1[b], {"jit": 2}) for a, b in
+              [("aos", "soa_mb"), ("soa_mb", "aos"), ("aosoa32", "soa_sb"), ("aosoa32", "aos")]]
+    for schema, a, b in [(W.LISTING1, "aos", "split_pos"), (W.HEP100, "aos", "split_hep"), (W.HEP100, "split_hep", "soa_mb"),
+                         (W.PARTICLE7, "split_p7", "aos")]:
+        cases.append((f"split_{a}_{b}", llama.Mapping.from_spec(schema, [1 << 20], W.resolve_spec(a)),
+                      llama.Mapping.from_spec(schema, [1 << 20], W.resolve_spec(b)), None))
+    return cases
+
+
 def test_jit_plans_compile_without_spills():
-    """The plan-time specialised kernels of the C3 pairs compile on the host
-    (NVRTC needs no GPU) and their generated source, compiled again by ptxas,
-    spills nothing."""
+    """The plan-time specialised kernels of the C3 pairs, Listing-1 pairs (odd
+    record strides: 4-record groups) and splits compile on the host (NVRTC needs
+    no GPU) and their generated source, compiled again by ptxas, spills
+    nothing."""
     import subprocess
     import tempfile
-    m = {k: llama.Mapping(W.HEP100, [1 << 20], *W.MAPPINGS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
     with tempfile.TemporaryDirectory() as tmp:
-        for a in m:
-            for b in m:
-                if a == b:
-                    continue
-                pl = llama.plan(m[a], m[b])
-                assert pl["jit"] and pl["path"] == "permute", (a, b, pl)
-                src = llama.plan_source(m[a], m[b])
-                assert "llb_jit_permute" in src
-                fn = os.path.join(tmp, f"{a}_{b}.cu")
-                with open(fn, "w") as f:
-                    f.write(src)
-                r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin",
-                                    "-std=c++17", "-Xptxas", "-v", "-o", fn + ".cubin", fn],
-                                   capture_output=True, text=True)
-                assert r.returncode == 0, r.stderr[-2000:]
-                assert "0 bytes spill stores, 0 bytes spill loads" in r.stderr, (a, b, r.stderr[-600:])
+        for name, sm, dm, knobs in _jit_cases():
+            pl = llama.plan(sm, dm, knobs=knobs)
+            assert pl["jit"] and pl["path"] == "permute", (name, pl)
+            src = llama.plan_source(sm, dm, knobs=knobs)
+            assert "llb_jit_permute" in src
+            fn = os.path.join(tmp, name + ".cu")
+            with open(fn, "w") as f:
+                f.write(src)
+            r = subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin",
+                                "-std=c++17", "-Xptxas", "-v", "-o", fn + ".cubin", fn], capture_output=True, text=True)
+            assert r.returncode == 0, r.stderr[-2000:]
+            assert "0 bytes spill stores, 0 bytes spill loads" in r.stderr, (name, r.stderr[-600:])
