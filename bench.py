@@ -474,11 +474,9 @@ def measure_config(ctx, name, steps, warmup, headline=False):
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    clocks = None
-    if headline:
-        clocks = ClockSampler(ctx.local)
-        clocks.start()
-        time.sleep(0.3)
+    clocks = ClockSampler(ctx.local)  # every config: C3's 60-ms steps draw the most power
+    clocks.start()
+    time.sleep(0.3)
     ctx.barrier()
     torch.cuda.synchronize()
     l0 = llama.launch_count()
@@ -490,7 +488,7 @@ def measure_config(ctx, name, steps, warmup, headline=False):
     torch.cuda.synchronize()
     ctx.barrier()
     launches = llama.launch_count() - l0
-    clk = clocks.stop() if clocks else None
+    clk = clocks.stop()
     ms = ctx.max_over_ranks(t0.elapsed_time(t1) / steps)
     value = sum_over_ranks(ctx, step_bytes) / (ms * 1e-3) / 1e9  # every rank's bytes / the slowest rank's time
 
@@ -656,7 +654,7 @@ def run_ours(args, world, rank, local):
                 "min_pair_frac": {"frac": worst["frac"], "gbs": worst["gbs"], "config": worst["config"],
                                   "pair": f"{worst['src']}->{worst['dst']}", "kernel": worst["kernel"],
                                   "over_pairs": len(allp)},
-                "configs": {n: {k: v for k, v in r.items() if k not in ("clocks",)} for n, r in results.items()}}
+                "configs": results}
         print(json.dumps(line), flush=True)
         if args.per_pair:
             with open(args.per_pair, "w") as f:

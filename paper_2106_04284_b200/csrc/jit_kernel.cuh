@@ -77,6 +77,12 @@ __device__ __forceinline__ void llb_stg(uint8_t* p, uint8_t v) { asm volatile("s
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint16_t v) { asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory"); }
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint32_t v) { asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint64_t v) { asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 
 __device__ __forceinline__ uint64_t llb_nf(const LlbJitLeaf& l, uint64_t i) {
   const uint64_t q = i / l.L;
