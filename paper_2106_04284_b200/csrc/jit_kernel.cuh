@@ -151,12 +151,15 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
       if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
       if (LLB_ND > 0) {
         if (lane == 0) {
+          // store tile i, keep up to ND - 1 stores in flight: hand back the
+          // buffer of tile i - (ND - 1) once its store has read it out (the
+          // load issue of the next tiles never waits on a store)
           const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
           llb_mbar_wait_sleep(&dfull[d], dph);
           llb_dst_tma(p, dring + d * LLB_DSTAGE, t0);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          llb_mbar_arrive(&dempty[d]);
+          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(LLB_ND > 0 ? LLB_ND - 1 : 0) : "memory");
+          if (i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0)) llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
         }
         if (++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
       }
