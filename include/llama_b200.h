@@ -246,9 +246,8 @@ typedef enum {
   LLAMA_KNOB_TRANSPOSE_RAW_TYPED, /* TRANSPOSE: typed 4-byte raw passes (1) */
   LLAMA_KNOB_JIT,              /* PERMUTE: plan-time specialised kernel (NVRTC): 0 off, 1 wide records (> 16
                                   leaves) and splits, 2 every eligible pair (1) */
-  LLAMA_KNOB_JIT_TILE,         /* JIT: records per tile, 32 / 64 / 128 / 256 / 512 (~12 KB SoA source tiles,
-                                  else ~64 KB of images per tile) */
-  LLAMA_KNOB_JIT_STAGES,       /* JIT: source stages 2..6 (SoA source: 2; else 3 while <= 180 KB, else 2) */
+  LLAMA_KNOB_JIT_TILE,         /* JIT: records per tile, 32 / 64 / 128 / 256 / 512 (<= 64 KB of images per tile) */
+  LLAMA_KNOB_JIT_STAGES,       /* JIT: source stages 2..6 (3 while the ring fits 180 KB, else 2) */
   LLAMA_KNOB_JIT_DST_BUFS,     /* JIT: destination image buffers 2..4 (3 while <= 180 KB, else 2) */
   LLAMA_KNOB_JIT_RESERVED,     /* reserved (no effect) */
   LLAMA_KNOB_COUNT

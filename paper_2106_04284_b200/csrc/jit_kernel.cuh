@@ -13,16 +13,18 @@
 // LLB_GENERATED marker, llb_ctab[] (SoA source chunks: smem offset | log2 s_k
 // << 18 | leaf << 20), llb_src_tma(), llb_dst_tma(), llb_permute().
 //
-// Roles (warp-specialised like k_permute_ws):
-//   producer warp  source tile i+NS: TMA bulk loads of the AoS-like parts
-//                  (lane 0, expect_tx) and 16-byte cp.async chunks of every
-//                  SoA leaf's T * s_k run (all 32 lanes; completion counted on
-//                  the same mbarrier with cp.async.mbarrier.arrive.noinc);
-//                  destination tile i: TMA bulk stores of the AoS-like parts.
-//   8 consumer warps  wait for the source stage, run llb_permute for their
-//                  records (lane = record) and program part (warp % P), hand
-//                  the stage back; SoA destination leaves are stored straight
-//                  to global memory by llb_permute (coalesced: lane = record).
+// Roles:
+//   8 consumer warps  wait for source stage s, run llb_permute for their
+//                  records (lane = record group) and program part (warp % P);
+//                  SoA destination leaves are stored straight to global memory
+//                  by llb_permute (coalesced: lane = record); then, the stage
+//                  free, they issue source tile i+NS into it: TMA bulk loads of
+//                  the AoS-like parts (thread 0, expect_tx) and 16-byte
+//                  cp.async chunks of every SoA leaf's T * s_k run (all
+//                  threads; completion counted on the stage's mbarrier with
+//                  cp.async.mbarrier.arrive.noinc).
+//   store warp     TMA bulk stores of the AoS-like destination parts of each
+//                  tile, up to ND - 1 in flight.
 // The last partial tile (and AoSoA tail lanes) is moved element-wise through
 // the normal form by the consumers of the last CTA.
 
@@ -64,8 +66,11 @@ __device__ __forceinline__ void llb_s2g(void* g, const void* s, uint32_t bytes) 
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(llb_sa(s)), "r"(bytes)
                : "memory");
 }
+// (no "memory" clobber: the producer's chunk loop must be free to hoist the
+// next chunks' table loads above this one; the cp.async.mbarrier.arrive after
+// the loop orders the copies against the consumers)
 __device__ __forceinline__ void llb_cp16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(llb_sa(s)), "l"(g) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(llb_sa(s)), "l"(g));
 }
 __device__ __forceinline__ void llb_cp_arrive_noinc(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(llb_sa(b)) : "memory");
@@ -93,7 +98,6 @@ __device__ __forceinline__ uint64_t llb_nf(const LlbJitLeaf& l, uint64_t i) {
 
 extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_permute(const __grid_constant__ LlbJitParams p) {
   uint64_t* full = reinterpret_cast<uint64_t*>(llb_smem);
-  uint64_t* empty = full + 8;
   uint64_t* dfull = full + 16;
   uint64_t* dempty = full + 24;
   uint8_t* sring = llb_smem + 256;
@@ -104,10 +108,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   uint32_t* ctab = reinterpret_cast<uint32_t*>(sgs + LLB_JIT_MAX_LEAVES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < LLB_NS; ++s) {
-      llb_mbar_init(&full[s], 32);  // the producer lanes' cp.async arrivals (+ TMA bytes)
-      llb_mbar_init(&empty[s], 1);
-    }
+    for (int s = 0; s < LLB_NS; ++s) llb_mbar_init(&full[s], LLB_CONS);  // every consumer's cp.async arrival (+ TMA bytes)
     for (int d = 0; d < (LLB_ND > 0 ? LLB_ND : 1); ++d) {
       llb_mbar_init(&dfull[d], 1);
       llb_mbar_init(&dempty[d], 1);
@@ -130,45 +131,45 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   const uint64_t first = blockIdx.x, stride = gridDim.x;
   const uint32_t n_my = first < p.n_full ? (uint32_t)((p.n_full - first + stride - 1) / stride) : 0;
 
-  if (warp == LLB_CONS / 32) {  // ------------------------------------ producer
-    auto issue = [&](uint32_t i, uint32_t s) {
-      const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
-      uint8_t* stage = sring + s * LLB_SSTAGE;
-      if (LLB_SRC_TMA > 0 && lane == 0) {
-        llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
-        llb_src_tma(p, stage, t0, &full[s]);
-      }
-      for (uint32_t c = lane; c < LLB_NCHUNK; c += 32) {
-        const uint32_t e = ctab[c], so = e & 0x3FFFFu;
-        llb_cp16(stage + so, sgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)));
-      }
-      llb_cp_arrive_noinc(&full[s]);
-    };
-    for (uint32_t i = 0; i < LLB_NS && i < n_my; ++i) issue(i, i);
-    uint32_t s = 0, sph = 0, d = 0, dph = 0;
-    for (uint32_t i = 0; i < n_my; ++i) {
-      llb_mbar_wait_sleep(&empty[s], sph);
-      if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
-      if (LLB_ND > 0) {
-        if (lane == 0) {
-          // store tile i, keep up to ND - 1 stores in flight: hand back the
-          // buffer of tile i - (ND - 1) once its store has read it out (the
-          // load issue of the next tiles never waits on a store)
-          const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
-          llb_mbar_wait_sleep(&dfull[d], dph);
-          llb_dst_tma(p, dring + d * LLB_DSTAGE, t0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(LLB_ND > 0 ? LLB_ND - 1 : 0) : "memory");
-          if (i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0)) llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
-        }
+  if (warp == LLB_CONS / 32) {  // ------------------------------ store warp
+    if (LLB_ND > 0 && lane == 0) {
+      uint32_t d = 0, dph = 0;
+      for (uint32_t i = 0; i < n_my; ++i) {
+        // store tile i, keep up to ND - 1 stores in flight: hand back the
+        // buffer of tile i - (ND - 1) once its store has read it out
+        const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
+        llb_mbar_wait_sleep(&dfull[d], dph);
+        llb_dst_tma(p, dring + d * LLB_DSTAGE, t0);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(LLB_ND > 0 ? LLB_ND - 1 : 0) : "memory");
+        if (i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0)) llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
         if (++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
       }
-      if (++s == LLB_NS) { s = 0; sph ^= 1; }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     return;
   }
   // ------------------------------------------------------------- consumers
+  // Source tile i+NS goes into stage s as soon as every consumer has finished
+  // tile i there: TMA bulk loads of the AoS-like parts (thread 0, expect_tx)
+  // and the SoA leaves' 16-byte cp.async chunks spread over all 256 consumer
+  // threads (measured: one issuing warp per CTA capped a CTA at ~15 GB/s);
+  // each thread's cp.async.mbarrier.arrive.noinc counts on full[s].
+  auto issue = [&](uint32_t i, uint32_t s) {
+    const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
+    uint8_t* stage = sring + s * LLB_SSTAGE;
+    if (LLB_SRC_TMA > 0 && tid == 0) {
+      llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
+      llb_src_tma(p, stage, t0, &full[s]);
+    }
+#pragma unroll 4
+    for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS) {
+      const uint32_t e = ctab[c], so = e & 0x3FFFFu;
+      llb_cp16(stage + so, sgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)));
+    }
+    llb_cp_arrive_noinc(&full[s]);
+  };
+  for (uint32_t i = 0; i < LLB_NS && i < n_my; ++i) issue(i, i);
   const uint32_t part = (uint32_t)warp % LLB_P, grp = (uint32_t)warp / LLB_P;
   uint32_t s = 0, sph = 0, d = 0, dph = 0;
   for (uint32_t i = 0; i < n_my; ++i) {
@@ -183,11 +184,9 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
     // r = a group of LLB_G consecutive records (lane = group)
     for (uint32_t r = grp * 32 + lane; r < LLB_T / LLB_G; r += (LLB_CONS / LLB_P)) llb_permute(p, sim, dim, t0, part, r);
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    llb_cons_sync();
-    if (tid == 0) {
-      llb_mbar_arrive(&empty[s]);
-      if (LLB_ND > 0) llb_mbar_arrive(&dfull[d]);
-    }
+    llb_cons_sync();  // every consumer is done with stage s (and destination buffer d)
+    if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
+    if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
     if (++s == LLB_NS) { s = 0; sph ^= 1; }
     if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
   }

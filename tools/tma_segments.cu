@@ -21,6 +21,8 @@ struct P {
   const uint8_t* aos_r;
   uint64_t N;
   uint32_t K, T, S, Sp, ns, nd, s2a, lanes;  // lanes: producer lanes issuing the segment ops
+  uint32_t chunks;     // 1: SoA source segments as 16-byte cp.async chunks (all 32 lanes, mbarrier arrive.noinc)
+  uint32_t pad_smem;   // extra dynamic shared memory (fewer CTAs per SM)
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(288) k(const __grid_constant__ P p) {
     uint32_t off = 0;
     for (uint32_t k = 0; k < p.K; ++k) { segoff[k] = off; off += p.T * p.sz[k]; }
     for (int i = 0; i < 8; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(full + i)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(full + i)), "r"(p.chunks ? 32u : 1u));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(empty + i)));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(dfull + i)));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(dempty + i)));
@@ -60,10 +62,20 @@ __global__ void __launch_bounds__(288) k(const __grid_constant__ P p) {
     // segment offsets (prefix sums, same for every tile)
     auto load = [&](uint32_t i, uint32_t s) {
       const uint64_t t0 = (blockIdx.x + (uint64_t)i * gridDim.x) * p.T;
+      uint8_t* d = src + s * sstage;
+      if (p.chunks) {
+        for (uint32_t k = 0; k < p.K; ++k) {
+          const uint32_t n = p.T * p.sz[k] / 16;
+          for (uint32_t c = lane; c < n; c += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(d + segoff[k] + 16 * c)),
+                         "l"(p.soa[k] + t0 * p.sz[k] + 16 * c) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sa(full + s)) : "memory");
+        return;
+      }
       if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(full + s)), "r"(sstage));
       __syncwarp(p.lanes >= 32 ? 0xffffffffu : ((1u << p.lanes) - 1u));
-      uint8_t* d = src + s * sstage;
       if (p.s2a) {
         for (uint32_t k = lane; k < p.K; k += p.lanes) {
           const uint32_t b = p.T * p.sz[k];
@@ -151,20 +163,24 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  printf("dir        S    T  ns nd lanes smem_KB ctas/SM   GB/s\n");
-  for (uint32_t s2a : {1u, 0u})
-    for (uint32_t S : {480u, 380u})
-      for (uint32_t T : {32u, 64u, 128u})
-        for (uint32_t ns : {2u, 3u})
-          for (uint32_t lanes : {1u, 4u, 32u})
+  printf("dir        S    T  ns nd lanes chunks pad_KB smem_KB ctas/SM   GB/s\n");
+  for (uint32_t s2a : {1u})
+    for (uint32_t S : {380u})
+      for (uint32_t T : {32u, 64u})
+        for (uint32_t ns : {2u, 3u, 4u})
+          for (uint32_t lanes : {32u})
+          for (uint32_t chunks : {0u, 1u})
+          for (uint32_t pad : {0u, 40u, 80u, 120u})
           for (uint32_t nd : {2u}) {
             p.lanes = lanes;
+            p.chunks = chunks;
+            p.pad_smem = pad * 1024;
             p.S = S;
             p.T = T;
             p.ns = ns;
             p.nd = nd;
             p.s2a = s2a;
-            const uint32_t smem = 256 + ns * T * (s2a ? Sp : S) + nd * T * (s2a ? S : Sp);
+            const uint32_t smem = 256 + ns * T * (s2a ? Sp : S) + nd * T * (s2a ? S : Sp) + p.pad_smem;
             if (smem > 226 * 1024) continue;
             int per = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 288, smem);
@@ -179,7 +195,7 @@ int main() {
             float ms = 0;
             cudaEventElapsedTime(&ms, e0, e1);
             const double gbs = (double)N * (Sp + S) * 5 / (ms * 1e-3) / 1e9;
-            printf("%s %4u %4u %3u %2u %5u %8.1f %7d %7.0f\n", s2a ? "SoA->AoS" : "AoS->SoA", S, T, ns, nd, lanes, smem / 1024.0, per, gbs);
+            printf("%s %4u %4u %3u %2u %5u %6u %6u %8.1f %7d %7.0f\n", s2a ? "SoA->AoS" : "AoS->SoA", S, T, ns, nd, lanes, chunks, pad, smem / 1024.0, per, gbs);
           }
   return 0;
 }
