@@ -21,7 +21,8 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 
 # device sources compiled at plan time by NVRTC (jit.cpp), embedded as strings
-JIT_EMBED = [("kJitParamsSrc", "jit_params.h"), ("kJitKernelSrc", "jit_kernel.cuh")]
+JIT_EMBED = [("kJitParamsSrc", "jit_params.h"), ("kJitKernelSrc", "jit_kernel.cuh"),
+             ("kJitKernel2dSrc", "jit_kernel2d.cuh")]
 
 
 def _write_embed():

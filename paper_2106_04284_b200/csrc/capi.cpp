@@ -285,6 +285,10 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
     switch (plan->path) {
       case LLAMA_PATH_NAIVE:
       case LLAMA_PATH_TRANSPOSE: {
+        if (plan->jit) {
+          e = llb::launch_jit(*plan->jit, s, src_blobs, d, dst_blobs, plan->pdl, stream);
+          break;
+        }
         if (plan->naive_zero_fill) {
           llb::FillParams f = *plan->fill;
           for (int b = 0; b < f.nb; ++b) f.ptr[b] = static_cast<uint8_t*>(dst_blobs[b]);

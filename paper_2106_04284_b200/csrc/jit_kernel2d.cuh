@@ -1,0 +1,194 @@
+// jit_kernel2d.cuh -- device skeleton of the plan-time specialised
+// TRANSPOSING copy: 2-d views whose
+// linearisations differ (row-major / column-major / Morton), so the
+// copy is also a transpose / Morton reorder.  NOT compiled by nvcc: embedded
+// by _build.py, compiled by NVRTC with the code jit.cpp generates.
+//
+// A tile is 32 x 32 records (ty, tx).  On each side the tile is a set of
+// contiguous storage segments: 32 rows (row-major), 32 columns (column-major)
+// or one block of 1024 codes (Morton).  Every segment of an AoS part moves by
+// one TMA bulk copy (loads issued by consumer threads 0..31, stores by the
+// store warp's 32 lanes); every segment of a SoA source leaf moves as 16-byte
+// cp.async chunks spread over the consumers; SoA destination leaves are
+// stored straight to global memory by llb_permute2d.  In shared memory the
+// segments of a part / leaf sit at a padded pitch (odd multiple of 16 B), so
+// records of one warp that lie in 32 different segments spread over the banks.
+//
+// Generated before the marker: LLB_NS, LLB_ND, LLB_SSTAGE, LLB_DSTAGE,
+// LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_NTX (tiles along x), LLB_NTILES,
+// LLB_H, LLB_W (extents), LLB_SLIN / LLB_DLIN (0 row, 1 col, 2 Morton); at the
+// marker: llb_ctab[] (chunk: smem offset | log2 s_k << 18 | leaf << 20, and
+// the segment index in a second word), llb_seg_delta[] (per leaf), llb_src_tma2d(),
+// llb_dst_tma2d(), llb_permute2d().
+
+#define LLB_CONS 256
+
+extern __shared__ __align__(128) uint8_t llb_smem[];
+
+__device__ __forceinline__ uint32_t llb_sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void llb_mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(llb_sa(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void llb_mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nLLBW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra LLBW_%=;\n}" ::"r"(
+          llb_sa(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void llb_mbar_wait_sleep(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nLLBS_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t@!p bra LLBS_%=;\n}" ::"r"(
+          llb_sa(b)),
+      "r"(ph), "r"(20000)
+      : "memory");
+}
+__device__ __forceinline__ void llb_mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(llb_sa(b)) : "memory");
+}
+__device__ __forceinline__ void llb_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(llb_sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void llb_g2s(void* s, const void* g, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(llb_sa(s)),
+               "l"(g), "r"(bytes), "r"(llb_sa(b))
+               : "memory");
+}
+__device__ __forceinline__ void llb_s2g(void* g, const void* s, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(llb_sa(s)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void llb_cp16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(llb_sa(s)), "l"(g));
+}
+__device__ __forceinline__ void llb_cp_arrive_noinc(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(llb_sa(b)) : "memory");
+}
+__device__ __forceinline__ void llb_cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(LLB_CONS) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint8_t v) { asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint16_t v) { asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint32_t v) { asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint64_t v) { asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory"); }
+
+// bits of a 5-bit index spread to the even positions (Morton, #26:
+// the last index supplies bit 0)
+__device__ __forceinline__ uint32_t llb_spread(uint32_t v) {
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__device__ __forceinline__ uint64_t llb_morton(uint32_t y, uint32_t x) {
+  return ((uint64_t)llb_spread(y) << 1) | (uint64_t)llb_spread(x);
+}
+// the storage position of tile (ty, tx)'s first record and the distance between
+// its segments, for a linearisation
+__device__ __forceinline__ void llb_tile_pos(uint32_t lin, uint32_t ty, uint32_t tx, uint64_t* pos0, uint64_t* pitch) {
+  if (lin == 0) { *pos0 = (uint64_t)(ty * 32) * LLB_W + tx * 32; *pitch = LLB_W; }
+  else if (lin == 1) { *pos0 = (uint64_t)(tx * 32) * LLB_H + ty * 32; *pitch = LLB_H; }
+  else { *pos0 = llb_morton(ty, tx) * 1024; *pitch = 0; }
+}
+
+// ==== LLB_GENERATED ====
+
+extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_transpose(const __grid_constant__ LlbJitParams p) {
+  uint64_t* full = reinterpret_cast<uint64_t*>(llb_smem);
+  uint64_t* dfull = full + 16;
+  uint64_t* dempty = full + 24;
+  uint8_t* sring = llb_smem + 256;
+  uint8_t* dring = sring + LLB_NS * LLB_SSTAGE;
+  const uint8_t** sgs = reinterpret_cast<const uint8_t**>(dring + LLB_ND * LLB_DSTAGE);
+  long long* sdelta = reinterpret_cast<long long*>(sgs + LLB_JIT_MAX_LEAVES);
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(sdelta + LLB_JIT_MAX_LEAVES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < LLB_NS; ++s) llb_mbar_init(&full[s], LLB_CONS);
+    for (int d = 0; d < (LLB_ND > 0 ? LLB_ND : 1); ++d) {
+      llb_mbar_init(&dfull[d], 1);
+      llb_mbar_init(&dempty[d], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (uint32_t o = 16 * tid; o < LLB_ND * LLB_DSTAGE; o += 16 * (LLB_CONS + 32))
+    *reinterpret_cast<uint4*>(dring + o) = make_uint4(0, 0, 0, 0);
+  for (uint32_t c = tid; c < 2 * LLB_NCHUNK; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
+  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) {
+    sgs[k] = p.sg[k] - llb_seg_base[k];
+    sdelta[k] = llb_seg_delta[k];
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (blockIdx.x == 0 && warp < LLB_CONS / 32)
+    for (uint32_t g = 0; g < p.n_gaps; ++g)
+      for (uint32_t o = tid; o < p.gap_len[g]; o += LLB_CONS) p.blobs[1][p.gap_blob[g]][p.gap_off[g] + o] = 0;
+
+  const uint64_t first = blockIdx.x, stride = gridDim.x;
+  const uint32_t n_my = first < LLB_NTILES ? (uint32_t)((LLB_NTILES - first + stride - 1) / stride) : 0;
+  auto tile_of = [&](uint32_t i, uint32_t* ty, uint32_t* tx) {
+    const uint32_t t = (uint32_t)(first + (uint64_t)i * stride);
+    *ty = t / LLB_NTX;
+    *tx = t % LLB_NTX;
+  };
+
+  if (warp == LLB_CONS / 32) {  // ------------------------------ store warp
+    if (LLB_ND > 0) {
+      uint32_t d = 0, dph = 0;
+      for (uint32_t i = 0; i < n_my; ++i) {
+        uint32_t ty, tx;
+        tile_of(i, &ty, &tx);
+        llb_mbar_wait_sleep(&dfull[d], dph);
+        llb_dst_tma2d(p, dring + d * LLB_DSTAGE, ty, tx, lane);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(LLB_ND > 0 ? LLB_ND - 1 : 0) : "memory");
+        __syncwarp();
+        if (lane == 0 && i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0))
+          llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
+        if (++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
+  // ------------------------------------------------------------- consumers
+  auto issue = [&](uint32_t i, uint32_t s) {
+    uint32_t ty, tx;
+    tile_of(i, &ty, &tx);
+    uint8_t* stage = sring + s * LLB_SSTAGE;
+    if (LLB_SRC_TMA > 0) {
+      if (tid == 0) llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
+      if (tid < 32) llb_src_tma2d(p, stage, ty, tx, (uint32_t)tid, &full[s]);
+    }
+    uint64_t pos0, pitch;
+    llb_tile_pos(LLB_SLIN, ty, tx, &pos0, &pitch);
+#pragma unroll 4
+    for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS) {
+      const uint32_t e = ctab[2 * c], sg = ctab[2 * c + 1], so = e & 0x3FFFFu, lg = (e >> 18) & 3u, k = e >> 20;
+      llb_cp16(stage + so, sgs[k] + so + ((pos0 + (uint64_t)sg * pitch) << lg) - (long long)sg * sdelta[k]);
+    }
+    llb_cp_arrive_noinc(&full[s]);
+  };
+  for (uint32_t i = 0; i < LLB_NS && i < n_my; ++i) issue(i, i);
+  // thread -> record of the tile: warp w, lane l -> (yy, xx) = (w + 8 * j, l), j = 0..3
+  uint32_t s = 0, sph = 0, d = 0, dph = 0;
+  for (uint32_t i = 0; i < n_my; ++i) {
+    uint32_t ty, tx;
+    tile_of(i, &ty, &tx);
+    if (tid == 0) {
+      llb_mbar_wait(&full[s], sph);
+      if (LLB_ND > 0 && i >= (uint32_t)LLB_ND) llb_mbar_wait(&dempty[d], dph ^ 1);
+    }
+    llb_cons_sync();
+    const uint8_t* sim = sring + s * LLB_SSTAGE;
+    uint8_t* dim = dring + d * LLB_DSTAGE;
+#pragma unroll 1
+    for (uint32_t yy = (uint32_t)warp; yy < 32; yy += LLB_CONS / 32) llb_permute2d(p, sim, dim, ty, tx, yy, (uint32_t)lane);
+    if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    llb_cons_sync();
+    if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
+    if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
+    if (++s == LLB_NS) { s = 0; sph ^= 1; }
+    if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
+  }
+}

@@ -707,6 +707,18 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   // record (index) -> record (index) across storage orders, or counting every
   // address resolution (Trace / Heatmap): the element-wise kernel only
   if (s.lin != d.lin || s.trace || d.trace) {
+    if (path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) {
+      std::unique_ptr<JitPlan> jp(new JitPlan);
+      if (plan_jit2d(s, d, kn, jp.get(), &why)) {
+        out->path = LLAMA_PATH_TRANSPOSE;
+        out->smem_bytes = (int)jp->smem;
+        out->jit = std::move(jp);
+        return LLAMA_OK;
+      }
+#ifdef LLB_DEBUG_JIT
+      std::fprintf(stderr, "plan_jit2d: %s\n", why.c_str());
+#endif
+    }
     if ((path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) && plan_transpose(s, d, kn, out, &why))
       return LLAMA_OK;
     if (path != LLAMA_PATH_AUTO && path != LLAMA_PATH_NAIVE) {
