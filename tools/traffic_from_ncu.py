@@ -42,7 +42,8 @@ def load(path):
             x = float(v)
         except ValueError:
             continue
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9,
+                 "us": 1e-6, "ms": 1e-3, "s": 1.0,
                  "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
         launches[key][r[idx["Metric Name"]]] = x * scale
     return launches
