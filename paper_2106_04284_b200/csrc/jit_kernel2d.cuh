@@ -79,6 +79,14 @@ __device__ __forceinline__ uint32_t llb_spread(uint32_t v) {
   v = (v | (v << 1)) & 0x55555555u;
   return v;
 }
+__device__ __forceinline__ uint32_t llb_unspread(uint32_t v) {  // the even bits of v, packed
+  v &= 0x55555555u;
+  v = (v | (v >> 1)) & 0x33333333u;
+  v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+  v = (v | (v >> 4)) & 0x00FF00FFu;
+  v = (v | (v >> 8)) & 0x0000FFFFu;
+  return v;
+}
 __device__ __forceinline__ uint64_t llb_morton(uint32_t y, uint32_t x) {
   return ((uint64_t)llb_spread(y) << 1) | (uint64_t)llb_spread(x);
 }
@@ -182,8 +190,20 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     llb_cons_sync();
     const uint8_t* sim = sring + s * LLB_SSTAGE;
     uint8_t* dim = dring + d * LLB_DSTAGE;
+    // lanes run along the destination's storage order when it is stored
+    // straight to global memory (SoA leaves): row (xx), column (yy), Morton
+    // (the low 5 bits of the tile's Morton code) -- coalesced element stores
 #pragma unroll 1
-    for (uint32_t yy = (uint32_t)warp; yy < 32; yy += LLB_CONS / 32) llb_permute2d(p, sim, dim, ty, tx, yy, (uint32_t)lane);
+    for (uint32_t q = (uint32_t)warp; q < 32; q += LLB_CONS / 32) {
+      uint32_t yy, xx;
+      if (LLB_LANES == 1) { yy = (uint32_t)lane; xx = q; }
+      else if (LLB_LANES == 2) {
+        const uint32_t code = q * 32 + (uint32_t)lane;  // Morton code within the tile: bit 0 from x
+        yy = llb_unspread(code >> 1);
+        xx = llb_unspread(code);
+      } else { yy = q; xx = (uint32_t)lane; }
+      llb_permute2d(p, sim, dim, ty, tx, yy, xx);
+    }
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     llb_cons_sync();
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
