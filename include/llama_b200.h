@@ -249,7 +249,7 @@ typedef enum {
   LLAMA_KNOB_JIT_TILE,         /* JIT: records per tile, 32 / 64 / 128 / 256 / 512 (<= 64 KB of images per tile) */
   LLAMA_KNOB_JIT_STAGES,       /* JIT: source stages 2..6 (3 while the ring fits 180 KB, else 2) */
   LLAMA_KNOB_JIT_DST_BUFS,     /* JIT: destination image buffers 2..4 (3 while <= 180 KB, else 2) */
-  LLAMA_KNOB_JIT_RESERVED,     /* reserved (no effect) */
+  LLAMA_KNOB_JIT_CHUNKS,       /* JIT transpose: AoS source segments as 16-byte cp.async chunks (1) or TMA (0) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

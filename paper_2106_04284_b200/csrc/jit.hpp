@@ -21,6 +21,7 @@ struct JitPlan {
   LlbJitParams params;          // everything but the per-call pointers
   std::string kernel = "llb_jit_permute";  // or "llb_jit_transpose" (2-d tiles, different linearisations)
   uint64_t n_tiles = 0;         // tiles of the tile pipeline (the grid is bounded by it)
+  uint32_t threads = 256 + 32;  // CTA size (consumers + the store warp)
   uint32_t T = 0, ns = 0, nd = 0, parts = 0, minb = 1;
   uint32_t smem = 0;            // dynamic shared memory per CTA
   uint32_t src_soa[LLB_JIT_MAX_LEAVES] = {};  // 1: src leaf k is a SoA leaf (sg pointer patched per call)

@@ -21,7 +21,9 @@
 // the segment index in a second word), llb_seg_delta[] (per leaf), llb_src_tma2d(),
 // llb_dst_tma2d(), llb_permute2d().
 
-#define LLB_CONS 256
+#ifndef LLB_CONS
+#define LLB_CONS 256  // consumer threads (generated)
+#endif
 
 extern __shared__ __align__(128) uint8_t llb_smem[];
 
@@ -164,10 +166,8 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     uint32_t ty, tx;
     tile_of(i, &ty, &tx);
     uint8_t* stage = sring + s * LLB_SSTAGE;
-    if (LLB_SRC_TMA > 0) {
-      if (tid == 0) llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
-      if (tid < 32) llb_src_tma2d(p, stage, ty, tx, (uint32_t)tid, &full[s]);
-    }
+    if (LLB_SRC_TMA > 0 && tid == 0) llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
+    llb_src_tma2d(p, stage, ty, tx, (uint32_t)tid, &full[s]);  // TMA segment ops (tid < 32) / cp.async chunks
     uint64_t pos0, pitch;
     llb_tile_pos(LLB_SLIN, ty, tx, &pos0, &pitch);
 #pragma unroll 4
@@ -193,7 +193,8 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     // lanes run along the destination's storage order when it is stored
     // straight to global memory (SoA leaves): row (xx), column (yy), Morton
     // (the low 5 bits of the tile's Morton code) -- coalesced element stores
-#pragma unroll 1
+    // the thread's 4 records unrolled: independent load -> store chains overlap
+#pragma unroll
     for (uint32_t q = (uint32_t)warp; q < 32; q += LLB_CONS / 32) {
       uint32_t yy, xx;
       if (LLB_LANES == 1) { yy = (uint32_t)lane; xx = q; }
