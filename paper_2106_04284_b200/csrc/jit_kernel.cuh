@@ -132,17 +132,20 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   const uint32_t n_my = first < p.n_full ? (uint32_t)((p.n_full - first + stride - 1) / stride) : 0;
 
   if (warp == LLB_CONS / 32) {  // ------------------------------ store warp
-    if (LLB_ND > 0 && lane == 0) {
+    if (LLB_ND > 0) {
       uint32_t d = 0, dph = 0;
       for (uint32_t i = 0; i < n_my; ++i) {
-        // store tile i, keep up to ND - 1 stores in flight: hand back the
-        // buffer of tile i - (ND - 1) once its store has read it out
+        // store tile i (its TMA ops spread over the 32 lanes), keep up to
+        // ND - 1 stores in flight: hand back the buffer of tile i - (ND - 1)
+        // once its stores have read it out
         const uint64_t t0 = (first + (uint64_t)i * stride) * LLB_T;
         llb_mbar_wait_sleep(&dfull[d], dph);
-        llb_dst_tma(p, dring + d * LLB_DSTAGE, t0);
+        llb_dst_tma(p, dring + d * LLB_DSTAGE, t0, (uint32_t)lane);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(LLB_ND > 0 ? LLB_ND - 1 : 0) : "memory");
-        if (i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0)) llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
+        __syncwarp();
+        if (lane == 0 && i >= (uint32_t)(LLB_ND > 0 ? LLB_ND - 1 : 0))
+          llb_mbar_arrive(&dempty[(d + 1) % (LLB_ND > 0 ? LLB_ND : 1)]);
         if (++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
       }
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

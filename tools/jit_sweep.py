@@ -17,7 +17,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--records", type=int, default=1 << 24)
 ap.add_argument("--pairs", default="soa_mb:aos,soa_mb:aos_aligned,aos:soa_mb,aos_aligned:soa_mb,aos:aos_aligned,aos_aligned:aos")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--extra", default="", help="knobs added to every setting, k=v,...")
 a = ap.parse_args()
+extra = {k: int(v) for k, v in (kv.split("=") for kv in a.extra.split(",") if kv)}
 n = a.records
 views = {}
 for pair in a.pairs.split(","):
@@ -34,7 +36,7 @@ for pair in a.pairs.split(","):
     dm, _, db = views[d]
     res = []
     for vals in itertools.product(*grid.values()):
-        knobs = dict(zip(grid.keys(), vals), jit=2)
+        knobs = dict(zip(grid.keys(), vals), jit=2, **extra)
         try:
             pl = llama.plan(sm, dm, path="permute", knobs=knobs)
         except llama.LlamaError:
