@@ -105,7 +105,9 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   // per leaf: the SoA source element-0 pointer minus the leaf's segment offset
   // in the stage, so a chunk's global address is sgs[k] + soff + (t0 << lg)
   const uint8_t** sgs = reinterpret_cast<const uint8_t**>(dring + LLB_ND * LLB_DSTAGE);
-  uint32_t* ctab = reinterpret_cast<uint32_t*>(sgs + LLB_JIT_MAX_LEAVES);
+  uint8_t** dgs = reinterpret_cast<uint8_t**>(dring + LLB_ND * LLB_DSTAGE + 8 * LLB_JIT_MAX_LEAVES);  // SoA dst pointers minus segment offsets
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(dgs + LLB_JIT_MAX_LEAVES);
+  uint32_t* dctab = ctab + LLB_NCHUNK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < LLB_NS; ++s) llb_mbar_init(&full[s], LLB_CONS);  // every consumer's cp.async arrival (+ TMA bytes)
@@ -120,7 +122,11 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   for (uint32_t o = 16 * tid; o < LLB_ND * LLB_DSTAGE; o += 16 * (LLB_CONS + 32))
     *reinterpret_cast<uint4*>(dring + o) = make_uint4(0, 0, 0, 0);
   for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
-  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) sgs[k] = p.sg[k] - llb_seg[k];
+  for (uint32_t c = tid; c < LLB_NDCHUNK; c += LLB_CONS + 32) dctab[c] = llb_dctab[c];
+  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) {
+    sgs[k] = p.sg[k] - llb_seg[k];
+    dgs[k] = p.dg[k] - llb_dseg[k];
+  }
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -190,6 +196,12 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
     llb_cons_sync();  // every consumer is done with stage s (and destination buffer d)
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
     if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
+    // image-staged SoA destination leaves: 16-byte chunks out by every consumer
+#pragma unroll 4
+    for (uint32_t c = tid; c < LLB_NDCHUNK; c += LLB_CONS) {
+      const uint32_t e = dctab[c], so = e & 0x3FFFFu;
+      llb_stg(dgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)), *reinterpret_cast<const uint4*>(dim + so));
+    }
     if (++s == LLB_NS) { s = 0; sph ^= 1; }
     if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
   }

@@ -55,7 +55,8 @@ def test_small_records_forced_jit(llama, oracle_mod, schema_name, n):
 
 @pytest.mark.parametrize("knobs", [{"jit_tile": 32}, {"jit_tile": 64}, {"jit_tile": 128}, {"jit_stages": 3},
                                    {"jit_stages": 4, "jit_dst_bufs": 3}, {"jit_tile": 256}, {"jit_stages": 2, "jit_dst_bufs": 2},
-                                   {"jit_soa_tma": 1}, {"jit_soa_tma": 1, "jit_tile": 32}])
+                                   {"jit_soa_tma": 1}, {"jit_soa_tma": 1, "jit_tile": 32}, {"jit_soa_tma": 2},
+                                   {"jit_soa_tma": 2, "jit_tile": 128}])
 def test_jit_geometry_knobs(llama, oracle_mod, knobs):
     for a, b in [("aos", "soa_mb"), ("soa_mb", "aos_aligned"), ("aos", "aos_aligned"), ("soa_sb", "aosoa8"),
                  ("aos_aligned", "soa_sb")]:
