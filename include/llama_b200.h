@@ -251,7 +251,8 @@ typedef enum {
   LLAMA_KNOB_JIT_DST_BUFS,     /* JIT: destination image buffers 2..4 (3 while <= 180 KB, else 2) */
   LLAMA_KNOB_JIT_CHUNKS,       /* JIT transpose: AoS source segments as 16-byte cp.async chunks (1) or TMA (0) */
   LLAMA_KNOB_JIT_SOA_TMA,      /* JIT permute: SoA destination leaves stored from registers (0), or staged in shared
-                                  memory and TMA-stored per leaf (1) / stored as 16-byte chunks by the consumers (2) */
+                                  memory and TMA-stored per leaf (1) / stored as 16-byte chunks by the consumers
+                                  (2; the default when every destination part is SoA) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

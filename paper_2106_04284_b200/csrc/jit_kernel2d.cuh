@@ -4,9 +4,10 @@
 // copy is also a transpose / Morton reorder.  NOT compiled by nvcc: embedded
 // by _build.py, compiled by NVRTC with the code jit.cpp generates.
 //
-// A tile is 32 x 32 records (ty, tx).  On each side the tile is a set of
-// contiguous storage segments: 32 rows (row-major), 32 columns (column-major)
-// or one block of 1024 codes (Morton).  Every segment of an AoS part moves by
+// A tile is LLB_TY x 32 records (ty, tx), LLB_TY = 32 or 16 (16 keeps two
+// CTAs per SM for small records).  On each side the tile is a set of
+// contiguous storage segments: LLB_TY rows of 32 (row-major), 32 columns of
+// LLB_TY (column-major) or one run of 32 * LLB_TY codes (Morton).  Every segment of an AoS part moves by
 // one TMA bulk copy (loads issued by consumer threads 0..31, stores by the
 // store warp's 32 lanes); every segment of a SoA source leaf moves as 16-byte
 // cp.async chunks spread over the consumers; SoA destination leaves are
@@ -95,9 +96,9 @@ __device__ __forceinline__ uint64_t llb_morton(uint32_t y, uint32_t x) {
 // the storage position of tile (ty, tx)'s first record and the distance between
 // its segments, for a linearisation
 __device__ __forceinline__ void llb_tile_pos(uint32_t lin, uint32_t ty, uint32_t tx, uint64_t* pos0, uint64_t* pitch) {
-  if (lin == 0) { *pos0 = (uint64_t)(ty * 32) * LLB_W + tx * 32; *pitch = LLB_W; }
-  else if (lin == 1) { *pos0 = (uint64_t)(tx * 32) * LLB_H + ty * 32; *pitch = LLB_H; }
-  else { *pos0 = llb_morton(ty, tx) * 1024; *pitch = 0; }
+  if (lin == 0) { *pos0 = (uint64_t)(ty * LLB_TY) * LLB_W + tx * 32; *pitch = LLB_W; }
+  else if (lin == 1) { *pos0 = (uint64_t)(tx * 32) * LLB_H + ty * LLB_TY; *pitch = LLB_H; }
+  else { *pos0 = llb_morton(ty * LLB_TY, tx * 32); *pitch = 0; }  // the tile's codes are one aligned run
 }
 
 // ==== LLB_GENERATED ====
@@ -195,7 +196,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     // (the low 5 bits of the tile's Morton code) -- coalesced element stores
     // the thread's 4 records unrolled: independent load -> store chains overlap
 #pragma unroll
-    for (uint32_t q = (uint32_t)warp; q < 32; q += LLB_CONS / 32) {
+    for (uint32_t q = (uint32_t)warp; q < LLB_TY; q += LLB_CONS / 32) {
       uint32_t yy, xx;
       if (LLB_LANES == 1) { yy = (uint32_t)lane; xx = q; }
       else if (LLB_LANES == 2) {
