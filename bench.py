@@ -12,12 +12,13 @@ The same run also measures, as sub-objects of the line (`configs`):
   C2_soa_sb  the 9 further ordered pairs with SoA single-blob
   C3         67,108,864 HEP100 event records, packed AoS <-> aligned AoS <-> SoA MB
              (the paper's 100-leaf event workload), weak scaling
+  C3_soa_sb  the same records, the 4 pairs of {packed, aligned AoS} <-> SoA single-blob
   C4         Listing-1 8192 x 8192, AoSoA32 -> SoA SB, rows sharded over ranks (strong)
 each with per-pair GB/s, the dominant kernel's roofline and an in-run
 device-memcpy ceiling; `min_pair_frac` is the weakest pair over all of them.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C4]
+                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C3_soa_sb,C4]
 
 --gpus N > 1 without torchrun re-launches itself under torch.distributed.run
 with N processes (one per GPU); under torchrun WORLD_SIZE must equal N.
@@ -53,7 +54,7 @@ METRIC = "layout-copy GB/s (read+write) per mapping pair vs 8 TB/s HBM, 1/2/4/8 
 KERNEL = {"permute": "k_permute_ws", "permute_direct": "k_permute_direct", "permute_jit": "llb_jit_permute",
           "blobcopy": "k_bulkcopy",
           "run": "k_run", "naive": "k_naive", "transpose": "k_transpose2d"}
-DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C4"
+DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C3_soa_sb,C4"
 
 
 def parse(argv=None):
@@ -354,6 +355,10 @@ def workload_desc(name, world):
                              "SoA SB} that involve SoA single-blob, 16,777,216 Particle7 records per GPU",
                     records_per_gpu=16_777_216, pairs=9, l2="inputs larger than L2",
                     parallelism=f"dp{world} (weak scaling)")
+    if name == "C3_soa_sb":
+        return dict(workload="C3 + SoA SB: HEP100 stand-in x 67,108,864 records per GPU, the 4 ordered pairs of "
+                             "{packed AoS, aligned AoS} <-> SoA single-blob", records_per_gpu=67_108_864, pairs=4,
+                    l2="inputs larger than L2", parallelism=f"dp{world} (weak scaling)")
     if name == "C3":
         return dict(workload="C3: HEP100 stand-in (100 leaves, packed 380 B / aligned 480 B) x 67,108,864 records "
                              "per GPU, 6 ordered pairs of {packed AoS, aligned AoS, SoA MB}",
@@ -370,6 +375,7 @@ SUBCFG = {
     "C2": dict(schema="particle7", extents=[16_777_216], kinds=["aos", "soa_mb", "aosoa8", "aosoa32"]),
     "C2_soa_sb": dict(schema="particle7", extents=[16_777_216], kinds=["aos", "soa_mb", "aosoa8", "aosoa32", "soa_sb"]),
     "C3": dict(schema="hep100", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_mb"]),
+    "C3_soa_sb": dict(schema="hep100", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_sb"]),
     "C4": dict(schema="listing1", extents=[8192, 8192], kinds=["aosoa32", "soa_sb"]),
 }
 
@@ -384,6 +390,8 @@ def pairs_of(name):
         return ([("soa_sb", "soa_sb")] + [p for k in o for p in (("soa_sb", k), (k, "soa_sb"))])[::-1]
     if name == "C3":
         return l2_free_order(sc["kinds"], identities=False)
+    if name == "C3_soa_sb":  # the 4 pairs with SoA SB, alternating directions
+        return [("aos", "soa_sb"), ("soa_sb", "aos_aligned"), ("aos_aligned", "soa_sb"), ("soa_sb", "aos")]
     return [("aosoa32", "soa_sb")]
 
 
