@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""One n-body move per layout (AoS, SoA MB, AoSoA32) on 64Mi particles, for ncu captures."""
+"""One n-body move per layout (SoA MB, AoS, AoSoA32, split_p7) at the bench's 256Mi particles
+(W.NBODY_MOVE_N), for ncu captures (tools/traffic_from_ncu.py ...:MOVE)."""
 import os
 import sys
 
@@ -9,8 +10,8 @@ import torch  # noqa: E402
 import paper_2106_04284_b200 as llama  # noqa: E402
 import workloads as W  # noqa: E402
 
-n = 1 << 26
-for name in ("soa_mb", "aos", "aosoa32"):
+n = W.NBODY_MOVE_N
+for name in ("soa_mb", "aos", "aosoa32", "split_p7"):
     m = llama.Mapping.from_spec(W.PARTICLE7, [n], W.resolve_spec(name))
     b = m.alloc("cuda")
     for t in b:

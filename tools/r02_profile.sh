@@ -20,4 +20,6 @@ ncu --metrics $S --clock-control none --csv --log-file gpurun_out/r02_sectors_di
 ncu --metrics $S --clock-control none --csv --log-file gpurun_out/r02_sectors_ws.csv python tools/profile_pairs.py --config C2 --iters 1 --pairs aos:soa_mb,soa_mb:aos > /dev/null 2>&1
 python tools/f4_bench.py > gpurun_out/f4_pre.txt 2>&1
 ncu --metrics $S --clock-control none --csv --log-file gpurun_out/r02_sectors_f4.csv -k regex:k_transpose2d -c 6 python tools/f4_bench.py > /dev/null 2>&1
+python tools/move_once.py > /dev/null || exit 1
+ncu --metrics $M --clock-control none --csv --log-file gpurun_out/r02_traffic_move.csv -k regex:k_move_runs python tools/move_once.py > /dev/null 2>&1
 ls -la gpurun_out/r02_*
