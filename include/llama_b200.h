@@ -250,6 +250,8 @@ typedef enum {
   LLAMA_KNOB_JIT_STAGES,       /* JIT: source stages 2..6 (3 while the ring fits 180 KB, else 2) */
   LLAMA_KNOB_JIT_DST_BUFS,     /* JIT: destination image buffers 2..4 (3 while <= 180 KB, else 2) */
   LLAMA_KNOB_JIT_CHUNKS,       /* JIT transpose: AoS source segments as 16-byte cp.async chunks (1) or TMA (0) */
+  LLAMA_KNOB_JIT_LANES,        /* JIT transpose: lanes along x (0), y (1), Morton codes (2), 4 x 8 blocks (3);
+                                  default: the SoA destination's order, else a Morton source's, else x */
   LLAMA_KNOB_JIT_SOA_TMA,      /* JIT permute: SoA destination leaves stored from registers (0), or staged in shared
                                   memory and TMA-stored per leaf (1) / stored as 16-byte chunks by the consumers
                                   (2; the default when every destination part is SoA) */

@@ -199,6 +199,11 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     for (uint32_t q = (uint32_t)warp; q < LLB_TY; q += LLB_CONS / 32) {
       uint32_t yy, xx;
       if (LLB_LANES == 1) { yy = (uint32_t)lane; xx = q; }
+      else if (LLB_LANES == 3) {  // 4 rows x 8 columns per warp access: both a row- and a column-major
+        // image see 4 / 8 segments and 8 / 4 consecutive records (no 4-way bank conflicts)
+        yy = (q / 4) * 4 + ((uint32_t)lane >> 3);
+        xx = (q % 4) * 8 + ((uint32_t)lane & 7u);
+      }
       else if (LLB_LANES == 2) {
         const uint32_t code = q * 32 + (uint32_t)lane;  // Morton code within the tile: bit 0 from x
         yy = llb_unspread(code >> 1);

@@ -82,3 +82,26 @@ def test_jit_chosen_for_wide_records(llama):
         for b in m:
             if a != b:
                 assert llama.plan(m[a], m[b])["jit"], (a, b)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_jit_random_fuzz(llama, oracle_mod, seed):
+    """Random schemas (all scalar types, static arrays, nesting) x random
+    mapping kinds and splits x ragged extents, forced onto the JIT kernel
+    (knob jit=2; pairs it cannot take fall back, the oracle checks every
+    byte either way), and a random JIT geometry."""
+    import random
+
+    from test_gpu_parity import _random_schema, _random_spec
+    rng = random.Random(1000 + seed)
+    schema = _random_schema(rng)
+    k = llama.Mapping(schema, [1], "aos").leaf_count
+    n = rng.choice([1, 31, 64, 65, 500, 4097, 20_000])
+    knobs = {"jit": 2}
+    if rng.random() < 0.5:
+        knobs["jit_tile"] = rng.choice([32, 64, 128, 256])
+    if rng.random() < 0.3:
+        knobs["jit_soa_tma"] = rng.choice([0, 2])
+    for _ in range(6):
+        sspec, dspec = _random_spec(rng, k), _random_spec(rng, k)
+        run_spec_case(llama, oracle_mod, schema, [n], sspec, dspec, seed=seed, knobs=knobs, paths=("permute",))

@@ -19,8 +19,8 @@ for sspec, slin, dspec, dlin in CASES:
     dm = llama.Mapping.from_spec(W.PARTICLE7, EXT, dspec, lin=dlin)
     sb, db = sm.alloc(), dm.alloc()
     llama.generate(sm, sb, 1)
-    for knobs in ({}, {"jit_chunks": 0}, {"jit_stages": 2, "jit_dst_bufs": 2}, {"jit_stages": 2, "jit_dst_bufs": 3},
-                  {"jit_stages": 3, "jit_dst_bufs": 2}, {"jit_stages": 4, "jit_dst_bufs": 2}, {"jit": 0}):
+    for knobs in ({}, {"jit_chunks": 0}, {"jit_lanes": 3}, {"jit_lanes": 3, "jit_tile": 1024}, {"jit_lanes": 0},
+                  {"jit_stages": 2, "jit_dst_bufs": 2}, {"jit_stages": 2, "jit_dst_bufs": 3}, {"jit": 0}):
         pl = llama.plan(sm, dm, knobs=knobs)
         llama.copy(sm, sb, dm, db, knobs=knobs)
         torch.cuda.synchronize()
