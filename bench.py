@@ -72,6 +72,9 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-child", action="store_true", help=argparse.SUPPRESS)  # the pinned CPU-baseline process
+    # functional test of the N > 1 branch on a one-GPU box (tests/test_gpu_bench.py): every rank on
+    # cuda:0, gloo process group -- exercises the code path, is never a measurement
+    ap.add_argument("--test-one-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--per-pair", default=None, help="write per-pair timings (json) to this file")
     return ap.parse_args(argv)
 
@@ -404,6 +407,7 @@ class Ctx:
         self.torch, self.dist, self.llama = torch, dist, llama
         self.args, self.world, self.rank, self.local = args, world, rank, local
         self.stream = torch.cuda.current_stream()
+        self.rdev = "cpu" if getattr(args, "test_one_device", False) else "cuda"  # reduction tensors (gloo: host)
 
     def barrier(self):
         if self.world > 1:
@@ -412,7 +416,7 @@ class Ctx:
     def max_over_ranks(self, v):
         if self.world == 1:
             return float(v)
-        t = self.torch.tensor([float(v)], device="cuda", dtype=self.torch.float64)
+        t = self.torch.tensor([float(v)], device=self.rdev, dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -580,7 +584,7 @@ def measure_config(ctx, name, steps, warmup, headline=False):
 def sum_over_ranks(ctx, v):
     if ctx.world == 1:
         return float(v)
-    t = ctx.torch.tensor([float(v)], device="cuda", dtype=ctx.torch.float64)
+    t = ctx.torch.tensor([float(v)], device=ctx.rdev, dtype=ctx.torch.float64)
     ctx.dist.all_reduce(t)
     return float(t.item())
 
@@ -621,9 +625,14 @@ def e2e_leg(ctx, maps, src, dst, pairs, steps):
 def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
+    if args.test_one_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.test_one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = Ctx(args, world, rank, local)
     names = (args.configs or (DEFAULT_CONFIGS if args.config == "C2" else args.config)).split(",")
     head = args.config if args.config in names else names[0]
