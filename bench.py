@@ -14,11 +14,12 @@ The same run also measures, as sub-objects of the line (`configs`):
              (the paper's 100-leaf event workload), weak scaling
   C3_soa_sb  the same records, the 4 pairs of {packed, aligned AoS} <-> SoA single-blob
   C4         Listing-1 8192 x 8192, AoSoA32 -> SoA SB, rows sharded over ranks (strong)
+  F1_hep / F1_listing1  Split mappings against plain ones
 each with per-pair GB/s, the dominant kernel's roofline and an in-run
 device-memcpy ceiling; `min_pair_frac` is the weakest pair over all of them.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C3_soa_sb,C4]
+                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C3_soa_sb,C4,F1_hep,F1_listing1]
 
 --gpus N > 1 without torchrun re-launches itself under torch.distributed.run
 with N processes (one per GPU); under torchrun WORLD_SIZE must equal N.
@@ -54,7 +55,7 @@ METRIC = "layout-copy GB/s (read+write) per mapping pair vs 8 TB/s HBM, 1/2/4/8 
 KERNEL = {"permute": "k_permute_ws", "permute_direct": "k_permute_direct", "permute_jit": "llb_jit_permute",
           "blobcopy": "k_bulkcopy",
           "run": "k_run", "naive": "k_naive", "transpose": "k_transpose2d"}
-DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C3_soa_sb,C4"
+DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C3_soa_sb,C4,F1_hep,F1_listing1"
 
 
 def parse(argv=None):
@@ -358,6 +359,14 @@ def workload_desc(name, world):
                              "SoA SB} that involve SoA single-blob, 16,777,216 Particle7 records per GPU",
                     records_per_gpu=16_777_216, pairs=9, l2="inputs larger than L2",
                     parallelism=f"dp{world} (weak scaling)")
+    if name == "F1_hep":
+        return dict(workload="F1: HEP100 x 16,777,216 records per GPU, split_hep (the 4-momenta of the 10 objects -> SoA "
+                             "MB, the rest aligned AoS; P:479-481) <-> packed AoS / SoA MB, 4 pairs",
+                    records_per_gpu=16_777_216, pairs=4, l2="inputs larger than L2", parallelism=f"dp{world} (weak scaling)")
+    if name == "F1_listing1":
+        return dict(workload="F1: Listing-1 record x 67,108,864 per GPU, split_pos (Pos -> SoA MB, the rest packed AoS; "
+                             "S:304) <-> packed / aligned AoS / SoA MB, 6 pairs",
+                    records_per_gpu=67_108_864, pairs=6, l2="inputs larger than L2", parallelism=f"dp{world} (weak scaling)")
     if name == "C3_soa_sb":
         return dict(workload="C3 + SoA SB: HEP100 stand-in x 67,108,864 records per GPU, the 4 ordered pairs of "
                              "{packed AoS, aligned AoS} <-> SoA single-blob", records_per_gpu=67_108_864, pairs=4,
@@ -380,6 +389,9 @@ SUBCFG = {
     "C3": dict(schema="hep100", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_mb"]),
     "C3_soa_sb": dict(schema="hep100", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_sb"]),
     "C4": dict(schema="listing1", extents=[8192, 8192], kinds=["aosoa32", "soa_sb"]),
+    # Split mappings in the same line
+    "F1_hep": dict(schema="hep100", extents=[16_777_216], kinds=["aos", "soa_mb", "split_hep"]),
+    "F1_listing1": dict(schema="listing1", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_mb", "split_pos"]),
 }
 
 
@@ -395,6 +407,11 @@ def pairs_of(name):
         return l2_free_order(sc["kinds"], identities=False)
     if name == "C3_soa_sb":  # the 4 pairs with SoA SB, alternating directions
         return [("aos", "soa_sb"), ("soa_sb", "aos_aligned"), ("aos_aligned", "soa_sb"), ("soa_sb", "aos")]
+    if name == "F1_hep":
+        return [("aos", "split_hep"), ("split_hep", "soa_mb"), ("soa_mb", "split_hep"), ("split_hep", "aos")]
+    if name == "F1_listing1":
+        return [("aos", "split_pos"), ("split_pos", "aos_aligned"), ("soa_mb", "split_pos"), ("split_pos", "aos"),
+                ("aos_aligned", "split_pos"), ("split_pos", "soa_mb")]
     return [("aosoa32", "soa_sb")]
 
 
@@ -437,7 +454,7 @@ def setup_views(ctx, name):
         ext, _ = shard_extents(ext, ctx.world, ctx.rank, multiple=32)
     pairs = pairs_of(name)
     kinds = sorted({x for p in pairs for x in p})
-    maps = {k: llama.Mapping(schema, ext, *W.MAPPINGS[k]) for k in kinds}
+    maps = {k: llama.Mapping.from_spec(schema, ext, W.resolve_spec(k)) for k in kinds}
     src = {k: maps[k].alloc("cuda") for k in kinds}
     dst = {k: maps[k].alloc("cuda") for k in kinds}
     for k in kinds:
