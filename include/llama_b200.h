@@ -255,6 +255,10 @@ typedef enum {
   LLAMA_KNOB_JIT_SOA_TMA,      /* JIT permute: SoA destination leaves stored from registers (0), or staged in shared
                                   memory and TMA-stored per leaf (1) / stored as 16-byte chunks by the consumers
                                   (2; the default when every destination part is SoA) */
+  LLAMA_KNOB_JIT_PAD,          /* JIT permute: shared-memory images of AoS parts whose record-group stride is a
+                                  multiple of 32 bytes get a 16-byte pad per group (bank conflicts), moved as
+                                  16-byte chunks instead of one TMA op: 0 never, 1 strides multiple of 128 B
+                                  (1), 2 every even 16-byte multiple */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

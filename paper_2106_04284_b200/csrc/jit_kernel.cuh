@@ -9,9 +9,14 @@
 // copies, specialised at plan time instead).
 //
 // Generated: the macros LLB_T, LLB_NS, LLB_ND, LLB_SSTAGE, LLB_DSTAGE,
-// LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_P, LLB_G (before this file) and, at the
-// LLB_GENERATED marker, llb_ctab[] (SoA source chunks: smem offset | log2 s_k
-// << 18 | leaf << 20), llb_src_tma(), llb_dst_tma(), llb_permute().
+// LLB_NCHUNK, LLB_NDCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_P, LLB_G, LLB_CW, LLB_DCW,
+// LLB_NSLOT, LLB_NMUL (before this file) and, at the LLB_GENERATED marker,
+// llb_ctab[] / llb_dctab[] (source / destination 16-byte chunks: one word
+// smem offset | log2 s_k << 18 | leaf << 20 per SoA leaf chunk, or, with
+// padded AoS part images (LLB_CW / LLB_DCW == 2), two words: smem offset |
+// slot << 18 and the offset in the tile's run, the global address being
+// gs[slot] + t0 * mul[slot] + offset), llb_fill_slots(), llb_src_tma(),
+// llb_dst_tma(), llb_permute().
 //
 // Roles:
 //   8 consumer warps  wait for source stage s, run llb_permute for their
@@ -102,12 +107,15 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   uint64_t* dempty = full + 24;
   uint8_t* sring = llb_smem + 256;
   uint8_t* dring = sring + LLB_NS * LLB_SSTAGE;
-  // per leaf: the SoA source element-0 pointer minus the leaf's segment offset
-  // in the stage, so a chunk's global address is sgs[k] + soff + (t0 << lg)
+  // per slot: the SoA source element-0 pointer minus the leaf's segment offset
+  // in the stage, so a 1-word chunk's global address is sgs[k] + soff + (t0 <<
+  // lg); 2-word chunks: sgs[slot] + t0 * smul[slot] + offset
   const uint8_t** sgs = reinterpret_cast<const uint8_t**>(dring + LLB_ND * LLB_DSTAGE);
-  uint8_t** dgs = reinterpret_cast<uint8_t**>(dring + LLB_ND * LLB_DSTAGE + 8 * LLB_JIT_MAX_LEAVES);  // SoA dst pointers minus segment offsets
-  uint32_t* ctab = reinterpret_cast<uint32_t*>(dgs + LLB_JIT_MAX_LEAVES);
-  uint32_t* dctab = ctab + LLB_NCHUNK;
+  uint8_t** dgs = reinterpret_cast<uint8_t**>(dring + LLB_ND * LLB_DSTAGE + 8 * LLB_NSLOT);  // SoA dst pointers minus segment offsets
+  uint32_t* smul = reinterpret_cast<uint32_t*>(dgs + LLB_NSLOT);
+  uint32_t* dmul = smul + LLB_NMUL;
+  uint32_t* ctab = dmul + LLB_NMUL;
+  uint32_t* dctab = ctab + ((LLB_NCHUNK * LLB_CW + 1u) & ~1u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < LLB_NS; ++s) llb_mbar_init(&full[s], LLB_CONS);  // every consumer's cp.async arrival (+ TMA bytes)
@@ -121,12 +129,13 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
   // they stay 0 (reading #12)
   for (uint32_t o = 16 * tid; o < LLB_ND * LLB_DSTAGE; o += 16 * (LLB_CONS + 32))
     *reinterpret_cast<uint4*>(dring + o) = make_uint4(0, 0, 0, 0);
-  for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
-  for (uint32_t c = tid; c < LLB_NDCHUNK; c += LLB_CONS + 32) dctab[c] = llb_dctab[c];
+  for (uint32_t c = tid; c < LLB_NCHUNK * LLB_CW; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
+  for (uint32_t c = tid; c < LLB_NDCHUNK * LLB_DCW; c += LLB_CONS + 32) dctab[c] = llb_dctab[c];
   for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) {
     sgs[k] = p.sg[k] - llb_seg[k];
     dgs[k] = p.dg[k] - llb_dseg[k];
   }
+  if (tid == LLB_CONS) llb_fill_slots(p, sgs, smul, dgs, dmul);
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -171,11 +180,20 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
       llb_mbar_expect_tx(&full[s], LLB_SRC_TMA);
       llb_src_tma(p, stage, t0, &full[s]);
     }
+#if LLB_CW == 2
+#pragma unroll 4
+    for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS) {
+      const uint2 e = reinterpret_cast<const uint2*>(ctab)[c];
+      const uint32_t sl = e.x >> 18;
+      llb_cp16(stage + (e.x & 0x3FFFFu), sgs[sl] + t0 * smul[sl] + e.y);
+    }
+#else
 #pragma unroll 4
     for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS) {
       const uint32_t e = ctab[c], so = e & 0x3FFFFu;
       llb_cp16(stage + so, sgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)));
     }
+#endif
     llb_cp_arrive_noinc(&full[s]);
   };
   for (uint32_t i = 0; i < LLB_NS && i < n_my; ++i) issue(i, i);
@@ -196,12 +214,22 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
     llb_cons_sync();  // every consumer is done with stage s (and destination buffer d)
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
     if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
-    // image-staged SoA destination leaves: 16-byte chunks out by every consumer
+    // image-staged SoA destination leaves and padded AoS parts: 16-byte
+    // chunks out by every consumer
+#if LLB_DCW == 2
+#pragma unroll 4
+    for (uint32_t c = tid; c < LLB_NDCHUNK; c += LLB_CONS) {
+      const uint2 e = reinterpret_cast<const uint2*>(dctab)[c];
+      const uint32_t sl = e.x >> 18;
+      llb_stg(dgs[sl] + t0 * dmul[sl] + e.y, *reinterpret_cast<const uint4*>(dim + (e.x & 0x3FFFFu)));
+    }
+#else
 #pragma unroll 4
     for (uint32_t c = tid; c < LLB_NDCHUNK; c += LLB_CONS) {
       const uint32_t e = dctab[c], so = e & 0x3FFFFu;
       llb_stg(dgs[e >> 20] + so + (t0 << ((e >> 18) & 3u)), *reinterpret_cast<const uint4*>(dim + so));
     }
+#endif
     if (++s == LLB_NS) { s = 0; sph ^= 1; }
     if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
   }

@@ -310,7 +310,28 @@ def _jit_cases():
                          (W.PARTICLE7, "split_p7", "aos")]:
         cases.append((f"split_{a}_{b}", llama.Mapping.from_spec(schema, [1 << 20], W.resolve_spec(a)),
                       llama.Mapping.from_spec(schema, [1 << 20], W.resolve_spec(b)), None))
+    for a, b in [("aos_aligned", "split_pos"), ("split_pos", "aos_aligned")]:  # padded images (2-word chunk tables)
+        cases.append((f"pad_{a}_{b}", llama.Mapping.from_spec(W.LISTING1, [1 << 20], W.resolve_spec(a)),
+                      llama.Mapping.from_spec(W.LISTING1, [1 << 20], W.resolve_spec(b)), None))
     return cases
+
+
+def test_jit_padded_image_decision():
+    """Knob jit_pad: Listing-1 aligned records (32 B, groups of 4 -> 128-byte
+    group stride) get padded images by default, moved through 2-word chunk
+    tables; jit_pad=0 keeps the TMA op; HEP100 aligned (480-byte stride) is
+    padded only under jit_pad=2."""
+    al = llama.Mapping.from_spec(W.LISTING1, [1 << 20], W.resolve_spec("aos_aligned"))
+    sp = llama.Mapping.from_spec(W.LISTING1, [1 << 20], W.resolve_spec("split_pos"))
+    src = llama.plan_source(al, sp)
+    assert "#define LLB_CW 2u" in src and "#define LLB_DCW 1u" in src and "r * 144u" in src
+    src = llama.plan_source(sp, al)
+    assert "#define LLB_CW 1u" in src and "#define LLB_DCW 2u" in src and "dgs[" in src
+    src = llama.plan_source(al, sp, knobs={"jit_pad": 0})
+    assert "#define LLB_CW 1u" in src and "r * 144u" not in src
+    h = {k: llama.Mapping(W.HEP100, [1 << 16], *W.MAPPINGS[k]) for k in ("aos_aligned", "soa_mb")}
+    assert "#define LLB_CW 1u" in llama.plan_source(h["aos_aligned"], h["soa_mb"])
+    assert "#define LLB_CW 2u" in llama.plan_source(h["aos_aligned"], h["soa_mb"], knobs={"jit_pad": 2})
 
 
 def test_jit_plans_compile_without_spills():

@@ -76,6 +76,22 @@ def test_splits_jit(llama, oracle_mod, n):
                       knobs={"jit": 2}, paths=("permute",))
 
 
+@pytest.mark.parametrize("pad", [0, 1, 2])
+@pytest.mark.parametrize("n", [64, 4097, 70_001])
+def test_jit_padded_images(llama, oracle_mod, pad, n):
+    """AoS part images with a 16-byte pad per record group (knob jit_pad;
+    group strides multiple of 128 bytes by default: Listing-1 aligned 32-byte
+    records in groups of 4), moved as 2-word-table 16-byte chunks on both
+    sides, next to SoA leaves and packed parts."""
+    cases = [("listing1", "aos_aligned", "split_pos"), ("listing1", "split_pos", "aos_aligned"),
+             ("listing1", "aos", "aos_aligned"), ("listing1", "aos_aligned", "soa_mb"),
+             ("listing1", "soa_mb", "aos_aligned"), ("hep100", "aos_aligned", "soa_mb"),
+             ("hep100", "split_hep", "aos_aligned"), ("particle7", "aos_aligned", "soa_mb")]
+    for schema_name, a, b in cases:
+        run_spec_case(llama, oracle_mod, W.SCHEMAS[schema_name], [n], W.resolve_spec(a), W.resolve_spec(b), seed=n + pad,
+                      knobs={"jit": 2, "jit_pad": pad}, paths=("permute",))
+
+
 def test_jit_chosen_for_wide_records(llama):
     m = {k: llama.Mapping(W.HEP100, [1 << 16], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
     for a in m:
@@ -102,6 +118,8 @@ def test_jit_random_fuzz(llama, oracle_mod, seed):
         knobs["jit_tile"] = rng.choice([32, 64, 128, 256])
     if rng.random() < 0.3:
         knobs["jit_soa_tma"] = rng.choice([0, 2])
+    if rng.random() < 0.3:
+        knobs["jit_pad"] = rng.choice([0, 2])
     for _ in range(6):
         sspec, dspec = _random_spec(rng, k), _random_spec(rng, k)
         run_spec_case(llama, oracle_mod, schema, [n], sspec, dspec, seed=seed, knobs=knobs, paths=("permute",))
