@@ -259,6 +259,12 @@ typedef enum {
                                   multiple of 32 bytes get a 16-byte pad per group (bank conflicts), moved as
                                   16-byte chunks instead of one TMA op: 0 never, 1 strides multiple of 128 B
                                   (1), 2 every even 16-byte multiple */
+  LLAMA_KNOB_JIT_BLOCK,        /* JIT transpose: a thread moves a 4 x 4 block of records with 16-byte vector
+                                  accesses (1) or one record per thread (0) */
+  LLAMA_KNOB_JIT_BMAP,         /* JIT transpose, blocks: thread -> block order 0 x-fastest, 1 y-fastest, 2 / 3
+                                  their diagonals, 4 Morton (default: the fewest simulated bank conflicts) */
+  LLAMA_KNOB_JIT_TORDER,       /* JIT transpose: tile order over the CTAs, 0 x fastest, 1 y fastest, 2 Morton
+                                  within 8 x 8-tile groups */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

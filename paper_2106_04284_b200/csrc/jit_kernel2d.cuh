@@ -72,6 +72,12 @@ __device__ __forceinline__ void llb_stg(uint8_t* p, uint8_t v) { asm volatile("s
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint16_t v) { asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory"); }
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint32_t v) { asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 __device__ __forceinline__ void llb_stg(uint8_t* p, uint64_t v) { asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory"); }
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void llb_stg(uint8_t* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 
 // bits of a 5-bit index spread to the even positions (Morton, #26:
 // the last index supplies bit 0)
@@ -102,6 +108,17 @@ __device__ __forceinline__ void llb_tile_pos(uint32_t lin, uint32_t ty, uint32_t
 }
 
 // ==== LLB_GENERATED ====
+
+// block mode: block b of the tile -> (by, bx) in units of 4 x 4 records
+// (LLB_BMAP: 0 x fastest, 1 y fastest, 2 / 3 their diagonals, 4 Morton)
+__device__ __forceinline__ void llb_bmap(uint32_t b, uint32_t* by, uint32_t* bx) {
+  constexpr uint32_t nby = LLB_TY / 4;
+  if (LLB_BMAP == 0) { *bx = b % 8u; *by = b / 8u; }
+  else if (LLB_BMAP == 1) { *by = b % nby; *bx = b / nby; }
+  else if (LLB_BMAP == 2) { *bx = b % 8u; *by = (b / 8u + *bx) % nby; }
+  else if (LLB_BMAP == 3) { *by = b % nby; *bx = (b / nby + *by) % 8u; }
+  else { *by = llb_unspread(b >> 1); *bx = llb_unspread(b); }
+}
 
 extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_transpose(const __grid_constant__ LlbJitParams p) {
   uint64_t* full = reinterpret_cast<uint64_t*>(llb_smem);
@@ -139,8 +156,17 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
   const uint32_t n_my = first < LLB_NTILES ? (uint32_t)((LLB_NTILES - first + stride - 1) / stride) : 0;
   auto tile_of = [&](uint32_t i, uint32_t* ty, uint32_t* tx) {
     const uint32_t t = (uint32_t)(first + (uint64_t)i * stride);
-    *ty = t / LLB_NTX;
-    *tx = t % LLB_NTX;
+    if (LLB_TORDER == 1) {
+      *ty = t % LLB_NTY;
+      *tx = t / LLB_NTY;
+    } else if (LLB_TORDER == 2) {  // Morton order inside groups of 8 x 8 tiles, groups x fastest
+      const uint32_t g = t / 64u, w = t % 64u;
+      *ty = (g / (LLB_NTX / 8u)) * 8u + llb_unspread(w >> 1);
+      *tx = (g % (LLB_NTX / 8u)) * 8u + llb_unspread(w);
+    } else {
+      *ty = t / LLB_NTX;
+      *tx = t % LLB_NTX;
+    }
   };
 
   if (warp == LLB_CONS / 32) {  // ------------------------------ store warp
@@ -191,6 +217,18 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     llb_cons_sync();
     const uint8_t* sim = sring + s * LLB_SSTAGE;
     uint8_t* dim = dring + d * LLB_DSTAGE;
+#if LLB_BLOCK
+    // a thread = one 4 x 4 block and program part (warp % LLB_P)
+    {
+      const uint32_t part = (uint32_t)warp % LLB_P, grp = (uint32_t)warp / LLB_P;
+#pragma unroll 1
+      for (uint32_t b = grp * 32u + (uint32_t)lane; b < (LLB_TY / 4) * 8u; b += LLB_CONS / LLB_P) {
+        uint32_t by, bx;
+        llb_bmap(b, &by, &bx);
+        llb_block2d(p, sim, dim, ty, tx, by, bx, part);
+      }
+    }
+#else
     // lanes run along the destination's storage order when it is stored
     // straight to global memory (SoA leaves): row (xx), column (yy), Morton
     // (the low 5 bits of the tile's Morton code) -- coalesced element stores
@@ -211,6 +249,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
       } else { yy = q; xx = (uint32_t)lane; }
       llb_permute2d(p, sim, dim, ty, tx, yy, xx);
     }
+#endif
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     llb_cons_sync();
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);

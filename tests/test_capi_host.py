@@ -316,6 +316,17 @@ def _jit_cases():
     return cases
 
 
+def test_jit_transpose_block_chosen():
+    """Block programs are the default for transposes into SoA destinations
+    (not next to a Morton SoA side), per-record programs into AoS images."""
+    for sk, sl, dk, dl, blk in [("soa_mb", "col", "soa_mb", "row", 1), ("aos", "row", "soa_mb", "col", 1),
+                                ("aos", "row", "aos", "col", 0), ("soa_mb", "morton", "soa_mb", "row", 0)]:
+        sm = llama.Mapping.from_spec(W.PARTICLE7, [256, 256], (sk, 1, False), lin=sl)
+        dm = llama.Mapping.from_spec(W.PARTICLE7, [256, 256], (dk, 1, False), lin=dl)
+        assert llama.plan(sm, dm)["jit"]
+        assert f"#define LLB_BLOCK {blk}" in llama.plan_source(sm, dm), (sk, sl, dk, dl)
+
+
 def test_jit_padded_image_decision():
     """Knob jit_pad: Listing-1 aligned records (32 B, groups of 4 -> 128-byte
     group stride) get padded images by default, moved through 2-word chunk

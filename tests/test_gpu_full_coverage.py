@@ -199,7 +199,8 @@ F4 = [(("soa_mb", 1, False), "col", ("soa_mb", 1, False), "row"),
       (("aos", 1, False), "row", ("soa_mb", 1, False), "col"),
       (("soa_mb", 1, False), "morton", ("aos", 1, False), "col"),
       (("aos", 1, False), "row", ("aos", 1, False), "col"),
-      (("aos", 1, False), "row", ("aos", 1, False), "morton")]
+      (("aos", 1, False), "row", ("aos", 1, False), "morton"),
+      (("soa_mb", 1, False), "row", ("aos", 1, False), "col")]
 
 
 @pytest.mark.parametrize("case", range(len(F4)))

@@ -92,6 +92,27 @@ def test_jit_padded_images(llama, oracle_mod, pad, n):
                       knobs={"jit": 2, "jit_pad": pad}, paths=("permute",))
 
 
+T2D_KINDS = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, True)]
+T2D_LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "col"), ("col", "morton"), ("morton", "row")]
+
+
+@pytest.mark.parametrize("knobs", [{}, {"jit_block": 0}, {"jit_bmap": 0}, {"jit_bmap": 1}, {"jit_bmap": 2},
+                                   {"jit_bmap": 3}, {"jit_bmap": 4}, {"jit_tile": 512}, {"jit_tile": 1024}])
+def test_jit_transpose_knobs(llama, oracle_mod, knobs):
+    """The JIT transposing copy (rank 2, different linearisations):
+    4 x 4 record blocks under every thread -> block order, per-record
+    programs, both tile heights; Particle7 (4-byte leaves) and Listing-1
+    (1- to 8-byte leaves, aligned records); every destination byte against
+    the oracle."""
+    from test_gpu_lin_trace import _pair
+    for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [32, 64])):
+        for sk in T2D_KINDS:
+            for dk in T2D_KINDS:
+                for lins in T2D_LINS:
+                    _pair(llama, oracle_mod, schema, ext if "morton" not in lins else [64, 64], sk, lins[0], dk,
+                          lins[1], seed=21, paths=("auto",), knobs=dict(knobs, jit=2))
+
+
 def test_jit_chosen_for_wide_records(llama):
     m = {k: llama.Mapping(W.HEP100, [1 << 16], *KINDS[k]) for k in ("aos", "aos_aligned", "soa_mb")}
     for a in m:

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
-"""Stage / buffer sweep of the JIT transposing copy (llb_jit_transpose) on the
-f4 cases (4096 x 4096 Particle7): GB/s per (jit_stages, jit_dst_bufs)."""
+"""Knob sweep of the JIT transposing copy (llb_jit_transpose) on the f4 cases
+(4096 x 4096 Particle7): GB/s per knob set (block / per-record programs,
+block orders, tile, stages / buffers)."""
 import os
 import sys
 
@@ -14,13 +15,18 @@ EXT = [4096, 4096]
 AOS, SOA = ("aos", 1, False), ("soa_mb", 1, False)
 CASES = [(AOS, "row", AOS, "col"), (AOS, "row", SOA, "col"), (SOA, "col", SOA, "row"), (AOS, "row", AOS, "morton"),
          (SOA, "morton", AOS, "col"), (SOA, "row", AOS, "col")]
+KNOBS = [{}, {"jit_block": 0}, {"jit_bmap": 0}, {"jit_bmap": 1}, {"jit_bmap": 2}, {"jit_bmap": 3}, {"jit_bmap": 4},
+         {"jit_tile": 1024}, {"jit_tile": 512}, {"jit_stages": 2, "jit_dst_bufs": 2}, {"jit_stages": 3, "jit_dst_bufs": 3},
+         {"jit": 0}]
+if len(sys.argv) > 1:  # knob sets as JSON: python tools/f4_sweep.py '[{}, {"jit_block": 0}]'
+    import json
+    KNOBS = json.loads(sys.argv[1])
 for sspec, slin, dspec, dlin in CASES:
     sm = llama.Mapping.from_spec(W.PARTICLE7, EXT, sspec, lin=slin)
     dm = llama.Mapping.from_spec(W.PARTICLE7, EXT, dspec, lin=dlin)
     sb, db = sm.alloc(), dm.alloc()
     llama.generate(sm, sb, 1)
-    for knobs in ({}, {"jit_chunks": 0}, {"jit_lanes": 3}, {"jit_lanes": 3, "jit_tile": 1024}, {"jit_lanes": 0},
-                  {"jit_stages": 2, "jit_dst_bufs": 2}, {"jit_stages": 2, "jit_dst_bufs": 3}, {"jit": 0}):
+    for knobs in KNOBS:
         pl = llama.plan(sm, dm, knobs=knobs)
         llama.copy(sm, sb, dm, db, knobs=knobs)
         torch.cuda.synchronize()
