@@ -265,6 +265,10 @@ typedef enum {
                                   their diagonals, 4 Morton (default: the fewest simulated bank conflicts) */
   LLAMA_KNOB_JIT_TORDER,       /* JIT transpose: tile order over the CTAs, 0 x fastest, 1 y fastest, 2 Morton
                                   within 8 x 8-tile groups */
+  LLAMA_KNOB_JIT_DST_LSU,      /* JIT transpose: AoS destination segments stored by the store warp's TMA ops (0) or
+                                  as 16-byte chunks by the consumers (1; default unless the destination is Morton) */
+  LLAMA_KNOB_JIT_ABLATE,        /* JIT kernels, ablation only: 1 = skip the move program (tile loads and stores
+                                  only; the destination is NOT the copy) to measure the data movement alone (0) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

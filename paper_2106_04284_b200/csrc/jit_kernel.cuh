@@ -209,7 +209,8 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_pe
     const uint8_t* sim = sring + s * LLB_SSTAGE;
     uint8_t* dim = dring + d * LLB_DSTAGE;
     // r = a group of LLB_G consecutive records (lane = group)
-    for (uint32_t r = grp * 32 + lane; r < LLB_T / LLB_G; r += (LLB_CONS / LLB_P)) llb_permute(p, sim, dim, t0, part, r);
+    for (uint32_t r = grp * 32 + lane; r < LLB_T / LLB_G; r += (LLB_CONS / LLB_P))
+      if (!LLB_ABLATE) llb_permute(p, sim, dim, t0, part, r);
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     llb_cons_sync();  // every consumer is done with stage s (and destination buffer d)
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);

@@ -225,7 +225,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
       for (uint32_t b = grp * 32u + (uint32_t)lane; b < (LLB_TY / 4) * 8u; b += LLB_CONS / LLB_P) {
         uint32_t by, bx;
         llb_bmap(b, &by, &bx);
-        llb_block2d(p, sim, dim, ty, tx, by, bx, part);
+        if (!LLB_ABLATE) llb_block2d(p, sim, dim, ty, tx, by, bx, part);
       }
     }
 #else
@@ -247,13 +247,14 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
         yy = llb_unspread(code >> 1);
         xx = llb_unspread(code);
       } else { yy = q; xx = (uint32_t)lane; }
-      llb_permute2d(p, sim, dim, ty, tx, yy, xx);
+      if (!LLB_ABLATE) llb_permute2d(p, sim, dim, ty, tx, yy, xx);
     }
 #endif
     if (LLB_ND > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     llb_cons_sync();
     if (LLB_ND > 0 && tid == 0) llb_mbar_arrive(&dfull[d]);
     if (i + LLB_NS < n_my) issue(i + LLB_NS, s);
+    llb_dst_lsu2d(p, dim, ty, tx, (uint32_t)tid);  // AoS destination segments as 16-byte chunks (knob jit_dst_lsu)
     if (++s == LLB_NS) { s = 0; sph ^= 1; }
     if (LLB_ND > 0 && ++d == (LLB_ND > 0 ? LLB_ND : 1)) { d = 0; dph ^= 1; }
   }
