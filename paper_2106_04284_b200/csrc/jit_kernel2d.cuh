@@ -117,7 +117,10 @@ __device__ __forceinline__ void llb_bmap(uint32_t b, uint32_t* by, uint32_t* bx)
   else if (LLB_BMAP == 1) { *by = b % nby; *bx = b / nby; }
   else if (LLB_BMAP == 2) { *bx = b % 8u; *by = (b / 8u + *bx) % nby; }
   else if (LLB_BMAP == 3) { *by = b % nby; *bx = (b / nby + *by) % 8u; }
-  else { *by = llb_unspread(b >> 1); *bx = llb_unspread(b); }
+  else {  // Morton over the 8 columns and the first 8 rows of blocks, then further rows (64-row tiles)
+    *by = llb_unspread((b >> 1) & 0x15u) | ((b >> 6) << 3);
+    *bx = llb_unspread(b & 0x15u);
+  }
 }
 
 extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_transpose(const __grid_constant__ LlbJitParams p) {
