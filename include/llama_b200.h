@@ -267,6 +267,8 @@ typedef enum {
                                   within 8 x 8-tile groups */
   LLAMA_KNOB_JIT_DST_LSU,      /* JIT transpose: AoS destination segments stored by the store warp's TMA ops (0) or
                                   as 16-byte chunks by the consumers (1; default unless the destination is Morton) */
+  LLAMA_KNOB_JIT_SWIZZLE,      /* JIT transpose, blocks: source segment chunks XOR-swizzled by block row / column
+                                  (1) or plain padded pitches (0) */
   LLAMA_KNOB_JIT_ABLATE,        /* JIT kernels, ablation only: 1 = skip the move program (tile loads and stores
                                   only; the destination is NOT the copy) to measure the data movement alone (0) */
   LLAMA_KNOB_COUNT

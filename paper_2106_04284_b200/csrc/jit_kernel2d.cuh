@@ -19,7 +19,8 @@
 // LLB_NCHUNK, LLB_SRC_TMA, LLB_MINB, LLB_NTX (tiles along x), LLB_NTILES,
 // LLB_H, LLB_W (extents), LLB_SLIN / LLB_DLIN (0 row, 1 col, 2 Morton); at the
 // marker: llb_ctab[] (chunk: smem offset | log2 s_k << 18 | leaf << 20, and
-// the segment index in a second word), llb_seg_delta[] (per leaf), llb_src_tma2d(),
+// segment index | chunk index in the segment << 16 in a second word; the smem
+// offset may be swizzled), llb_src_tma2d(),
 // llb_dst_tma2d(), llb_permute2d().
 
 #ifndef LLB_CONS
@@ -130,8 +131,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
   uint8_t* sring = llb_smem + 256;
   uint8_t* dring = sring + LLB_NS * LLB_SSTAGE;
   const uint8_t** sgs = reinterpret_cast<const uint8_t**>(dring + LLB_ND * LLB_DSTAGE);
-  long long* sdelta = reinterpret_cast<long long*>(sgs + LLB_JIT_MAX_LEAVES);
-  uint32_t* ctab = reinterpret_cast<uint32_t*>(sdelta + LLB_JIT_MAX_LEAVES);
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(sgs + 2 * LLB_JIT_MAX_LEAVES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < LLB_NS; ++s) llb_mbar_init(&full[s], LLB_CONS);
@@ -144,10 +144,7 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
   for (uint32_t o = 16 * tid; o < LLB_ND * LLB_DSTAGE; o += 16 * (LLB_CONS + 32))
     *reinterpret_cast<uint4*>(dring + o) = make_uint4(0, 0, 0, 0);
   for (uint32_t c = tid; c < 2 * LLB_NCHUNK; c += LLB_CONS + 32) ctab[c] = llb_ctab[c];
-  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) {
-    sgs[k] = p.sg[k] - llb_seg_base[k];
-    sdelta[k] = llb_seg_delta[k];
-  }
+  for (uint32_t k = tid; k < p.K; k += LLB_CONS + 32) sgs[k] = p.sg[k];
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -202,8 +199,8 @@ extern "C" __global__ void __launch_bounds__(LLB_CONS + 32, LLB_MINB) llb_jit_tr
     llb_tile_pos(LLB_SLIN, ty, tx, &pos0, &pitch);
 #pragma unroll 4
     for (uint32_t c = tid; c < LLB_NCHUNK; c += LLB_CONS) {
-      const uint32_t e = ctab[2 * c], sg = ctab[2 * c + 1], so = e & 0x3FFFFu, lg = (e >> 18) & 3u, k = e >> 20;
-      llb_cp16(stage + so, sgs[k] + so + ((pos0 + (uint64_t)sg * pitch) << lg) - (long long)sg * sdelta[k]);
+      const uint32_t e = ctab[2 * c], w = ctab[2 * c + 1], so = e & 0x3FFFFu, lg = (e >> 18) & 3u, k = e >> 20;
+      llb_cp16(stage + so, sgs[k] + ((pos0 + (uint64_t)(w & 0xFFFFu) * pitch) << lg) + 16u * (w >> 16));
     }
     llb_cp_arrive_noinc(&full[s]);
   };

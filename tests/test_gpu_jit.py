@@ -99,7 +99,9 @@ T2D_LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "col")
 @pytest.mark.parametrize("knobs", [{}, {"jit_block": 0}, {"jit_bmap": 0}, {"jit_bmap": 1}, {"jit_bmap": 2},
                                    {"jit_bmap": 3}, {"jit_bmap": 4}, {"jit_tile": 512}, {"jit_tile": 1024},
                                    {"jit_dst_lsu": 1}, {"jit_dst_lsu": 1, "jit_block": 1}, {"jit_torder": 1},
-                                   {"jit_torder": 2}, {"jit_tile": 2048}, {"jit_tile": 2048, "jit_stages": 2}])
+                                   {"jit_torder": 2}, {"jit_tile": 2048}, {"jit_tile": 2048, "jit_stages": 2},
+                                   {"jit_swizzle": 1}, {"jit_swizzle": 1, "jit_bmap": 2},
+                                   {"jit_swizzle": 1, "jit_block": 1, "jit_tile": 1024}])
 def test_jit_transpose_knobs(llama, oracle_mod, knobs):
     """The JIT transposing copy (rank 2, different linearisations):
     4 x 4 record blocks under every thread -> block order, per-record

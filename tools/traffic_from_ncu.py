@@ -50,12 +50,51 @@ def load(path):
     return launches
 
 
+def pair_bytes(cfg):
+    """Algorithmic bytes (source + destination footprint) of each pair of a
+    bench sub-config, in bench.py's pair order (bench.SUBCFG / pairs_of)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2106_04284_b200 as llama
+    import workloads as W
+    sc = bench.SUBCFG[cfg]
+    schema = W.SCHEMAS[sc["schema"]]
+    out = []
+    for a, b in bench.pairs_of(cfg):
+        sm = llama.Mapping.from_spec(schema, sc["extents"], W.resolve_spec(a))
+        dm = llama.Mapping.from_spec(schema, sc["extents"], W.resolve_spec(b))
+        out.append(sm.footprint() + dm.footprint())
+    return out
+
+
 def main(args):
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     out = {}
     for spec in args:
         path, cfg = spec.split(":")
         launches = load(path)
+        if cfg.startswith("@"):  # a bench sub-config run pair by pair (tools/r02_profile3.sh): per-launch bytes
+            cfg = cfg[1:]
+            pb = pair_bytes(cfg)
+            copies = [(name, m) for (lid, name), m in sorted(launches.items(), key=lambda kv: int(kv[0][0]))
+                      if short(name) not in ("k_gen", "k_fill")]
+            timed = copies[1::2]  # warm-up + timed launch per pair
+            per = defaultdict(list)
+            for j, (name, m) in enumerate(timed[:len(pb)]):
+                per[short(name)].append((m, pb[j]))
+            for k, ms in per.items():
+                dram = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m, _ in ms) / len(ms)
+                dur = sum(m.get("gpu__time_duration.sum", 0) for m, _ in ms) / len(ms)
+                algo = sum(b for _, b in ms) / len(ms)
+                out[f"{cfg}/{k}"] = {
+                    "launches": len(ms), "dram_bytes_per_launch": dram,
+                    "dram_read_per_launch": sum(m.get("dram__bytes_read.sum", 0) for m, _ in ms) / len(ms),
+                    "dram_write_per_launch": sum(m.get("dram__bytes_write.sum", 0) for m, _ in ms) / len(ms),
+                    "duration_s_per_launch": dur, "algorithmic_bytes_per_launch": algo,
+                    "cold_frac": algo / dur / 1e9 / peak, "dram_over_algorithmic": dram / algo,
+                    "source": f"{os.path.basename(path)} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
+                              "gpu__time_duration.sum --clock-control none; tools/r02_profile3.sh)"}
+            continue
         per = defaultdict(list)
         for (lid, name), m in sorted(launches.items(), key=lambda kv: int(kv[0][0])):
             per[short(name)].append(m)
