@@ -65,13 +65,12 @@ int launch_bulkcopy(const BulkCopyParams& p, void* stream) {
   const uint64_t total = p.cstart[p.nb];
   if (total == 0) return 0;
   const int smem = 128 + (int)(p.NS * p.CH);
-  cudaError_t e = cudaFuncSetAttribute(k_bulkcopy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return (int)e;
-  cudaFuncSetAttribute(k_bulkcopy, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  int sms = 148, per_sm = 1;
+  static LaunchCache cache[64];
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  int e = prepare_kernel(k_bulkcopy, kThreads, smem, &cache[dev & 63], &per_sm);
+  if (e) return e;
   current_device_sms(&sms);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bulkcopy, kThreads, smem);
-  if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
   if (grid > total) grid = total;
   k_bulkcopy<<<(unsigned)grid, kThreads, smem, (cudaStream_t)stream>>>(p);

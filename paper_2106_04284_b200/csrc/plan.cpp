@@ -190,8 +190,15 @@ bool plan_blobcopy(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p,
   BulkCopyParams& b = *p->bulkcopy;
   std::memset(&b, 0, sizeof(b));
   b.nb = d.nblobs();
-  b.CH = (uint32_t)kn.get(LLAMA_KNOB_BULK_CHUNK, 65536) & ~15u;  // 64 KB x 3 stages: measured best on B200
+  const uint64_t ch = kn.get(LLAMA_KNOB_BULK_CHUNK, 65536) & ~15ull;  // 64 KB x 3 stages: measured best on B200
   b.NS = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_BULK_STAGES, 3)));
+  b.CH = (uint32_t)std::min<uint64_t>(ch, 1u << 30);
+  // the ring (bulk_chunk x bulk_stages) must fit one CTA's shared memory
+  if (ch < 16 || 128 + (uint64_t)b.NS * ch > 227ull * 1024) {
+    *why = "bulk_chunk x bulk_stages exceed 227 KB of shared memory";
+    p->bulkcopy.reset();
+    return false;
+  }
   for (int j = 0; j < b.nb; ++j) {
     b.bytes[j] = d.blob_sizes[j];
     b.cstart[j + 1] = b.cstart[j] + ceil_div(d.blob_sizes[j], b.CH);
