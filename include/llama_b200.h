@@ -269,6 +269,8 @@ typedef enum {
                                   as 16-byte chunks by the consumers (1; default unless the destination is Morton) */
   LLAMA_KNOB_JIT_SWIZZLE,      /* JIT transpose, blocks: source segment chunks XOR-swizzled by block row / column
                                   (1) or plain padded pitches (0) */
+  LLAMA_KNOB_JIT_GROUP,        /* JIT permute: records per thread group, 1 / 2 / 4 (at least what odd record strides
+                                  need; larger groups move SoA / AoSoA leaves and AoS records as wider vectors) */
   LLAMA_KNOB_JIT_ABLATE,        /* JIT kernels, ablation only: 1 = skip the move program (tile loads and stores
                                   only; the destination is NOT the copy) to measure the data movement alone (0) */
   LLAMA_KNOB_COUNT

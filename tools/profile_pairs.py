@@ -24,6 +24,8 @@ ap.add_argument("--path", default=None)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--records", type=int, default=0)
 ap.add_argument("--knobs", default="")
+ap.add_argument("--stagger", type=int, default=0, help="allocate blob k at a k * STAGGER byte offset (alignment study)")
+ap.add_argument("--pool", action="store_true", help="all blobs of a side in one allocation, back to back")
 a = ap.parse_args()
 knobs = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)} or None
 cfg = W.CONFIGS[a.config]
@@ -33,7 +35,20 @@ for pair in a.pairs.split(","):
     s, d = pair.split(":")
     sm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(s))
     dm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(d))
-    sb, db = sm.alloc(), dm.alloc()
+    def alloc(m):
+        if a.pool:
+            sizes = [(x + 255) // 256 * 256 for x in m.blob_sizes()]
+            base = torch.empty(sum(sizes) + 256, dtype=torch.uint8, device="cuda")
+            out, o = [], 0
+            for x, sz in zip(m.blob_sizes(), sizes):
+                out.append(base[o:o + x])
+                o += sz
+            return out
+        if not a.stagger:
+            return m.alloc()
+        return [torch.empty(x + k * a.stagger + 16, dtype=torch.uint8, device="cuda")[k * a.stagger:k * a.stagger + x]
+                for k, x in enumerate(m.blob_sizes())]
+    sb, db = alloc(sm), alloc(dm)
     llama.generate(sm, sb, 42)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
