@@ -148,3 +148,32 @@ def test_jit_random_fuzz(llama, oracle_mod, seed):
     for _ in range(6):
         sspec, dspec = _random_spec(rng, k), _random_spec(rng, k)
         run_spec_case(llama, oracle_mod, schema, [n], sspec, dspec, seed=seed, knobs=knobs, paths=("permute",))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_jit_transpose_fuzz(llama, oracle_mod, seed):
+    """Random schemas (1- to 8-byte leaves, arrays, nesting) x AoS / SoA kinds
+    x different storage orders of rank-2 views whose extents fit the 2-d
+    tiles, forced onto the JIT transposing copy with a random geometry (block
+    or per-record programs, thread -> block order, tile height, copy-out,
+    swizzle); every destination byte against the oracle (pairs the JIT path
+    cannot take fall back to the other kernels and are checked the same way)."""
+    import random
+
+    from test_gpu_lin_trace import _pair
+    from test_gpu_parity import _random_schema
+    rng = random.Random(5000 + seed)
+    schema = _random_schema(rng)
+    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False), ("soa_sb", 1, True)]
+    for _ in range(6):  # (about a third of the draws are JIT-eligible: 4-byte-multiple AoS records, SoA)
+        ext = rng.choice([[64, 64], [128, 64], [64, 96], [32, 32], [48, 32]])
+        lins = ["row", "col"] + (["morton"] if ext[0] == ext[1] else [])
+        slin = rng.choice(lins)
+        dlin = rng.choice([x for x in lins if x != slin])
+        knobs = {"jit": 2}
+        for name, choices in (("jit_block", [0, 1]), ("jit_bmap", [0, 1, 2, 3, 4]), ("jit_tile", [512, 1024, 2048]),
+                              ("jit_dst_lsu", [0, 1]), ("jit_swizzle", [0, 1]), ("jit_lanes", [0, 1, 2, 3])):
+            if rng.random() < 0.4:
+                knobs[name] = rng.choice(choices)
+        _pair(llama, oracle_mod, schema, ext, rng.choice(kinds), slin, rng.choice(kinds), dlin, seed=seed,
+              paths=("auto",), knobs=knobs)
