@@ -19,7 +19,7 @@ each with per-pair GB/s, the dominant kernel's roofline and an in-run
 device-memcpy ceiling; `min_pair_frac` is the weakest pair over all of them.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C3_soa_sb,C4,F1_hep,F1_listing1]
+                    [--config C2|C3|C4|C5|MOVE] [--configs C2,C2_soa_sb,C3,C3_soa_sb,C4,C4_pairs,F1_hep,F1_listing1]
 
 --gpus N > 1 without torchrun re-launches itself under torch.distributed.run
 with N processes (one per GPU); under torchrun WORLD_SIZE must equal N.
@@ -55,7 +55,7 @@ METRIC = "layout-copy GB/s (read+write) per mapping pair vs 8 TB/s HBM, 1/2/4/8 
 KERNEL = {"permute": "k_permute_ws", "permute_direct": "k_permute_direct", "permute_jit": "llb_jit_permute",
           "blobcopy": "k_bulkcopy",
           "run": "k_run", "naive": "k_naive", "transpose": "k_transpose2d"}
-DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C3_soa_sb,C4,F1_hep,F1_listing1"
+DEFAULT_CONFIGS = "C2,C2_soa_sb,C3,C3_soa_sb,C4,C4_pairs,F1_hep,F1_listing1"
 
 
 def parse(argv=None):
@@ -363,6 +363,11 @@ def workload_desc(name, world):
         return dict(workload="F1: HEP100 x 16,777,216 records per GPU, split_hep (the 4-momenta of the 10 objects -> SoA "
                              "MB, the rest aligned AoS; P:479-481) <-> packed AoS / SoA MB, 4 pairs",
                     records_per_gpu=16_777_216, pairs=4, l2="inputs larger than L2", parallelism=f"dp{world} (weak scaling)")
+    if name == "C4_pairs":
+        return dict(workload="C4 record (Listing-1: 1- to 8-byte leaves, 21-byte packed / 32-byte aligned) x "
+                             "67,108,864 per GPU, the 12 ordered pairs of {packed AoS, aligned AoS, SoA MB, AoSoA32}",
+                    records_per_gpu=67_108_864, pairs=12, l2="inputs larger than L2; consecutive copies share no buffer",
+                    parallelism=f"dp{world} (weak scaling)")
     if name == "F1_listing1":
         return dict(workload="F1: Listing-1 record x 67,108,864 per GPU, split_pos (Pos -> SoA MB, the rest packed AoS; "
                              "S:304) <-> packed / aligned AoS / SoA MB, 6 pairs",
@@ -392,6 +397,7 @@ SUBCFG = {
     # Split mappings in the same line
     "F1_hep": dict(schema="hep100", extents=[16_777_216], kinds=["aos", "soa_mb", "split_hep"]),
     "F1_listing1": dict(schema="listing1", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_mb", "split_pos"]),
+    "C4_pairs": dict(schema="listing1", extents=[67_108_864], kinds=["aos", "aos_aligned", "soa_mb", "aosoa32"]),
 }
 
 
@@ -409,6 +415,8 @@ def pairs_of(name):
         return [("aos", "soa_sb"), ("soa_sb", "aos_aligned"), ("aos_aligned", "soa_sb"), ("soa_sb", "aos")]
     if name == "F1_hep":
         return [("aos", "split_hep"), ("split_hep", "soa_mb"), ("soa_mb", "split_hep"), ("split_hep", "aos")]
+    if name == "C4_pairs":  # the 12 non-identity pairs, consecutive ones sharing no buffer
+        return l2_free_order(sc["kinds"])[len(sc["kinds"]):]
     if name == "F1_listing1":
         return [("aos", "split_pos"), ("split_pos", "aos_aligned"), ("soa_mb", "split_pos"), ("split_pos", "aos"),
                 ("aos_aligned", "split_pos"), ("split_pos", "soa_mb")]

@@ -271,6 +271,8 @@ typedef enum {
                                   (1) or plain padded pitches (0) */
   LLAMA_KNOB_JIT_GROUP,        /* JIT permute: records per thread group, 1 / 2 / 4 (at least what odd record strides
                                   need; larger groups move SoA / AoSoA leaves and AoS records as wider vectors) */
+  LLAMA_KNOB_JIT_CTAS,         /* JIT permute: most CTAs per SM the launch bounds promise (4; the register budget
+                                  per thread shrinks with it) */
   LLAMA_KNOB_JIT_ABLATE,        /* JIT kernels, ablation only: 1 = skip the move program (tile loads and stores
                                   only; the destination is NOT the copy) to measure the data movement alone (0) */
   LLAMA_KNOB_COUNT

@@ -69,17 +69,21 @@ def test_relaunch_runs_n_processes_without_a_gpu():
     assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
 
 
-@pytest.mark.parametrize("name", ["C2", "C2_soa_sb", "C3", "C3_soa_sb", "C4", "F1_hep", "F1_listing1"])
+@pytest.mark.parametrize("name", ["C2", "C2_soa_sb", "C3", "C3_soa_sb", "C4", "C4_pairs", "F1_hep", "F1_listing1"])
 def test_pair_orders(name):
     pairs = bench.pairs_of(name)
-    expected = {"C2": 16, "C2_soa_sb": 9, "C3": 6, "C3_soa_sb": 4, "C4": 1, "F1_hep": 4, "F1_listing1": 6}[name]
+    expected = {"C2": 16, "C2_soa_sb": 9, "C3": 6, "C3_soa_sb": 4, "C4": 1, "C4_pairs": 12, "F1_hep": 4,
+                "F1_listing1": 6}[name]
     assert len(pairs) == len(set(pairs)) == expected
     if name == "C2":
         kinds = bench.SUBCFG["C2"]["kinds"]
         assert set(pairs) == {(a, b) for a in kinds for b in kinds}
+    if name == "C4_pairs":
+        kinds = bench.SUBCFG[name]["kinds"]
+        assert set(pairs) == {(a, b) for a in kinds for b in kinds if a != b}
     if name in ("C2_soa_sb", "C3_soa_sb"):
         assert all("soa_sb" in p for p in pairs)
-    for j in range(len(pairs) - (0 if name in ("C2", "C3") else 1)):
+    for j in range(len(pairs) - (0 if name in ("C2", "C3", "C4_pairs") else 1)):
         a, b = pairs[j], pairs[(j + 1) % len(pairs)]
         if ("soa_sb", "soa_sb") in (a, b) or name.startswith("F1"):  # (F1: splits against 2-3 kinds)
             continue

@@ -19,6 +19,7 @@ run C3 C3 67108864
 run C3_soa_sb C3 67108864
 run F1_hep C3 16777216
 run F1_listing1 C4 67108864
+run C4_pairs C4 67108864
 S="smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct,smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
 python tools/f4_sweep.py '[{}]' > gpurun_out/f4_pre3.txt 2>&1
 ncu --metrics $S --clock-control none --csv --log-file gpurun_out/r02_sectors_f4_jit.csv -k regex:llb_jit python tools/f4_sweep.py '[{}]' > /dev/null 2>&1
