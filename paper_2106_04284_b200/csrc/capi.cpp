@@ -304,8 +304,13 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
         if (plan->bulkcopy) {
           llb::BulkCopyParams p = *plan->bulkcopy;
           for (int b = 0; b < p.nb; ++b) {
-            p.src[b] = static_cast<const uint8_t*>(src_blobs[b]);
-            p.dst[b] = static_cast<uint8_t*>(dst_blobs[b]);
+            if (p.seg) {
+              p.src[b] = static_cast<const uint8_t*>(src_blobs[p.sblob[b]]) + p.soff[b];
+              p.dst[b] = static_cast<uint8_t*>(dst_blobs[p.dblob[b]]) + p.doff[b];
+            } else {
+              p.src[b] = static_cast<const uint8_t*>(src_blobs[b]);
+              p.dst[b] = static_cast<uint8_t*>(dst_blobs[b]);
+            }
           }
           e = llb::launch_bulkcopy(p, stream);
           break;

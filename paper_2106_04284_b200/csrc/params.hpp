@@ -124,6 +124,11 @@ struct BulkCopyParams {
   uint64_t bytes[kMaxBlobs];
   const uint8_t* src[kMaxBlobs];
   uint8_t* dst[kMaxBlobs];
+  // segments (seg = 1): range j is leaf j's single contiguous run on both
+  // sides, src[j] = src blob sblob[j] + soff[j] (patched per call)
+  int32_t seg;
+  int32_t sblob[kMaxBlobs], dblob[kMaxBlobs];
+  uint64_t soff[kMaxBlobs], doff[kMaxBlobs];
 };
 
 // ------------------------------------------------------------------ run copy

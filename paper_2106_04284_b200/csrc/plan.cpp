@@ -171,8 +171,49 @@ bool plan_transpose(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p
   return true;
 }
 
+// Every leaf one contiguous run of N * s_k bytes in the mapping (SoA single /
+// multi blob, a part of one block), starting 16-byte aligned.
+static bool single_runs(const Mapping& m) {
+  for (int k = 0; k < m.K(); ++k) {
+    const bool run = m.Lk[k] >= m.N || m.Bk[k] == m.Lk[k] * m.sizes[k];
+    if (!run || (m.base[k] + m.F[k]) % 16) return false;
+  }
+  return true;
+}
+
+// Different layouts whose leaves are single runs on both sides (SoA SB <-> MB):
+// one bulk-copy range per leaf (each leaf's array moves as it is).
+static bool plan_segments(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
+  if (!single_runs(s) || !single_runs(d)) { *why = "leaves are not single contiguous runs"; return false; }
+  if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
+  if (s.K() > kMaxBlobs) { *why = "too many leaves"; return false; }
+  const uint64_t ch = kn.get(LLAMA_KNOB_BULK_CHUNK, 65536) & ~15ull;
+  const uint32_t ns = (uint32_t)std::min<uint64_t>(8, std::max<uint64_t>(2, kn.get(LLAMA_KNOB_BULK_STAGES, 3)));
+  if (ch < 16 || 128 + (uint64_t)ns * ch > 227ull * 1024) {
+    *why = "bulk_chunk x bulk_stages exceed 227 KB of shared memory";
+    return false;
+  }
+  p->path = LLAMA_PATH_BLOBCOPY;
+  p->bulkcopy.reset(new BulkCopyParams);
+  BulkCopyParams& b = *p->bulkcopy;
+  std::memset(&b, 0, sizeof(b));
+  b.seg = 1;
+  b.nb = s.K();
+  b.CH = (uint32_t)ch;
+  b.NS = ns;
+  for (int k = 0; k < s.K(); ++k) {
+    b.bytes[k] = s.N * s.sizes[k];
+    b.sblob[k] = s.blob[k];
+    b.soff[k] = s.base[k] + s.F[k];
+    b.dblob[k] = d.blob[k];
+    b.doff[k] = d.base[k] + d.F[k];
+    b.cstart[k + 1] = b.cstart[k] + ceil_div(b.bytes[k], b.CH);
+  }
+  return true;
+}
+
 bool plan_blobcopy(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
-  if (!same_layout(s, d)) { *why = "layouts differ"; return false; }
+  if (!same_layout(s, d)) return plan_segments(s, d, kn, p, why);
   if (d.has_padding()) { *why = "layout has padding (must be written as 0)"; return false; }
   p->path = LLAMA_PATH_BLOBCOPY;
   if (kn.get(LLAMA_KNOB_BLOBCOPY_LSU, 0)) {  // thread (LDG/STG) variant, for comparison
@@ -746,7 +787,10 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       // bulk blob copy) and run pairs (SoA <-> AoSoA) included
       // identities of SoA layouts with many leaves (many blobs / segments): the bulk blob copy
       // (HEP SoA MB: 6.4 TB/s vs 1.8 for 200 TMA segment ops per tile)
-      if (s.soa() && s.K() > 16 && plan_blobcopy(s, d, kn, out, &why)) return LLAMA_OK;
+      // and SoA layouts with many leaves into each other (one range per leaf:
+      // HEP100 SoA SB <-> MB 5.0 TB/s through the JIT program -> see DESIGN.md)
+      if (s.K() > 16 && (s.soa() || (single_runs(s) && single_runs(d))) && plan_blobcopy(s, d, kn, out, &why))
+        return LLAMA_OK;
       if (plan_jit_path(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_direct(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
       if (plan_permute(s, d, tile_records, kn, out, &why)) return LLAMA_OK;
