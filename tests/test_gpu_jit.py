@@ -93,6 +93,7 @@ def test_jit_padded_images(llama, oracle_mod, pad, n):
 
 
 T2D_KINDS = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, True)]
+T2D_AOSOA = [("aosoa", 8, False), ("aosoa", 4, True), ("aosoa", 32, False)]
 T2D_LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "col"), ("col", "morton"), ("morton", "row")]
 
 
@@ -115,6 +116,21 @@ def test_jit_transpose_knobs(llama, oracle_mod, knobs):
                 for lins in T2D_LINS:
                     _pair(llama, oracle_mod, schema, ext if "morton" not in lins else [64, 64], sk, lins[0], dk,
                           lins[1], seed=21, paths=("auto",), knobs=dict(knobs, jit=2))
+
+
+@pytest.mark.parametrize("knobs", [{}, {"jit_bmap": 1}, {"jit_swizzle": 1}, {"jit_pad": 0}])
+def test_jit_transpose_aosoa(llama, oracle_mod, knobs):
+    """AoSoA sides of transposing copies (block programs: a run of 4 records
+    is a piece of one block), against every other kind, both schemas."""
+    from test_gpu_lin_trace import _pair
+    for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [32, 64])):
+        for sk in T2D_KINDS + T2D_AOSOA:
+            for dk in T2D_KINDS + T2D_AOSOA:
+                if sk not in T2D_AOSOA and dk not in T2D_AOSOA:
+                    continue
+                for lins in T2D_LINS:
+                    _pair(llama, oracle_mod, schema, ext if "morton" not in lins else [64, 64], sk, lins[0], dk,
+                          lins[1], seed=23, paths=("auto",), knobs=dict(knobs, jit=2))
 
 
 def test_jit_chosen_for_wide_records(llama):
@@ -164,7 +180,8 @@ def test_jit_transpose_fuzz(llama, oracle_mod, seed):
     from test_gpu_parity import _random_schema
     rng = random.Random(5000 + seed)
     schema = _random_schema(rng)
-    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False), ("soa_sb", 1, True)]
+    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False), ("soa_sb", 1, True),
+             ("aosoa", 4, False), ("aosoa", 8, True), ("aosoa", 16, False), ("aosoa", 32, False)]
     for _ in range(6):  # (about a third of the draws are JIT-eligible: 4-byte-multiple AoS records, SoA)
         ext = rng.choice([[64, 64], [128, 64], [64, 96], [32, 32], [48, 32]])
         lins = ["row", "col"] + (["morton"] if ext[0] == ext[1] else [])

@@ -3,7 +3,7 @@ sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 import numpy as np, torch
 import paper_2106_04284_b200 as llama, workloads as W, oracle
 from test_gpu_lin_trace import _pair
-KINDS = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, True)]
+KINDS = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, True), ("aosoa", 8, False), ("aosoa", 4, True), ("aosoa", 32, False)]
 LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "col"), ("col", "morton"), ("morton", "row")]
 for schema, ext in ((W.PARTICLE7, [64, 96]), (W.LISTING1, [32, 64])):
     for sk in KINDS:
