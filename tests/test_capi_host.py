@@ -318,9 +318,10 @@ def _jit_cases():
 
 def test_jit_transpose_block_chosen():
     """Block programs are the default for transposes into SoA destinations
-    (not next to a Morton SoA side), per-record programs into AoS images."""
+    (a Morton source's runs are padded in them), per-record programs into
+    AoS images."""
     for sk, sl, dk, dl, blk in [("soa_mb", "col", "soa_mb", "row", 1), ("aos", "row", "soa_mb", "col", 1),
-                                ("aos", "row", "aos", "col", 0), ("soa_mb", "morton", "soa_mb", "row", 0)]:
+                                ("aos", "row", "aos", "col", 0), ("soa_mb", "morton", "soa_mb", "row", 1)]:
         sm = llama.Mapping.from_spec(W.PARTICLE7, [256, 256], (sk, 1, False), lin=sl)
         dm = llama.Mapping.from_spec(W.PARTICLE7, [256, 256], (dk, 1, False), lin=dl)
         assert llama.plan(sm, dm)["jit"]
