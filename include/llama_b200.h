@@ -275,6 +275,10 @@ typedef enum {
                                   per thread shrinks with it) */
   LLAMA_KNOB_JIT_ABLATE,        /* JIT kernels, ablation only: 1 = skip the move program (tile loads and stores
                                   only; the destination is NOT the copy) to measure the data movement alone (0) */
+  LLAMA_KNOB_WIDE,             /* TRANSPOSE: the wide-record transposing copy (k_transpose_wide): 0 never, 1 when
+                                  the JIT / 32 x 32 transposes do not apply (HEP100-sized records), 2 first (1) */
+  LLAMA_KNOB_WIDE_GROUP,       /* wide transpose, AoS <-> element-wise side: a thread moves 4 records along the
+                                  element-wise side's order, one vector per leaf there (1) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 
@@ -302,6 +306,7 @@ typedef struct {
   int32_t word_moves;       /* PERMUTE: > 0 if AoS <-> AoS word mode is used (words per record) */
   int32_t direct;           /* PERMUTE: 1 = direct variant (AoS side through TMA, SoA side element-wise) */
   int32_t jit;              /* PERMUTE: 1 = plan-time specialised kernel (NVRTC-compiled move program) */
+  int32_t wide;             /* TRANSPOSE: 1 = wide-record transposing copy (tile_records records per tile) */
 } llama_plan_info;
 
 llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_map,

@@ -69,14 +69,14 @@ KNOBS = ["tile_bytes", "smem_budget", "stages", "dst_bufs", "ws_order", "no_tma"
          "word_mode", "direct", "direct_stages", "direct_async", "direct_phase", "direct_staging",
          "direct_chunks", "direct_mix", "bulk_chunk", "bulk_stages", "blobcopy_lsu", "transpose_raw",
          "transpose_linear", "transpose_raw1", "transpose_fixed", "transpose_table", "transpose_raw_typed",
-         "jit", "jit_tile", "jit_stages", "jit_dst_bufs", "jit_chunks", "jit_lanes", "jit_soa_tma", "jit_pad", "jit_block", "jit_bmap", "jit_torder", "jit_dst_lsu", "jit_swizzle", "jit_group", "jit_ctas", "jit_ablate"]
+         "jit", "jit_tile", "jit_stages", "jit_dst_bufs", "jit_chunks", "jit_lanes", "jit_soa_tma", "jit_pad", "jit_block", "jit_bmap", "jit_torder", "jit_dst_lsu", "jit_swizzle", "jit_group", "jit_ctas", "jit_ablate", "wide", "wide_group"]
 
 
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int), ("tile_records", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("moves", ctypes.c_int32), ("tma", ctypes.c_int32), ("src_bytes", ctypes.c_uint64),
                 ("dst_bytes", ctypes.c_uint64), ("word_moves", ctypes.c_int32),
-                ("direct", ctypes.c_int32), ("jit", ctypes.c_int32)]
+                ("direct", ctypes.c_int32), ("jit", ctypes.c_int32), ("wide", ctypes.c_int32)]
 
 
 def _load():
@@ -394,7 +394,7 @@ def plan(src_map, dst_map, path=None, tile_records=0, knobs=None):
     return {"path": PATH_NAMES[info.path], "tile_records": info.tile_records, "smem_bytes": info.smem_bytes,
             "moves": info.moves, "tma": bool(info.tma), "src_bytes": int(info.src_bytes),
             "dst_bytes": int(info.dst_bytes), "word_moves": int(info.word_moves), "direct": bool(info.direct),
-            "jit": bool(info.jit)}
+            "jit": bool(info.jit), "wide": bool(info.wide)}
 
 
 def plan_source(src_map, dst_map, path=None, tile_records=0, knobs=None):

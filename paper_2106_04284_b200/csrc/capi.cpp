@@ -220,6 +220,12 @@ llama_status llama_plan(const llama_mapping* src_map, const llama_mapping* dst_m
       out->tma = 1;
       out->direct = 1;
     }
+    if (plan->wide) {
+      out->tile_records = (int32_t)(1u << (plan->wide->lty + plan->wide->ltx));
+      out->smem_bytes = plan->smem_bytes;
+      out->moves = (int32_t)plan->wide->mode;
+      out->wide = 1;
+    }
     return LLAMA_OK;
   } catch (...) {
     return fail(LLAMA_ERR_OOM, "planning failed");
@@ -287,6 +293,23 @@ llama_status llama_copy_ex(const llama_mapping* src_map, void* const* src_blobs,
       case LLAMA_PATH_TRANSPOSE: {
         if (plan->jit) {
           e = llb::launch_jit(*plan->jit, s, src_blobs, d, dst_blobs, plan->pdl, stream);
+          break;
+        }
+        if (plan->wide) {
+          if (plan->naive_zero_fill) {
+            llb::FillParams f = *plan->fill;
+            for (int b = 0; b < f.nb; ++b) f.ptr[b] = static_cast<uint8_t*>(dst_blobs[b]);
+            if ((e = llb::launch_fill(f, stream))) return cuda_fail(e, "fill launch");
+          }
+          llb::WideParams w = *plan->wide;
+          for (int b = 0; b < s.nblobs(); ++b) w.sb[b] = static_cast<const uint8_t*>(src_blobs[b]);
+          for (int b = 0; b < d.nblobs(); ++b) w.db[b] = static_cast<uint8_t*>(dst_blobs[b]);
+          for (uint32_t j = 0; j < w.K; ++j) {  // uniform E sides: blob + base + F per leaf
+            const int k = w.order[j];
+            w.leaf[j].sp = const_cast<uint8_t*>(w.sb[s.blob[k]]) + s.base[k] + s.F[k];
+            w.leaf[j].dp = w.db[d.blob[k]] + d.base[k] + d.F[k];
+          }
+          e = llb::launch_transpose_wide(w, stream);
           break;
         }
         if (plan->naive_zero_fill) {

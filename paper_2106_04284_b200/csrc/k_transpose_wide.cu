@@ -1,0 +1,831 @@
+// k_transpose_wide.cu -- transposing copy of wide records (SURVEY §8(f) f4:
+// rank-2 views of different storage orders; reading #26).
+//
+// The JIT transpose (jit_kernel2d.cuh) stages TY x 32-record tiles of every
+// side; a 100-leaf HEP100 record (380 / 480 B) does not fit that.  Here a tile
+// is 2^lty x 2^ltx records shaped per pair (WideParams): an AoS side ("A") is
+// staged whole-record as a shared-memory image of the tile's storage runs
+// (cp.async 16-/8-/4-byte chunks: contiguous global reads whatever the other
+// side's order), an SoA / AoSoA side ("E") is read or written element by
+// element with the warp's lanes along that side's own storage order, so every
+// global access is coalesced.  E -> E pairs transpose each leaf through a
+// shared-memory element buffer (32 x 32 elements, one pad element per 32).
+#include "device.cuh"
+#include "launch.hpp"
+
+namespace llb {
+namespace {
+
+constexpr int kWT = 256;
+
+__device__ __forceinline__ uint32_t part1by1(uint32_t x) {  // low 16 bits -> even bits
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t compact1by1(uint32_t x) {  // even bits -> low 16 bits
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  x = (x | (x >> 8)) & 0x0000FFFFu;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t spread64(uint64_t x) {  // low 32 bits -> even bits
+  x &= 0xFFFFFFFFull;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+
+// Tile-local index t along a side's storage order -> (row r, column c).
+// A Morton tile is 2^a x 2^a or 2^a x 2^(a+1) records at a multiple of its
+// size, i.e. one contiguous run of codes (reading #26: x on the even bits).
+__device__ __forceinline__ void t_rc(uint32_t lin, uint32_t t, uint32_t lty, uint32_t ltx, uint32_t& r,
+                                     uint32_t& c) {
+  if (lin == LLAMA_ROW_MAJOR) {
+    r = t >> ltx;
+    c = t & ((1u << ltx) - 1);
+  } else if (lin == LLAMA_COL_MAJOR) {
+    c = t >> lty;
+    r = t & ((1u << lty) - 1);
+  } else {
+    c = compact1by1(t);
+    r = compact1by1(t >> 1);
+  }
+}
+
+__device__ __forceinline__ uint32_t rc_t(uint32_t lin, uint32_t r, uint32_t c, uint32_t lty, uint32_t ltx) {
+  if (lin == LLAMA_ROW_MAJOR) return (r << ltx) | c;
+  if (lin == LLAMA_COL_MAJOR) return (c << lty) | r;
+  return part1by1(c) | (part1by1(r) << 1);
+}
+
+// storage position of array index (y, x)
+__device__ __forceinline__ uint64_t storage2(uint32_t lin, uint64_t y, uint64_t x, uint64_t H, uint64_t W) {
+  if (lin == LLAMA_ROW_MAJOR) return y * W + x;
+  if (lin == LLAMA_COL_MAJOR) return x * H + y;
+  return spread64(x) | (spread64(y) << 1);
+}
+
+// image offset of the record at index t along the A side's own order
+__device__ __forceinline__ uint32_t img_off(const WideSide& s, uint32_t t) {
+  return (t >> s.lrun) * s.pitch + (t & ((1u << s.lrun) - 1)) * s.S;
+}
+
+// hoisted block split of a uniform E side: off = leaf ptr + qB + rem * s_k
+__device__ __forceinline__ void esplit(const WideSide& s, uint64_t p, uint64_t& qB, uint64_t& rem) {
+  uint64_t q;
+  if (s.lshift != kNoShift) {
+    q = p >> s.lshift;
+  } else {  // round-up multiplier (Granlund-Montgomery): exact for every 64-bit p, no division call
+    const uint64_t t = __umul64hi(p, s.magic);
+    q = (t + ((p - t) >> 1)) >> (s.mshift - 1);
+  }
+  qB = q * s.B;
+  rem = p - q * s.L;
+}
+
+template <int U>
+__device__ __forceinline__ uint64_t ld_unit(const uint8_t* s) {
+  if constexpr (U == 8) return *reinterpret_cast<const uint64_t*>(s);
+  if constexpr (U == 4) return *reinterpret_cast<const uint32_t*>(s);
+  if constexpr (U == 2) return *reinterpret_cast<const uint16_t*>(s);
+  return *s;
+}
+
+template <int U>
+__device__ __forceinline__ void st_unit(uint8_t* d, uint64_t v) {
+  if constexpr (U == 8) *reinterpret_cast<uint64_t*>(d) = v;
+  if constexpr (U == 4) *reinterpret_cast<uint32_t*>(d) = (uint32_t)v;
+  if constexpr (U == 2) *reinterpret_cast<uint16_t*>(d) = (uint16_t)v;
+  if constexpr (U == 1) *d = (uint8_t)v;
+}
+
+// an SZ-byte element through accesses of U bytes (little endian)
+template <int SZ, int U>
+__device__ __forceinline__ uint64_t ld(const uint8_t* s) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int j = 0; j < SZ / U; ++j) v |= ld_unit<U>(s + j * U) << (8 * U * j);
+  return v;
+}
+
+template <int SZ, int U>
+__device__ __forceinline__ void st(uint8_t* d, uint64_t v) {
+#pragma unroll
+  for (int j = 0; j < SZ / U; ++j) st_unit<U>(d + j * U, v >> (8 * U * j));
+}
+
+// The per-record move loops issue the loads of KG leaves before their
+// stores (KG = 2 where the loads are global or shared-memory reads whose
+// latency would otherwise be exposed per element; 1 where only the stores
+// are global, which do not block).
+
+// (size, unit) -> one of the ten instantiations, f(integral_constant...) style
+template <typename F>
+__device__ __forceinline__ void dispatch(uint32_t size, uint32_t unit, F&& f) {
+  switch (size * 16 + unit) {
+    case 1 * 16 + 1: f.template run<1, 1>(); break;
+    case 2 * 16 + 2: f.template run<2, 2>(); break;
+    case 2 * 16 + 1: f.template run<2, 1>(); break;
+    case 4 * 16 + 4: f.template run<4, 4>(); break;
+    case 4 * 16 + 2: f.template run<4, 2>(); break;
+    case 4 * 16 + 1: f.template run<4, 1>(); break;
+    case 8 * 16 + 8: f.template run<8, 8>(); break;
+    case 8 * 16 + 4: f.template run<8, 4>(); break;
+    case 8 * 16 + 2: f.template run<8, 2>(); break;
+    default: f.template run<8, 1>(); break;
+  }
+}
+
+__device__ __forceinline__ void cp_async(uint8_t* s, const uint8_t* g, uint32_t n) {
+  if (n == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+  else if (n == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct Tile {
+  uint64_t y0, x0;
+  uint32_t h, w;  // valid rows / columns (ragged edge tiles)
+};
+
+// runs of an A side inside a tile: (count, records per valid run)
+__device__ __forceinline__ void runs_of(const WideSide& s, const Tile& tl, uint32_t& nruns, uint32_t& len) {
+  if (s.lin == LLAMA_ROW_MAJOR) nruns = tl.h, len = tl.w;
+  else if (s.lin == LLAMA_COL_MAJOR) nruns = tl.w, len = tl.h;
+  else nruns = 1, len = tl.h * tl.w;  // Morton tiles are always full
+}
+
+// global byte offset of run j's first record
+__device__ __forceinline__ uint64_t run_start(const WideParams& p, const WideSide& s, const Tile& tl, uint32_t j) {
+  uint32_t r, c;
+  t_rc(s.lin, j << s.lrun, p.lty, p.ltx, r, c);
+  return s.base + storage2(s.lin, tl.y0 + r, tl.x0 + c, p.H, p.W) * s.S;
+}
+
+// A source: the tile's runs -> image (cp.async; chunk-sized body, 4-byte tail)
+__device__ __forceinline__ void load_image(const WideParams& p, const WideSide& s, const Tile& tl, uint8_t* img) {
+  uint32_t nruns, len;
+  runs_of(s, tl, nruns, len);
+  const uint8_t* blob = p.sb[s.blob];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, ch = s.chunk;
+  for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+    const uint8_t* g = blob + run_start(p, s, tl, j);
+    uint8_t* d = img + j * s.pitch;
+    const uint32_t bytes = len * s.S, body = bytes / ch * ch;
+    for (uint32_t u = lane * ch; u < body; u += 32 * ch) cp_async(d + u, g + u, ch);
+    for (uint32_t u = body + lane * 4; u < bytes; u += 128) cp_async(d + u, g + u, 4);
+  }
+}
+
+template <int U>
+__device__ __forceinline__ void copy_run(uint8_t* g, const uint8_t* s, uint32_t bytes, uint32_t lane) {
+  for (uint32_t u = lane * U; u + U <= bytes; u += 32 * U) {
+    if constexpr (U == 16) *reinterpret_cast<uint4*>(g + u) = *reinterpret_cast<const uint4*>(s + u);
+    if constexpr (U == 8) *reinterpret_cast<uint2*>(g + u) = *reinterpret_cast<const uint2*>(s + u);
+    if constexpr (U == 4) *reinterpret_cast<uint32_t*>(g + u) = *reinterpret_cast<const uint32_t*>(s + u);
+  }
+}
+
+// A destination: image -> the tile's runs (vector stores; chunk-sized body, 4-byte tail)
+__device__ __forceinline__ void flush_image(const WideParams& p, const WideSide& s, const Tile& tl,
+                                            const uint8_t* img) {
+  uint32_t nruns, len;
+  runs_of(s, tl, nruns, len);
+  uint8_t* blob = p.db[s.blob];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+    uint8_t* g = blob + run_start(p, s, tl, j);
+    const uint8_t* d = img + j * s.pitch;
+    const uint32_t bytes = len * s.S, body = bytes / s.chunk * s.chunk;
+    if (s.chunk == 16) copy_run<16>(g, d, body, lane);
+    else if (s.chunk == 8) copy_run<8>(g, d, body, lane);
+    else copy_run<4>(g, d, body, lane);
+    copy_run<4>(g + body, d + body, bytes - body, lane);
+  }
+}
+
+__device__ __forceinline__ Tile tile_of(const WideParams& p, uint32_t tile) {
+  Tile tl;
+  const uint32_t ntx = (uint32_t)p.ntx, ty = tile / ntx, tx = tile - ty * ntx;  // (32-bit: no division call)
+  tl.y0 = ty << p.lty;
+  tl.x0 = tx << p.ltx;
+  const uint64_t hh = p.H - tl.y0, ww = p.W - tl.x0;
+  tl.h = (uint32_t)(hh < (1ull << p.lty) ? hh : (1ull << p.lty));
+  tl.w = (uint32_t)(ww < (1ull << p.ltx) ? ww : (1ull << p.ltx));
+  return tl;
+}
+
+// ---------------------------------------------------------------- moves
+// A -> E: thread = (record t along the destination's order, leaf lane kl);
+// a warp holds 32 consecutive destination records of one leaf: one coalesced
+// store per leaf.
+template <bool UNI>
+struct MovesAE {
+  const WideParams& p;
+  const uint8_t* src;  // src image + record offset
+  uint64_t qB, rem, pos;
+  uint32_t j0, j1, kl, nl;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    constexpr int KG = 1;
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl * KG) {
+      uint64_t v[KG];
+#pragma unroll
+      for (int g = 0; g < KG; ++g)
+        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff);
+#pragma unroll
+      for (int g = 0; g < KG; ++g) {
+        const uint32_t jj = j + g * nl;
+        if (jj >= j1) break;
+        uint8_t* d = UNI ? p.leaf[jj].dp + qB + rem * SZ : p.db[p.dl[jj].blob] + leaf_offset(pos, p.dl[jj]);
+        st<SZ, U>(d, v[g]);
+      }
+    }
+  }
+};
+
+// E -> A: thread = (record t along the source's order, leaf lane): coalesced loads
+template <bool UNI>
+struct MovesEA {
+  const WideParams& p;
+  uint8_t* dst;  // dst image + record offset
+  uint64_t qB, rem, pos;
+  uint32_t j0, j1, kl, nl;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    constexpr int KG = 2;
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl * KG) {
+      uint64_t v[KG];
+#pragma unroll
+      for (int g = 0; g < KG; ++g) {
+        const uint32_t jj = j + g * nl;
+        if (jj >= j1) break;
+        const uint8_t* s =
+            UNI ? p.leaf[jj].sp + qB + rem * SZ : p.sb[p.sl[jj].blob] + leaf_offset(pos, p.sl[jj]);
+        v[g] = ld<SZ, U>(s);
+      }
+#pragma unroll
+      for (int g = 0; g < KG; ++g)
+        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff, v[g]);
+    }
+  }
+};
+
+// A -> A with different record layouts: image -> image leaf moves
+struct MovesAA {
+  const WideParams& p;
+  const uint8_t* src;
+  uint8_t* dst;
+  uint32_t j0, j1, kl, nl;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    constexpr int KG = 2;
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl * KG) {
+      uint64_t v[KG];
+#pragma unroll
+      for (int g = 0; g < KG; ++g)
+        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff);
+#pragma unroll
+      for (int g = 0; g < KG; ++g)
+        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff, v[g]);
+    }
+  }
+};
+
+// ------------------------------------------------- 4-record groups (grp)
+// A thread moves 4 consecutive records along the E side's storage order:
+// one vector of 4 * s_k bytes on the E side (a leaf class whose group
+// addresses are all 16-byte / 4 * s_k aligned, VEC) and 4 scalar accesses to
+// the image.  4 elements of SZ bytes are packed into SZ 32-bit words.
+// 4 elements of SZ bytes packed little endian into 4 * SZ bytes (two uint4 at most);
+// the element index is a template argument, so the pack never leaves registers
+struct Pk {
+  uint4 a, b;
+};
+
+template <int I>
+struct Ix {
+  static constexpr int v = I;
+};
+
+template <typename F>
+__device__ __forceinline__ void each4(F&& f) {
+  f(Ix<0>{});
+  f(Ix<1>{});
+  f(Ix<2>{});
+  f(Ix<3>{});
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t& word(Pk& k) {
+  if constexpr (W == 0) return k.a.x;
+  if constexpr (W == 1) return k.a.y;
+  if constexpr (W == 2) return k.a.z;
+  if constexpr (W == 3) return k.a.w;
+  if constexpr (W == 4) return k.b.x;
+  if constexpr (W == 5) return k.b.y;
+  if constexpr (W == 6) return k.b.z;
+  return k.b.w;
+}
+
+template <int SZ, int I>
+__device__ __forceinline__ void pk_set(Pk& k, uint64_t v) {
+  if constexpr (SZ == 1) word<0>(k) = I == 0 ? (uint32_t)v : (word<0>(k) | ((uint32_t)v << (8 * I)));
+  if constexpr (SZ == 2) word<I / 2>(k) = (I & 1) ? (word<I / 2>(k) | ((uint32_t)v << 16)) : (uint32_t)v;
+  if constexpr (SZ == 4) word<I>(k) = (uint32_t)v;
+  if constexpr (SZ == 8) word<2 * I>(k) = (uint32_t)v, word<2 * I + 1>(k) = (uint32_t)(v >> 32);
+}
+
+template <int SZ, int I>
+__device__ __forceinline__ uint64_t pk_get(Pk& k) {
+  if constexpr (SZ == 1) return (word<0>(k) >> (8 * I)) & 0xFFu;
+  if constexpr (SZ == 2) return (word<I / 2>(k) >> (16 * (I & 1))) & 0xFFFFu;
+  if constexpr (SZ == 4) return word<I>(k);
+  return (uint64_t)word<2 * I>(k) | ((uint64_t)word<2 * I + 1>(k) << 32);
+}
+
+template <int SZ>
+__device__ __forceinline__ void vst(uint8_t* d, const Pk& k) {
+  if constexpr (SZ == 1) *reinterpret_cast<uint32_t*>(d) = k.a.x;
+  if constexpr (SZ == 2) *reinterpret_cast<uint2*>(d) = make_uint2(k.a.x, k.a.y);
+  if constexpr (SZ == 4) *reinterpret_cast<uint4*>(d) = k.a;
+  if constexpr (SZ == 8) reinterpret_cast<uint4*>(d)[0] = k.a, reinterpret_cast<uint4*>(d)[1] = k.b;
+}
+
+template <int SZ>
+__device__ __forceinline__ void vld(const uint8_t* s, Pk& k) {
+  if constexpr (SZ == 1) k.a.x = *reinterpret_cast<const uint32_t*>(s);
+  if constexpr (SZ == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(s);
+    k.a.x = v.x, k.a.y = v.y;
+  }
+  if constexpr (SZ == 4) k.a = *reinterpret_cast<const uint4*>(s);
+  if constexpr (SZ == 8) k.a = reinterpret_cast<const uint4*>(s)[0], k.b = reinterpret_cast<const uint4*>(s)[1];
+}
+
+template <typename F>
+__device__ __forceinline__ void dispatch_vec(uint32_t size, uint32_t unit, bool vec, F&& f) {
+  switch (size * 32 + unit * 2 + (vec ? 1 : 0)) {
+    case 1 * 32 + 1 * 2 + 1: f.template run<1, 1, true>(); break;
+    case 1 * 32 + 1 * 2: f.template run<1, 1, false>(); break;
+    case 2 * 32 + 2 * 2 + 1: f.template run<2, 2, true>(); break;
+    case 2 * 32 + 2 * 2: f.template run<2, 2, false>(); break;
+    case 2 * 32 + 1 * 2 + 1: f.template run<2, 1, true>(); break;
+    case 2 * 32 + 1 * 2: f.template run<2, 1, false>(); break;
+    case 4 * 32 + 4 * 2 + 1: f.template run<4, 4, true>(); break;
+    case 4 * 32 + 4 * 2: f.template run<4, 4, false>(); break;
+    case 4 * 32 + 2 * 2 + 1: f.template run<4, 2, true>(); break;
+    case 4 * 32 + 2 * 2: f.template run<4, 2, false>(); break;
+    case 4 * 32 + 1 * 2 + 1: f.template run<4, 1, true>(); break;
+    case 4 * 32 + 1 * 2: f.template run<4, 1, false>(); break;
+    case 8 * 32 + 8 * 2 + 1: f.template run<8, 8, true>(); break;
+    case 8 * 32 + 8 * 2: f.template run<8, 8, false>(); break;
+    case 8 * 32 + 4 * 2 + 1: f.template run<8, 4, true>(); break;
+    case 8 * 32 + 4 * 2: f.template run<8, 4, false>(); break;
+    case 8 * 32 + 2 * 2 + 1: f.template run<8, 2, true>(); break;
+    case 8 * 32 + 2 * 2: f.template run<8, 2, false>(); break;
+    case 8 * 32 + 1 * 2 + 1: f.template run<8, 1, true>(); break;
+    default: f.template run<8, 1, false>(); break;
+  }
+}
+
+// A -> E: image scalars -> one E vector per leaf (nv = valid records of the group)
+struct GroupAE {
+  const WideParams& p;
+  const uint8_t* img;
+  uint32_t ro0, ro1, ro2, ro3;
+  uint64_t qB, rem;
+  uint32_t nv, j0, j1, kl, nl;
+  template <int SZ, int U, bool VEC>
+  __device__ __forceinline__ void run() {
+    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl) {
+      const uint32_t so = p.leaf[j].soff;
+      Pk k{};
+      each4([&](auto I) {
+        if (I.v < (int)nv) pk_set<SZ, I.v>(k, ld<SZ, U>(img + ro[I.v] + so));
+      });
+      uint8_t* d = p.leaf[j].dp + qB + rem * SZ;
+      if (VEC && nv == 4) {
+        vst<SZ>(d, k);
+      } else {
+        each4([&](auto I) {
+          if (I.v < (int)nv) st<SZ, U>(d + I.v * SZ, pk_get<SZ, I.v>(k));
+        });
+      }
+    }
+  }
+};
+
+// E -> A: one E vector per leaf -> image scalars (two leaves' loads in flight)
+struct GroupEA {
+  const WideParams& p;
+  uint8_t* img;
+  uint32_t ro0, ro1, ro2, ro3;
+  uint64_t qB, rem;
+  uint32_t nv, j0, j1, kl, nl;
+  template <int SZ, int U, bool VEC>
+  __device__ __forceinline__ void ld_group(uint32_t j, Pk& k) {
+    const uint8_t* s = p.leaf[j].sp + qB + rem * SZ;
+    if (VEC && nv == 4) {
+      vld<SZ>(s, k);
+    } else {
+      each4([&](auto I) {
+        if (I.v < (int)nv) pk_set<SZ, I.v>(k, ld<SZ, U>(s + I.v * SZ));
+      });
+    }
+  }
+  template <int SZ, int U>
+  __device__ __forceinline__ void st_group(uint32_t j, Pk& k, const uint32_t* ro) {
+    const uint32_t doff = p.leaf[j].doff;
+    each4([&](auto I) {
+      if (I.v < (int)nv) st<SZ, U>(img + ro[I.v] + doff, pk_get<SZ, I.v>(k));
+    });
+  }
+  template <int SZ, int U, bool VEC>
+  __device__ __forceinline__ void run() {
+    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += 2 * nl) {
+      Pk k0{}, k1{};
+      const bool two = j + nl < j1;
+      ld_group<SZ, U, VEC>(j, k0);
+      if (two) ld_group<SZ, U, VEC>(j + nl, k1);
+      st_group<SZ, U>(j, k0, ro);
+      if (two) st_group<SZ, U>(j + nl, k1, ro);
+    }
+  }
+};
+
+// E -> E in 4-element groups (grp): the leaf's 32 x 32 tile sits in a
+// shared-memory buffer in source order, 16-byte chunks of a 32-element run
+// XOR-swizzled by (run / 4) % 8 (conflict-free transposed reads for 4-byte
+// elements); a group is one cp.async of 4 * s_k bytes in, and 4 shared reads
+// + one vector store out.
+__device__ __forceinline__ uint32_t ee_off(uint32_t t) {  // element index of source-order t in the buffer
+  const uint32_t run = t >> 5, q = (t >> 2) & 7;
+  return (run << 5) + ((q ^ ((run >> 2) & 7)) << 2) + (t & 3);
+}
+
+struct LoadEEg {
+  const WideParams& p;
+  uint8_t* buf;
+  uint64_t qB, rem;
+  uint32_t off0, nv, j;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    const WideLeaf& l = p.leaf[j];
+    const uint8_t* s = l.sp + qB + rem * SZ;
+    uint8_t* d = buf + l.buf + off0 * SZ;
+    if (nv == 4 && (l.vec & 1)) {
+      if constexpr (SZ == 8) {
+        cp_async(d, s, 16);
+        cp_async(d + 16, s + 16, 16);
+      } else {
+        cp_async(d, s, 4 * SZ);
+      }
+    } else {
+      each4([&](auto I) {
+        if (I.v < (int)nv) st<SZ, SZ>(d + I.v * SZ, ld<SZ, U>(s + I.v * SZ));
+      });
+    }
+  }
+};
+
+struct StoreEEg {
+  const WideParams& p;
+  const uint8_t* buf;
+  uint64_t qB, rem;
+  uint32_t o0, o1, o2, o3, nv, j;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    const WideLeaf& l = p.leaf[j];
+    const uint8_t* b = buf + l.buf;
+    const uint32_t o[4] = {o0, o1, o2, o3};
+    Pk k{};
+    each4([&](auto I) {
+      if (I.v < (int)nv) pk_set<SZ, I.v>(k, ld<SZ, SZ>(b + o[I.v] * SZ));
+    });
+    uint8_t* d = l.dp + qB + rem * SZ;
+    if (nv == 4 && (l.vec & 2)) {
+      vst<SZ>(d, k);
+    } else {
+      each4([&](auto I) {
+        if (I.v < (int)nv) st<SZ, U>(d + I.v * SZ, pk_get<SZ, I.v>(k));
+      });
+    }
+  }
+};
+
+// E -> E, one leaf of a batch: 4 records per thread (1024-record tiles)
+template <bool UNI>
+struct LoadEE {
+  const WideParams& p;
+  uint8_t* buf;
+  const uint64_t* qB;
+  const uint64_t* rem;
+  const uint64_t* pos;
+  const uint32_t* idx;
+  uint32_t valid, j;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    const WideLeaf& l = p.leaf[j];
+    uint64_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (valid >> i & 1) {
+        const uint8_t* s = UNI ? l.sp + qB[i] + rem[i] * SZ : p.sb[p.sl[j].blob] + leaf_offset(pos[i], p.sl[j]);
+        v[i] = ld<SZ, U>(s);
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (valid >> i & 1) st<SZ, SZ>(buf + l.buf + idx[i] * SZ, v[i]);
+  }
+};
+
+template <bool UNI>
+struct StoreEE {
+  const WideParams& p;
+  const uint8_t* buf;
+  const uint64_t* qB;
+  const uint64_t* rem;
+  const uint64_t* pos;
+  const uint32_t* idx;
+  uint32_t valid, j;
+  template <int SZ, int U>
+  __device__ __forceinline__ void run() {
+    const WideLeaf& l = p.leaf[j];
+    uint64_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (valid >> i & 1) v[i] = ld<SZ, SZ>(buf + l.buf + idx[i] * SZ);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (valid >> i & 1) {
+        uint8_t* d = UNI ? l.dp + qB[i] + rem[i] * SZ : p.db[p.dl[j].blob] + leaf_offset(pos[i], p.dl[j]);
+        st<SZ, U>(d, v[i]);
+      }
+  }
+};
+
+template <int MODE, bool UNI, bool GRP, int MINB>
+__global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_constant__ WideParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const WideSide& S0 = p.side[0];
+  const WideSide& S1 = p.side[1];
+  const uint32_t tid = threadIdx.x, lt = p.lty + p.ltx, n = 1u << lt;
+  if ((MODE == 1 || MODE == 2) && p.dzero) {  // padding bytes of the destination image stay 0
+    for (uint32_t u = tid * 16; u < S1.img_bytes; u += kWT * 16)
+      *reinterpret_cast<uint4*>(smem + S1.img + u) = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
+  // thread -> (record t, leaf lane kl of nl) for tiles of <= 256 records
+  const uint32_t nl = n >= kWT ? 1 : kWT >> lt, kl = n >= kWT ? 0 : tid >> lt, t0 = tid & (n - 1);
+  for (uint32_t item = blockIdx.x; item < (uint32_t)p.n_items; item += gridDim.x) {
+    if constexpr (MODE == 4 && GRP) {
+      const uint32_t tile = item / p.nbatch;
+      const uint32_t b = item - tile * p.nbatch;
+      const Tile tl = tile_of(p, tile);
+      uint8_t* buf = smem + p.buf;
+      const uint32_t t0 = 4 * tid;  // this thread's group: source order (load), destination order (store)
+      uint32_t nv = 0, r0 = 0, c0 = 0;
+      each4([&](auto I) {
+        uint32_t r, c;
+        t_rc(S0.lin, t0 + I.v, p.lty, p.ltx, r, c);
+        if (I.v == 0) r0 = r, c0 = c;
+        if (r < tl.h && c < tl.w && nv == (uint32_t)I.v) ++nv;
+      });
+      uint64_t qB = 0, rem = 0;
+      if (nv) esplit(S0, storage2(S0.lin, tl.y0 + r0, tl.x0 + c0, p.H, p.W), qB, rem);
+      if (nv) {
+#pragma unroll 1
+        for (uint32_t j = p.bstart[b]; j < p.bstart[b + 1]; ++j)
+          dispatch(p.leaf[j].size, p.leaf[j].unit, LoadEEg{p, buf, qB, rem, ee_off(t0), nv, j});
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      uint32_t o[4];
+      nv = 0;
+      each4([&](auto I) {
+        uint32_t r, c;
+        t_rc(S1.lin, t0 + I.v, p.lty, p.ltx, r, c);
+        if (I.v == 0) r0 = r, c0 = c;
+        o[I.v] = ee_off(rc_t(S0.lin, r, c, p.lty, p.ltx));
+        if (r < tl.h && c < tl.w && nv == (uint32_t)I.v) ++nv;
+      });
+      if (nv) {
+        esplit(S1, storage2(S1.lin, tl.y0 + r0, tl.x0 + c0, p.H, p.W), qB, rem);
+#pragma unroll 1
+        for (uint32_t j = p.bstart[b]; j < p.bstart[b + 1]; ++j)
+          dispatch(p.leaf[j].size, p.leaf[j].unit, StoreEEg{p, buf, qB, rem, o[0], o[1], o[2], o[3], nv, j});
+      }
+      __syncthreads();
+    } else if constexpr (MODE == 4) {
+      const uint32_t tile = item / p.nbatch;
+      const uint32_t b = item - tile * p.nbatch;
+      const Tile tl = tile_of(p, tile);
+      uint8_t* buf = smem + p.buf;
+      uint64_t qB[4], rem[4], pos[4];
+      uint32_t idx[4], valid = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // source order
+        uint32_t r, c;
+        const uint32_t t = tid + i * kWT;
+        t_rc(S0.lin, t, p.lty, p.ltx, r, c);
+        qB[i] = rem[i] = 0;
+        idx[i] = t + (t >> 5);
+        pos[i] = 0;
+        if (r < tl.h && c < tl.w) {
+          valid |= 1u << i;
+          pos[i] = storage2(S0.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
+          if (UNI) esplit(S0, pos[i], qB[i], rem[i]);
+        }
+      }
+#pragma unroll 1
+      for (uint32_t j = p.bstart[b]; j < p.bstart[b + 1]; ++j)
+        dispatch(p.leaf[j].size, p.leaf[j].unit, LoadEE<UNI>{p, buf, qB, rem, pos, idx, valid, j});
+      __syncthreads();
+      valid = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // destination order
+        uint32_t r, c;
+        const uint32_t t = tid + i * kWT;
+        t_rc(S1.lin, t, p.lty, p.ltx, r, c);
+        const uint32_t ts = rc_t(S0.lin, r, c, p.lty, p.ltx);
+        idx[i] = ts + (ts >> 5);
+        qB[i] = rem[i] = 0;
+        pos[i] = 0;
+        if (r < tl.h && c < tl.w) {
+          valid |= 1u << i;
+          pos[i] = storage2(S1.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
+          if (UNI) esplit(S1, pos[i], qB[i], rem[i]);
+        }
+      }
+#pragma unroll 1
+      for (uint32_t j = p.bstart[b]; j < p.bstart[b + 1]; ++j)
+        dispatch(p.leaf[j].size, p.leaf[j].unit, StoreEE<UNI>{p, buf, qB, rem, pos, idx, valid, j});
+      __syncthreads();
+    } else {
+      const Tile tl = tile_of(p, item);
+      if constexpr (MODE == 0 || MODE == 2 || MODE == 3) {
+        load_image(p, S0, tl, smem + S0.img);
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      if constexpr (MODE == 3) {  // same record layout: flush the destination runs from the source image
+        uint32_t nruns, len;
+        runs_of(S1, tl, nruns, len);
+        const uint32_t warp = tid >> 5, lane = tid & 31, u = p.u3;
+        for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+          uint8_t* g = p.db[S1.blob] + run_start(p, S1, tl, j);
+          for (uint32_t q = 0; q < len; ++q) {
+            uint32_t r, c;
+            t_rc(S1.lin, (j << S1.lrun) + q, p.lty, p.ltx, r, c);
+            const uint8_t* s = smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx));
+            uint8_t* d = g + (uint64_t)q * S1.S;
+            if (u == 16) copy_run<16>(d, s, S1.S, lane);
+            else if (u == 8) copy_run<8>(d, s, S1.S, lane);
+            else copy_run<4>(d, s, S1.S, lane);
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      if constexpr (GRP) {
+        {  // 4-record groups along the E side's order
+          const WideSide& E = MODE == 0 ? S1 : S0;
+          const WideSide& A = MODE == 0 ? S0 : S1;
+          const uint32_t ng = n >> 2, gl = ng >= kWT ? 1 : kWT / ng;
+          for (uint32_t gi = tid % ng; gi < ng; gi += kWT) {
+            uint32_t ro[4], nv = 0, r0 = 0, c0 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t r, c;
+              t_rc(E.lin, 4 * gi + i, p.lty, p.ltx, r, c);
+              if (i == 0) r0 = r, c0 = c;
+              ro[i] = img_off(A, rc_t(A.lin, r, c, p.lty, p.ltx));
+              if (r < tl.h && c < tl.w && nv == (uint32_t)i) ++nv;
+            }
+            if (!nv) continue;
+            uint64_t qB, rem;
+            esplit(E, storage2(E.lin, tl.y0 + r0, tl.x0 + c0, p.H, p.W), qB, rem);
+            const uint32_t kl2 = tid / ng < gl ? tid / ng : 0;
+#pragma unroll 1
+            for (uint32_t q = 0; q < p.n_cls; ++q) {
+              const WideClass& cl = p.cls[q];
+              if constexpr (MODE == 0) {
+                GroupAE m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], qB, rem, nv, cl.j0, cl.j1, kl2, gl};
+                dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
+              } else {
+                GroupEA m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], qB, rem, nv, cl.j0, cl.j1, kl2, gl};
+                dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
+              }
+            }
+          }
+          __syncthreads();
+          if constexpr (MODE == 1) {
+            flush_image(p, S1, tl, smem + S1.img);
+            __syncthreads();
+          }
+          continue;
+        }
+      }
+      if constexpr (!GRP) for (uint32_t t = t0; t < n; t += kWT) {
+        uint32_t r, c;
+        const uint32_t ord = MODE == 1 ? S0.lin : S1.lin;  // lanes along the E side (A -> A: the destination)
+        t_rc(ord, t, p.lty, p.ltx, r, c);
+        if (r >= tl.h || c >= tl.w) continue;
+        if constexpr (MODE == 0) {
+          MovesAE<UNI> m{p, smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx)), 0, 0, 0, 0, 0, kl, nl};
+          m.pos = storage2(S1.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
+          if (UNI) esplit(S1, m.pos, m.qB, m.rem);
+#pragma unroll 1
+          for (uint32_t q = 0; q < p.n_cls; ++q) {
+            m.j0 = p.cls[q].j0;
+            m.j1 = p.cls[q].j1;
+            dispatch(p.cls[q].size, p.cls[q].unit & 0xFF, m);
+          }
+        } else if constexpr (MODE == 1) {
+          MovesEA<UNI> m{p, smem + S1.img + img_off(S1, rc_t(S1.lin, r, c, p.lty, p.ltx)), 0, 0, 0, 0, 0, kl, nl};
+          m.pos = storage2(S0.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
+          if (UNI) esplit(S0, m.pos, m.qB, m.rem);
+#pragma unroll 1
+          for (uint32_t q = 0; q < p.n_cls; ++q) {
+            m.j0 = p.cls[q].j0;
+            m.j1 = p.cls[q].j1;
+            dispatch(p.cls[q].size, p.cls[q].unit & 0xFF, m);
+          }
+        } else {
+          MovesAA m{p, smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx)),
+                    smem + S1.img + img_off(S1, t), 0, 0, kl, nl};
+#pragma unroll 1
+          for (uint32_t q = 0; q < p.n_cls; ++q) {
+            m.j0 = p.cls[q].j0;
+            m.j1 = p.cls[q].j1;
+            dispatch(p.cls[q].size, p.cls[q].unit & 0xFF, m);
+          }
+        }
+      }
+      __syncthreads();
+      if constexpr (MODE == 1 || MODE == 2) {
+        flush_image(p, S1, tl, smem + S1.img);
+        __syncthreads();
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int launch_transpose_wide(const WideParams& p, void* stream) {
+  if (p.n_items == 0) return 0;
+  static LaunchCache cache[13][64];
+  // index: mode + 5 * (every E side uniform: block split hoisted, no per-leaf
+  // division); 10 / 11 / 12: modes 0 / 1 / 4 in 4-record groups.  Minimum CTAs per SM
+  // from the shared memory a HEP100 tile takes (48-61 KB: 3-4), so the
+  // register budget never costs occupancy.
+  void (*const kerns[13])(WideParams) = {
+      k_transpose_wide<0, false, false, 3>, k_transpose_wide<1, false, false, 3>,
+      k_transpose_wide<2, false, false, 3>, k_transpose_wide<3, false, false, 4>,
+      k_transpose_wide<4, false, false, 2>, k_transpose_wide<0, true, false, 3>,
+      k_transpose_wide<1, true, false, 3>,  k_transpose_wide<2, true, false, 3>,
+      k_transpose_wide<3, true, false, 4>,  k_transpose_wide<4, true, false, 2>,
+      k_transpose_wide<0, true, true, 4>,   k_transpose_wide<1, true, true, 4>,
+      k_transpose_wide<4, true, true, 4>};
+  if (p.mode > 4) return (int)cudaErrorInvalidValue;
+  const bool uni = (p.side[0].A || p.side[0].uni) && (p.side[1].A || p.side[1].uni);
+  const int v = p.grp && uni && (p.mode <= 1 || p.mode == 4) ? (p.mode == 4 ? 12 : 10 + (int)p.mode)
+                                                               : (int)p.mode + (uni ? 5 : 0);
+  int dev = 0, per_sm = 1, sms = 148;
+  cudaGetDevice(&dev);
+  auto kern = kerns[v];
+  int e = prepare_kernel(kern, kWT, (int)p.smem, &cache[v][dev & 63], &per_sm);
+  if (e) return e;
+  current_device_sms(&sms);
+  uint64_t grid = (uint64_t)sms * per_sm;
+  if (grid > p.n_items) grid = p.n_items;
+  kern<<<(unsigned)grid, kWT, p.smem, (cudaStream_t)stream>>>(p);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+}  // namespace llb

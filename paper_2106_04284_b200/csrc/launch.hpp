@@ -17,6 +17,7 @@ int launch_permute(const PermParams& p, int smem_bytes, bool v1, bool pdl, void*
 int launch_permute_v1(const PermParams& p, int smem_bytes, void* stream);
 int launch_permute_ws(const PermParams& p, int smem_bytes, bool pdl, void* stream);
 int launch_permute_direct(const DirectParams& p, void* stream);
+int launch_transpose_wide(const WideParams& p, void* stream);
 
 int launch_move_generic(const MoveParams& p, void* stream);
 int launch_move_runs(const MoveParams& p, void* stream);

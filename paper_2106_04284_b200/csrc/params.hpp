@@ -309,6 +309,75 @@ struct DirectParams {
 };
 static_assert(sizeof(DirectParams) <= 32764, "DirectParams exceeds the kernel parameter limit");
 
+// ------------------------------------------------- wide transposing copy
+// Rank-2 views of different storage orders whose records are too
+// wide for the JIT transpose's TY x 32-record tiles (HEP100: 380 / 480 B).
+// A tile is 2^lty x 2^ltx records; each side is either an "A" side (plain
+// AoS, record stride S % 4 == 0) staged as a shared-memory image of the
+// tile's storage runs (row: 2^ltx records, column: 2^lty, Morton: the whole
+// tile, which is Morton-contiguous), or an "E" side (SoA / AoSoA) accessed
+// element by element with the warp's lanes along that side's storage order.
+struct WideSide {
+  uint32_t A;       // 1: AoS image side
+  uint32_t lin;     // llama_linearizer
+  uint32_t S;       // A: record stride
+  uint32_t blob;    // A: the blob
+  uint64_t base;    // A: byte offset of record 0
+  uint32_t chunk;   // A: bytes per cp.async / vector access of a run (16, 8 or 4)
+  uint32_t pitch;   // A: image bytes per run (a multiple of chunk)
+  uint32_t lrun;    // A: log2 records per run
+  uint32_t img;     // A: shared-memory offset of the image
+  uint32_t img_bytes;
+  uint32_t uni;     // E: every leaf shares L / B below (the block split is hoisted out of the leaf loop)
+  uint64_t L, B;    // E, uni: lanes per block, block stride
+  uint32_t lshift;  // E, uni: log2(L) or kNoShift
+  uint32_t mshift;  // E, uni, L not a power of two: ceil(log2 L); q = (t + ((p - t) >> 1)) >> (mshift - 1),
+  uint64_t magic;   //   t = umulhi(p, magic), magic = floor(2^64 (2^mshift - L) / L) + 1
+};
+
+// Leaf j of the class order (positions, not leaf ids: the kernel walks them in order).
+struct WideLeaf {
+  uint8_t* sp;          // E source (uniform): blob + base + F (patched per launch)
+  uint8_t* dp;          // E destination (uniform)
+  uint32_t soff, doff;  // A sides: leaf offset inside a record
+  uint16_t size, unit;  // unit: widest access valid at every address on both sides (1, 2, 4, 8)
+  uint32_t buf;         // E -> E: offset of the leaf's element buffer inside the batch area
+  uint32_t vec;         // E -> E, grp: bit 0 / 1 = every 4-element group of the source / destination
+                        // is one 4 * s_k-byte range aligned to min(16, 4 * s_k)
+};
+
+struct WideClass {      // positions [j0, j1) share size, unit and (grp) the E-side vector flag
+  uint16_t j0, j1;
+  uint16_t size, unit;  // unit | 256: every 4-record group of the E side is one aligned vector
+};
+
+struct WideParams {
+  uint64_t H, W;
+  uint64_t ntx;         // tiles along x
+  uint64_t n_items;     // tiles (x nbatch for E -> E)
+  uint32_t lty, ltx;    // log2 tile rows / columns
+  uint32_t mode;        // 0 A -> E, 1 E -> A, 2 A -> A (leaf moves), 3 A -> A (same record layout), 4 E -> E
+  uint32_t K;
+  uint32_t nbatch;      // E -> E: leaf batches per tile
+  uint32_t dzero;       // the destination image has padding bytes: zeroed once per CTA
+  uint32_t smem;        // dynamic shared memory per CTA
+  uint32_t buf;         // E -> E: shared-memory offset of the batch area
+  uint32_t n_cls;
+  uint32_t u3;          // mode 3: bytes per access of a record copy (16, 8, 4)
+  uint32_t grp;         // modes 0 / 1: threads move 4-record groups along the E side's order
+  uint32_t pad2_;
+  uint16_t bstart[kMaxLeaves + 1];   // E -> E: batch b = positions [bstart[b], bstart[b+1])
+  uint16_t order[kMaxLeaves];        // leaf id at each position
+  WideClass cls[16];
+  WideSide side[2];
+  WideLeaf leaf[kMaxLeaves];
+  DevLeaf sl[kMaxLeaves];            // by position: E sides that are not uniform
+  DevLeaf dl[kMaxLeaves];
+  const uint8_t* sb[kMaxBlobs];
+  uint8_t* db[kMaxBlobs];
+};
+static_assert(sizeof(WideParams) <= 32764, "WideParams exceeds the kernel parameter limit");
+
 // kernel parameter blocks travel as __grid_constant__ arguments (<= 32764 B)
 static_assert(sizeof(PermParams) <= 32764, "PermParams exceeds the kernel parameter limit");
 static_assert(sizeof(NaiveParams) <= 32764, "NaiveParams exceeds the kernel parameter limit");

@@ -171,6 +171,235 @@ bool plan_transpose(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p
   return true;
 }
 
+// ------------------------------------------------ wide transposing copy (f4)
+// Rank-2 views of different storage orders with records too wide for the JIT
+// transpose's TY x 32 tiles (k_transpose_wide.cu).  A side is "A" (plain AoS:
+// one part, L = 1, stride S % 4 == 0) or "E" (anything else, element-wise).
+namespace {
+
+bool wide_a_side(const Mapping& m) {
+  return m.uniform && m.parts.size() == 1 && (m.kind == LLAMA_AOS || m.kind == LLAMA_AOSOA) && m.L == 1 &&
+         m.B > 0 && m.B % 4 == 0 && m.B <= 4096;
+}
+
+// alignment (power of two <= 16) of every element address of leaf k on an E side
+uint32_t wide_e_align(const Mapping& m, int k) {
+  uint64_t a = gcd64(16, m.base[k] + m.F[k]);
+  a = gcd64(a, m.sizes[k]);
+  if (m.Lk[k] < m.N) a = gcd64(a, m.Bk[k]);
+  return (uint32_t)a;
+}
+
+// largest chunk (16, 8, 4) dividing every run start and full-run length of
+// an A side whose runs hold 2^lrun records
+uint32_t wide_chunk(const Mapping& m, uint32_t lrun) {
+  const uint64_t S = m.B, H = (uint64_t)m.extents[0], W = (uint64_t)m.extents[1];
+  for (uint32_t c : {16u, 8u, 4u}) {
+    bool ok = m.base[0] % c == 0 && ((S << lrun) % c == 0);
+    if (m.lin == LLAMA_ROW_MAJOR) ok = ok && (W * S) % c == 0;
+    if (m.lin == LLAMA_COL_MAJOR) ok = ok && (H * S) % c == 0;
+    if (ok) return c;
+  }
+  return 4;
+}
+
+// image pitch: the run bytes rounded up to the chunk, then the candidate
+// (within 8 chunks) that spreads 32 consecutive runs over the most banks
+uint32_t wide_pitch(uint64_t run_bytes, uint32_t chunk, uint32_t nruns) {
+  const uint64_t p0 = (run_bytes + chunk - 1) / chunk * chunk;
+  if (nruns <= 1) return (uint32_t)p0;
+  uint64_t best = p0;
+  int best_banks = -1;
+  for (uint64_t p = p0; p < p0 + 8 * chunk; p += chunk) {
+    uint32_t mask = 0;
+    for (uint32_t j = 0; j < std::min<uint32_t>(nruns, 32); ++j) mask |= 1u << ((j * p / 4) % 32);
+    const int banks = __builtin_popcount(mask);
+    if (banks > best_banks) best_banks = banks, best = p;
+  }
+  return (uint32_t)best;
+}
+
+uint32_t ilog2(uint64_t x) {
+  uint32_t r = 0;
+  while ((1ull << (r + 1)) <= x) ++r;
+  return r;
+}
+
+}  // namespace
+
+static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
+  if (s.trace || d.trace) { *why = "traced views count through the naive kernel"; return false; }
+  if (s.lin == d.lin) { *why = "equal linearisations"; return false; }
+  if (s.extents.size() != 2) { *why = "the wide transposing copy is for 2-d views"; return false; }
+  if (!kn.get(LLAMA_KNOB_WIDE, 1)) { *why = "knob wide = 0"; return false; }
+  const bool sA = wide_a_side(s), dA = wide_a_side(d);
+  const uint64_t H = (uint64_t)s.extents[0], W = (uint64_t)s.extents[1];
+  const bool morton = s.lin == LLAMA_MORTON || d.lin == LLAMA_MORTON;
+  uint32_t lty = 5, ltx = 5;  // E -> E: 32 x 32
+  if (sA || dA) {
+    // 128 records per tile while the images stay <= 64 KB (HEP100 aligned: 61 KB)
+    bool same = sA && dA && s.B == d.B && !d.has_padding();
+    for (int k = 0; k < s.K() && same; ++k) same = s.F[k] == d.F[k];
+    const uint64_t S = (sA ? s.B : 0) + (dA && !same ? d.B : 0);
+    uint32_t lt = 7;
+    while (lt > 5 && (S << lt) > 64 * 1024) --lt;
+    // the E side's storage runs span the tile: 32 records along a row /
+    // column side; a Morton tile is 2^a x 2^a or 2^a x 2^(a+1) (contiguous codes)
+    const Mapping* e = !sA ? &s : !dA ? &d : nullptr;
+    if (morton || !e) lty = lt / 2, ltx = lt - lt / 2;
+    else if (e->lin == LLAMA_ROW_MAJOR) ltx = 5, lty = lt - 5;
+    else lty = 5, ltx = lt - 5;
+  }
+  if (morton) {  // extents equal powers of two: clip the tile (stays square or 1 x 2)
+    const uint32_t b = ilog2(H);
+    lty = std::min(lty, b);
+    ltx = std::min(ltx, b);
+  }
+  const uint32_t lt = lty + ltx, n = 1u << lt;
+  p->wide.reset(new WideParams);
+  WideParams& w = *p->wide;
+  std::memset(&w, 0, sizeof(w));
+  w.H = H;
+  w.W = W;
+  w.lty = lty;
+  w.ltx = ltx;
+  w.K = (uint32_t)s.K();
+  w.ntx = ceil_div(W, 1ull << ltx);
+  const uint64_t n_tiles = ceil_div(H, 1ull << lty) * w.ntx;
+  if (sA && dA) {
+    bool same = s.B == d.B && !d.has_padding();
+    for (int k = 0; k < s.K() && same; ++k) same = s.F[k] == d.F[k];
+    w.mode = same ? 3 : 2;
+  } else {
+    w.mode = sA ? 0 : dA ? 1 : 4;
+  }
+  uint64_t smem = 0;
+  for (int X = 0; X < 2; ++X) {
+    const Mapping& m = X == 0 ? s : d;
+    WideSide& sd = w.side[X];
+    sd.lin = (uint32_t)m.lin;
+    sd.A = (X == 0 ? sA : dA) ? 1 : 0;
+    if (sd.A) {
+      const bool image = !(X == 1 && sA && w.mode == 3);  // mode 3 flushes from the source image
+      sd.S = (uint32_t)m.B;
+      sd.blob = m.blob[0];
+      sd.base = m.base[0];
+      sd.lrun = m.lin == LLAMA_ROW_MAJOR ? ltx : m.lin == LLAMA_COL_MAJOR ? lty : lt;
+      sd.chunk = wide_chunk(m, sd.lrun);
+      const uint32_t nruns = 1u << (lt - sd.lrun);
+      sd.pitch = wide_pitch((uint64_t)sd.S << sd.lrun, sd.chunk, nruns);
+      if (image) {
+        sd.img = (uint32_t)smem;
+        sd.img_bytes = (uint32_t)align16((uint64_t)nruns * sd.pitch);
+        smem += sd.img_bytes;
+      }
+    } else {
+      sd.uni = m.uniform ? 1 : 0;
+      sd.L = m.L;
+      sd.B = m.B;
+      sd.lshift = m.L >= m.N ? 63u : (m.L & (m.L - 1)) == 0 ? ilog2(m.L) : kNoShift;
+      if (sd.lshift == kNoShift) {  // division by L through a multiplier (k_transpose_wide.cu esplit)
+        sd.mshift = ilog2(m.L) + 1;  // ceil(log2 L), L not a power of two
+        const unsigned __int128 two64 = (unsigned __int128)1 << 64;
+        sd.magic = (uint64_t)(two64 * (((unsigned __int128)1 << sd.mshift) - m.L) / m.L) + 1;
+      }
+    }
+  }
+  w.dzero = (dA && d.has_padding()) ? 1 : 0;
+  // 4-record groups along the E side (modes 0 / 1, knob wide_group): the
+  // group of 4 consecutive storage positions starts at a multiple of 4 and
+  // lies in one block, so leaf k's 4 elements are one 4 * s_k-byte range
+  auto group_ok = [&](const Mapping& e) {
+    bool ok = e.uniform && (e.L >= e.N || e.L % 4 == 0) && lt >= 2;
+    if (e.lin == LLAMA_ROW_MAJOR) ok = ok && ltx >= 2 && W % 4 == 0;
+    if (e.lin == LLAMA_COL_MAJOR) ok = ok && lty >= 2 && H % 4 == 0;
+    return ok;
+  };
+  // group vectors: leaf k's 4 elements of a group, aligned to min(16, 4 s_k)
+  auto group_vec = [&](const Mapping& e, int k) {
+    uint64_t a = gcd64(gcd64(16, e.base[k] + e.F[k]), 4ull * e.sizes[k]);
+    if (e.L < e.N) a = gcd64(a, e.B);
+    return a >= std::min<uint64_t>(16, 4ull * e.sizes[k]);
+  };
+  if (kn.get(LLAMA_KNOB_WIDE_GROUP, 1)) {
+    if (w.mode <= 1) w.grp = group_ok(w.mode == 0 ? d : s) ? 1 : 0;
+    if (w.mode == 4) w.grp = group_ok(s) && group_ok(d) ? 1 : 0;
+  }
+  // leaf positions in class order: size, then unit, then the group vector flag, descending
+  struct LeafInfo { int k; uint32_t size, unit; };
+  std::vector<LeafInfo> li;
+  for (int k = 0; k < s.K(); ++k) {
+    uint32_t u = s.sizes[k];
+    for (int X = 0; X < 2; ++X) {
+      const Mapping& m = X == 0 ? s : d;
+      const WideSide& sd = w.side[X];
+      const uint32_t a = sd.A ? (uint32_t)gcd64(gcd64(16, sd.pitch), gcd64(sd.S, m.F[k])) : wide_e_align(m, k);
+      u = std::min(u, a);
+    }
+    if (w.grp && w.mode <= 1 && group_vec(w.mode == 0 ? d : s, k)) u |= 256;  // (f64: two 16-byte pieces)
+    li.push_back({k, s.sizes[k], u});
+  }
+  std::stable_sort(li.begin(), li.end(), [](const LeafInfo& a, const LeafInfo& b) {
+    return a.size != b.size ? a.size > b.size : a.unit > b.unit;  // (unit | 256 for vector groups)
+  });
+  for (size_t j = 0; j < li.size(); ++j) {
+    const int k = li[j].k;
+    WideLeaf& l = w.leaf[j];
+    l.size = (uint16_t)li[j].size;
+    l.unit = (uint16_t)li[j].unit;  // the class keeps the vector flag; leaves take the scalar unit
+    const uint16_t cls_unit = l.unit;
+    l.unit &= 0xFF;
+    l.soff = (uint32_t)s.F[k];
+    l.doff = (uint32_t)d.F[k];
+    w.order[j] = (uint16_t)k;
+    if (w.grp && w.mode == 4) l.vec = (group_vec(s, k) ? 1u : 0u) | (group_vec(d, k) ? 2u : 0u);
+    w.sl[j] = s.dev_leaf(k);
+    w.dl[j] = d.dev_leaf(k);
+    if (w.n_cls == 0 || w.cls[w.n_cls - 1].size != l.size || w.cls[w.n_cls - 1].unit != cls_unit) {
+      if (w.n_cls == 16) { *why = "too many leaf classes"; return false; }
+      w.cls[w.n_cls++] = WideClass{(uint16_t)j, (uint16_t)j, l.size, cls_unit};
+    }
+    w.cls[w.n_cls - 1].j1 = (uint16_t)(j + 1);
+  }
+  if (w.mode == 4) {  // leaf batches of element buffers (n + n / 32 elements each) within 40 KB
+    const uint64_t budget = 40 * 1024;
+    w.buf = (uint32_t)smem;
+    uint64_t used = 0;
+    w.nbatch = 0;
+    w.bstart[0] = 0;
+    for (size_t j = 0; j < li.size(); ++j) {
+      const uint64_t bytes = align16((uint64_t)(w.grp ? n : n + n / 32) * li[j].size);  // (grp: swizzled, unpadded)
+      if (used && used + bytes > budget) {
+        w.bstart[++w.nbatch] = (uint16_t)j;
+        used = 0;
+      }
+      w.leaf[j].buf = (uint32_t)used;
+      used += bytes;
+      smem = std::max<uint64_t>(smem, w.buf + used);
+    }
+    w.bstart[++w.nbatch] = (uint16_t)li.size();
+    if (lt != 10) { *why = "E -> E tiles are 32 x 32 records"; return false; }  // 4 records per thread
+  }
+  w.n_items = n_tiles * (w.mode == 4 ? w.nbatch : 1);
+  if (w.n_items >= (1ull << 31)) { *why = "more than 2^31 tiles"; return false; }  // 32-bit tile loop
+  if (w.mode == 3) w.u3 = (uint32_t)gcd64(gcd64(16, w.side[0].S), gcd64(w.side[0].pitch, w.side[1].chunk));
+  if (smem > 200 * 1024) { *why = "tile images exceed shared memory"; return false; }
+  w.smem = (uint32_t)align16(std::max<uint64_t>(smem, 16));
+  p->path = LLAMA_PATH_TRANSPOSE;
+  p->smem_bytes = (int)w.smem;
+  // E destinations with padding (aligned SoA SB gaps, aligned / tail AoSoA
+  // lanes) are zero-filled first; A destinations zero their images
+  p->naive_zero_fill = !dA && d.has_padding();
+  if (p->naive_zero_fill) p->fill.reset(new FillParams(make_fill(d, 0)));
+  return true;
+}
+
+bool plan_wide(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why) {
+  if (plan_wide_impl(s, d, kn, p, why)) return true;
+  p->wide.reset();
+  return false;
+}
+
 // Every leaf one contiguous run of N * s_k bytes in the mapping (SoA single /
 // multi blob, a part of one block), starting 16-byte aligned.
 static bool single_runs(const Mapping& m) {
@@ -755,6 +984,8 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
   // record (index) -> record (index) across storage orders, or counting every
   // address resolution (Trace / Heatmap): the element-wise kernel only
   if (s.lin != d.lin || s.trace || d.trace) {
+    const bool tr = path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE;
+    if (tr && kn.get(LLAMA_KNOB_WIDE, 1) == 2 && plan_wide(s, d, kn, out, &why)) return LLAMA_OK;
     if (path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) {
       std::unique_ptr<JitPlan> jp(new JitPlan);
       if (plan_jit2d(s, d, kn, jp.get(), &why)) {
@@ -767,8 +998,8 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
       std::fprintf(stderr, "plan_jit2d: %s\n", why.c_str());
 #endif
     }
-    if ((path == LLAMA_PATH_AUTO || path == LLAMA_PATH_TRANSPOSE) && plan_transpose(s, d, kn, out, &why))
-      return LLAMA_OK;
+    if (tr && plan_transpose(s, d, kn, out, &why)) return LLAMA_OK;
+    if (tr && plan_wide(s, d, kn, out, &why)) return LLAMA_OK;
     if (path != LLAMA_PATH_AUTO && path != LLAMA_PATH_NAIVE) {
       *err = "path not applicable to this mapping pair: linearised differently or traced: " + why;
       return LLAMA_ERR_UNSUPPORTED;

@@ -42,6 +42,7 @@ struct Plan {
   std::unique_ptr<PermParams> perm;
   std::unique_ptr<DirectParams> direct;  // PERMUTE path, direct variant (AoS <-> SoA, many leaves)
   std::unique_ptr<JitPlan> jit;          // PERMUTE path, plan-time specialised kernel (wide records, splits)
+  std::unique_ptr<WideParams> wide;      // TRANSPOSE path, wide records (k_transpose_wide)
 };
 
 // Checks S:484-486 (same leaf types, same extents).
@@ -55,6 +56,7 @@ llama_status make_plan(const Mapping& s, const Mapping& d, llama_path path, int 
 // Path-specific builders; return false (with *why) when not applicable.
 bool plan_blobcopy(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why);
 bool plan_transpose(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why);
+bool plan_wide(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p, std::string* why);
 bool plan_run(const Mapping& s, const Mapping& d, Plan* p, std::string* why);
 bool plan_permute(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why);
 bool plan_direct(const Mapping& s, const Mapping& d, int tile_records, const Knobs& kn, Plan* p, std::string* why);

@@ -366,3 +366,30 @@ def test_jit_plans_compile_without_spills():
                                 "-std=c++17", "-Xptxas", "-v", "-o", fn + ".cubin", fn], capture_output=True, text=True)
             assert r.returncode == 0, r.stderr[-2000:]
             assert "0 bytes spill stores, 0 bytes spill loads" in r.stderr, (name, r.stderr[-600:])
+
+
+def test_wide_transpose_plans():
+    """HEP100 transposing copies (380 / 480-byte records, too wide for the JIT
+    transpose's TY x 32 tiles) take the wide kernel: an AoS side is an image
+    side, tiles of 128 records with 32 along an element-wise side's order
+    (64 when two images exceed 64 KB), 32 x 32 between element-wise sides;
+    Morton tiles are 2^a x 2^a or 2^a x 2^(a+1); knob wide=0 -> naive."""
+    def pl(a, sl, b, dl, ext=(1024, 1024), knobs=None):
+        sm = llama.Mapping.from_spec(W.HEP100, list(ext), W.resolve_spec(a), lin=sl)
+        dm = llama.Mapping.from_spec(W.HEP100, list(ext), W.resolve_spec(b), lin=dl)
+        return llama.plan(sm, dm, knobs=knobs)
+    p = pl("aos", "row", "soa_mb", "col")
+    assert p["path"] == "transpose" and p["wide"] and p["tile_records"] == 128 and p["moves"] == 0
+    assert pl("soa_mb", "col", "aos_aligned", "row")["moves"] == 1
+    p = pl("aos", "row", "aos_aligned", "col")
+    assert p["moves"] == 2 and p["tile_records"] == 64
+    assert pl("aos", "row", "aos", "morton")["moves"] == 3
+    assert pl("aos_aligned", "row", "aos_aligned", "col")["moves"] == 2  # padding: never copied from the source
+    p = pl("soa_mb", "row", "soa_sb", "col")
+    assert p["moves"] == 4 and p["tile_records"] == 1024
+    assert pl("soa_mb", "morton", "soa_sb", "row", ext=(16, 16))["path"] == "naive"
+    assert pl("aos", "morton", "soa_sb", "row", ext=(4, 4))["tile_records"] == 16
+    assert pl("aos", "row", "soa_mb", "col", knobs={"wide": 0})["path"] == "naive"
+    small = llama.Mapping.from_spec(W.PARTICLE7, [64, 64], W.resolve_spec("aos"), lin="row")
+    smallc = llama.Mapping.from_spec(W.PARTICLE7, [64, 64], W.resolve_spec("soa_mb"), lin="col")
+    assert not llama.plan(small, smallc)["wide"] and llama.plan(small, smallc, knobs={"wide": 2})["wide"]

@@ -1,0 +1,108 @@
+"""GPU parity of the wide-record transposing copy (k_transpose_wide.cu; SURVEY
+§8(f) f4: rank-2 views of different storage orders, reading #26)
+against the oracle: every byte of every destination blob, destinations
+pre-filled with 0x5A, source padding poisoned with 0xCD."""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def llama():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_04284_b200 as m
+    return m
+
+
+def _check(llama, oracle, schema, ext, a, slin, b, dlin, knobs=None, expect_wide=True, seed=5):
+    sspec, dspec = W.resolve_spec(a), W.resolve_spec(b)
+    sm = llama.Mapping.from_spec(schema, ext, sspec, lin=slin)
+    dm = llama.Mapping.from_spec(schema, ext, dspec, lin=dlin)
+    if expect_wide:
+        assert llama.plan(sm, dm, knobs=knobs)["wide"], (a, slin, b, dlin)
+    so = oracle.mapping_from_spec(schema, ext, sspec, lin=slin)
+    do = oracle.mapping_from_spec(schema, ext, dspec, lin=dlin)
+    sb = sm.alloc("cuda")
+    llama.generate(sm, sb, seed, pad_byte=0xCD)
+    src = oracle.make_view(so, seed, pad_fill=0xCD)
+    exp = oracle.copy(so, src, do, nthreads=8)
+    db = dm.alloc("cuda")
+    for t in db:
+        t.fill_(0x5A)
+    llama.copy(sm, sb, dm, db, knobs=knobs)
+    torch.cuda.synchronize()
+    for j, t in enumerate(db):
+        got = t.cpu().numpy()
+        if not np.array_equal(got, exp[j]):
+            bad = np.nonzero(got != exp[j])[0]
+            raise AssertionError(f"{a}/{slin} -> {b}/{dlin} {ext}: blob {j}: {bad.size} bytes differ, first at {bad[0]}")
+
+
+HEP_KINDS = ["aos", "aos_aligned", "soa_mb", "soa_sb", "aosoa8", "soa_sb_aligned", "split_hep"]
+LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "col"), ("col", "morton")]
+
+
+@pytest.mark.parametrize("lins", LINS)
+@pytest.mark.parametrize("ext", [[64, 64], [32, 32]])
+def test_hep100_every_kind_pair(llama, oracle_mod, lins, ext):
+    """HEP100 (380 / 480-byte records) over every ordered kind pair; Morton
+    extents equal powers of two."""
+    for a in HEP_KINDS:
+        for b in HEP_KINDS:
+            if b == "split_hep" or a == "split_hep":
+                _check(llama, oracle_mod, W.HEP100, ext, a, lins[0], b, lins[1], expect_wide=False)
+            else:
+                _check(llama, oracle_mod, W.HEP100, ext, a, lins[0], b, lins[1])
+
+
+@pytest.mark.parametrize("ext", [[37, 70], [1, 300], [300, 1], [33, 129], [1, 1], [5, 3]])
+@pytest.mark.parametrize("lins", [("row", "col"), ("col", "row")])
+def test_hep100_ragged(llama, oracle_mod, ext, lins):
+    """Partial tiles on every edge (row / column extents not multiples of the tile)."""
+    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos_aligned"), ("aos", "aos_aligned"), ("aos", "aos"),
+                 ("aos_aligned", "aos"), ("soa_sb", "soa_mb"), ("aosoa8", "aos"), ("aos", "aosoa8"),
+                 ("soa_mb", "soa_sb_aligned")]:
+        _check(llama, oracle_mod, W.HEP100, ext, a, lins[0], b, lins[1])
+
+
+@pytest.mark.parametrize("ext", [[8, 8], [4, 4], [2, 2], [16, 16]])
+def test_hep100_small_morton(llama, oracle_mod, ext):
+    """Morton views smaller than the tile: the tile is clipped and stays square
+    or 1 x 2 (E -> E needs 32 x 32 and falls back to the naive kernel)."""
+    for a, b in [("aos", "soa_mb"), ("soa_mb", "aos"), ("aos", "aos_aligned"), ("soa_mb", "soa_sb")]:
+        for lins in [("row", "morton"), ("morton", "col")]:
+            _check(llama, oracle_mod, W.HEP100, ext, a, lins[0], b, lins[1],
+                   expect_wide=not (a.startswith("soa") and b.startswith("soa")))
+
+
+def test_hep100_aosoa_odd_lanes(llama, oracle_mod):
+    """AoSoA with a lane count that is not a power of two (division in the
+    block split, reading #8) on either side."""
+    sm = ("aosoa", 3, False)
+    for sl, dl in [("row", "col"), ("col", "morton")]:
+        for a, b in [(sm, "aos"), ("aos_aligned", sm), (sm, "soa_mb"), ("soa_sb", sm)]:
+            _check(llama, oracle_mod, W.HEP100, [32, 32], a, sl, b, dl)
+
+
+@pytest.mark.parametrize("schema", [W.PARTICLE7, W.LISTING1])
+def test_small_records_forced(llama, oracle_mod, schema):
+    """Knob wide=2: records the JIT transpose handles, forced onto the wide
+    kernel (Listing-1 packed, 21 B, is an element-wise side; aligned 32 B an
+    image side)."""
+    kn = {"wide": 2}
+    for a in ["aos", "aos_aligned", "soa_mb", "aosoa8"]:
+        for b in ["aos", "aos_aligned", "soa_sb"]:
+            for sl, dl in [("row", "col"), ("morton", "row")]:
+                _check(llama, oracle_mod, schema, [64, 64], a, sl, b, dl, knobs=kn)
+
+
+def test_hep100_full_size(llama, oracle_mod):
+    """1024 x 1024 HEP100 (the pair-matrix size), whole blobs."""
+    for a, sl, b, dl in [("aos", "row", "soa_mb", "col"), ("soa_mb", "col", "aos_aligned", "row"),
+                         ("aos", "row", "aos_aligned", "morton"), ("soa_sb", "morton", "soa_mb", "row")]:
+        _check(llama, oracle_mod, W.HEP100, [1024, 1024], a, sl, b, dl)

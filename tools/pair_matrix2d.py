@@ -17,7 +17,9 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
 KINDS = ["aos", "aos_aligned", "soa_mb", "soa_sb", "aosoa8"]
 LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "row"), ("col", "morton")]
 rows = []
-for schema, e in (("particle7", 4096), ("listing1", 4096), ("hep100", 1024)):
+SIZES = {"particle7": 4096, "listing1": 4096, "hep100": 1024}
+for schema in (sys.argv[1].split(",") if len(sys.argv) > 1 else list(SIZES)):
+    e = SIZES[schema]
     sch = W.SCHEMAS[schema]
     warm = None
     for sl, dl in LINS:
@@ -47,9 +49,10 @@ for schema, e in (("particle7", 4096), ("listing1", 4096), ("hep100", 1024)):
                 ms = e0.elapsed_time(e1) / 5
                 g = (sm.footprint() + dm.footprint()) / ms / 1e6
                 pl = llama.plan(sm, dm)
-                rows.append((g / PEAK, g, schema, e, f"{a}/{sl}", f"{b}/{dl}", pl["path"], pl["jit"]))
+                rows.append((g / PEAK, g, schema, e, f"{a}/{sl}", f"{b}/{dl}", pl["path"],
+                             " jit" if pl["jit"] else " wide" if pl["wide"] else ""))
         del src, dst
         torch.cuda.empty_cache()
 rows.sort()
 for f, g, schema, e, a, b, path, jit in rows:
-    print(f"{f:6.3f} {g:7.0f} GB/s  {schema:9s} {e}x{e}  {a:>18s} -> {b:<18s} {path}{' jit' if jit else ''}")
+    print(f"{f:6.3f} {g:7.0f} GB/s  {schema:9s} {e}x{e}  {a:>18s} -> {b:<18s} {path}{jit}")
