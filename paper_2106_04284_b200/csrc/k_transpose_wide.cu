@@ -183,18 +183,27 @@ __device__ __forceinline__ void load_image(const WideParams& p, const WideSide& 
   runs_of(s, tl, nruns, len);
   const uint8_t* blob = p.sb[s.blob];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, ch = s.chunk;
-  for (uint32_t j = warp; j < nruns; j += kWT / 32) {
-    const uint8_t* g = blob + run_start(p, s, tl, j);
-    uint8_t* d = img + j * s.pitch;
-    const uint32_t bytes = len * s.S, body = bytes / ch * ch;
-    for (uint32_t u = lane * ch; u < body; u += 32 * ch) cp_async(d + u, g + u, ch);
-    for (uint32_t u = body + lane * 4; u < bytes; u += 128) cp_async(d + u, g + u, 4);
+  const uint32_t bytes = len * s.S, body = bytes / ch * ch;
+  if (nruns >= kWT / 32) {  // a warp per run
+    for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+      const uint8_t* g = blob + run_start(p, s, tl, j);
+      uint8_t* d = img + j * s.pitch;
+      for (uint32_t u = lane * ch; u < body; u += 32 * ch) cp_async(d + u, g + u, ch);
+      for (uint32_t u = body + lane * 4; u < bytes; u += 128) cp_async(d + u, g + u, 4);
+    }
+  } else {  // few long runs (a Morton tile is one): the whole CTA per run
+    for (uint32_t j = 0; j < nruns; ++j) {
+      const uint8_t* g = blob + run_start(p, s, tl, j);
+      uint8_t* d = img + j * s.pitch;
+      for (uint32_t u = threadIdx.x * ch; u < body; u += kWT * ch) cp_async(d + u, g + u, ch);
+      for (uint32_t u = body + threadIdx.x * 4; u < bytes; u += kWT * 4) cp_async(d + u, g + u, 4);
+    }
   }
 }
 
-template <int U>
+template <int U, int STRIDE = 32>
 __device__ __forceinline__ void copy_run(uint8_t* g, const uint8_t* s, uint32_t bytes, uint32_t lane) {
-  for (uint32_t u = lane * U; u + U <= bytes; u += 32 * U) {
+  for (uint32_t u = lane * U; u + U <= bytes; u += STRIDE * U) {
     if constexpr (U == 16) *reinterpret_cast<uint4*>(g + u) = *reinterpret_cast<const uint4*>(s + u);
     if constexpr (U == 8) *reinterpret_cast<uint2*>(g + u) = *reinterpret_cast<const uint2*>(s + u);
     if constexpr (U == 4) *reinterpret_cast<uint32_t*>(g + u) = *reinterpret_cast<const uint32_t*>(s + u);
@@ -208,14 +217,25 @@ __device__ __forceinline__ void flush_image(const WideParams& p, const WideSide&
   runs_of(s, tl, nruns, len);
   uint8_t* blob = p.db[s.blob];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t j = warp; j < nruns; j += kWT / 32) {
-    uint8_t* g = blob + run_start(p, s, tl, j);
-    const uint8_t* d = img + j * s.pitch;
-    const uint32_t bytes = len * s.S, body = bytes / s.chunk * s.chunk;
-    if (s.chunk == 16) copy_run<16>(g, d, body, lane);
-    else if (s.chunk == 8) copy_run<8>(g, d, body, lane);
-    else copy_run<4>(g, d, body, lane);
-    copy_run<4>(g + body, d + body, bytes - body, lane);
+  const uint32_t bytes = len * s.S, body = bytes / s.chunk * s.chunk;
+  if (nruns >= kWT / 32) {  // a warp per run
+    for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+      uint8_t* g = blob + run_start(p, s, tl, j);
+      const uint8_t* d = img + j * s.pitch;
+      if (s.chunk == 16) copy_run<16>(g, d, body, lane);
+      else if (s.chunk == 8) copy_run<8>(g, d, body, lane);
+      else copy_run<4>(g, d, body, lane);
+      copy_run<4>(g + body, d + body, bytes - body, lane);
+    }
+  } else {  // the whole CTA per run
+    for (uint32_t j = 0; j < nruns; ++j) {
+      uint8_t* g = blob + run_start(p, s, tl, j);
+      const uint8_t* d = img + j * s.pitch;
+      if (s.chunk == 16) copy_run<16, kWT>(g, d, body, threadIdx.x);
+      else if (s.chunk == 8) copy_run<8, kWT>(g, d, body, threadIdx.x);
+      else copy_run<4, kWT>(g, d, body, threadIdx.x);
+      copy_run<4, kWT>(g + body, d + body, bytes - body, threadIdx.x);
+    }
   }
 }
 
@@ -695,9 +715,10 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
         uint32_t nruns, len;
         runs_of(S1, tl, nruns, len);
         const uint32_t warp = tid >> 5, lane = tid & 31, u = p.u3;
-        for (uint32_t j = warp; j < nruns; j += kWT / 32) {
+        const bool wpr = nruns >= kWT / 32;  // a warp per run, else the warps share each run's records
+        for (uint32_t j = wpr ? warp : 0; j < nruns; j += wpr ? kWT / 32 : 1) {
           uint8_t* g = p.db[S1.blob] + run_start(p, S1, tl, j);
-          for (uint32_t q = 0; q < len; ++q) {
+          for (uint32_t q = wpr ? 0 : warp; q < len; q += wpr ? 1 : kWT / 32) {
             uint32_t r, c;
             t_rc(S1.lin, (j << S1.lrun) + q, p.lty, p.ltx, r, c);
             const uint8_t* s = smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx));

@@ -203,18 +203,60 @@ uint32_t wide_chunk(const Mapping& m, uint32_t lrun) {
   return 4;
 }
 
-// image pitch: the run bytes rounded up to the chunk, then the candidate
-// (within 8 chunks) that spreads 32 consecutive runs over the most banks
-uint32_t wide_pitch(uint64_t run_bytes, uint32_t chunk, uint32_t nruns) {
+// host copies of the kernel's tile orders (k_transpose_wide.cu t_rc / rc_t)
+uint32_t h_compact(uint32_t x) {
+  uint32_t r = 0;
+  for (int b = 0; b < 16; ++b) r |= ((x >> (2 * b)) & 1u) << b;
+  return r;
+}
+uint32_t h_part(uint32_t x) {
+  uint32_t r = 0;
+  for (int b = 0; b < 16; ++b) r |= ((x >> b) & 1u) << (2 * b);
+  return r;
+}
+void h_t_rc(uint32_t lin, uint32_t t, uint32_t lty, uint32_t ltx, uint32_t& r, uint32_t& c) {
+  if (lin == LLAMA_ROW_MAJOR) r = t >> ltx, c = t & ((1u << ltx) - 1);
+  else if (lin == LLAMA_COL_MAJOR) c = t >> lty, r = t & ((1u << lty) - 1);
+  else c = h_compact(t), r = h_compact(t >> 1);
+}
+uint32_t h_rc_t(uint32_t lin, uint32_t r, uint32_t c, uint32_t lty, uint32_t ltx) {
+  if (lin == LLAMA_ROW_MAJOR) return (r << ltx) | c;
+  if (lin == LLAMA_COL_MAJOR) return (c << lty) | r;
+  return h_part(c) | (h_part(r) << 1);
+}
+
+// Shared-memory wavefronts of one warp's 4-byte accesses at byte offsets `off`
+// (the most distinct words that fall into one bank).
+uint32_t wavefronts(const std::vector<uint64_t>& off) {
+  std::vector<std::vector<uint64_t>> bank(32);
+  for (uint64_t o : off) {
+    auto& b = bank[(o / 4) % 32];
+    if (std::find(b.begin(), b.end(), o / 4) == b.end()) b.push_back(o / 4);
+  }
+  size_t w = 1;
+  for (auto& b : bank) w = std::max(w, b.size());
+  return (uint32_t)w;
+}
+
+// Image pitch of an A side: the run bytes rounded up to the chunk, then the
+// candidate (within 16 chunks) whose warp accesses of the move phase take the
+// fewest wavefronts.  `lanes(i)` gives warp 0's records (indices along the A
+// side's own order) of access i.
+template <typename Lanes>
+uint32_t wide_pitch(uint64_t run_bytes, uint32_t chunk, uint32_t nruns, uint32_t S, uint32_t lrun, int n_acc,
+                    Lanes lanes) {
   const uint64_t p0 = (run_bytes + chunk - 1) / chunk * chunk;
   if (nruns <= 1) return (uint32_t)p0;
   uint64_t best = p0;
-  int best_banks = -1;
-  for (uint64_t p = p0; p < p0 + 8 * chunk; p += chunk) {
-    uint32_t mask = 0;
-    for (uint32_t j = 0; j < std::min<uint32_t>(nruns, 32); ++j) mask |= 1u << ((j * p / 4) % 32);
-    const int banks = __builtin_popcount(mask);
-    if (banks > best_banks) best_banks = banks, best = p;
+  uint32_t best_w = ~0u;
+  for (uint64_t p = p0; p < p0 + 16 * chunk; p += chunk) {
+    uint32_t w = 0;
+    for (int i = 0; i < n_acc; ++i) {
+      std::vector<uint64_t> off;
+      for (uint32_t t : lanes(i)) off.push_back((t >> lrun) * p + (t & ((1u << lrun) - 1)) * (uint64_t)S);
+      w += wavefronts(off);
+    }
+    if (w < best_w) best_w = w, best = p;
   }
   return (uint32_t)best;
 }
@@ -287,7 +329,7 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
       sd.lrun = m.lin == LLAMA_ROW_MAJOR ? ltx : m.lin == LLAMA_COL_MAJOR ? lty : lt;
       sd.chunk = wide_chunk(m, sd.lrun);
       const uint32_t nruns = 1u << (lt - sd.lrun);
-      sd.pitch = wide_pitch((uint64_t)sd.S << sd.lrun, sd.chunk, nruns);
+      sd.pitch = (uint32_t)(((uint64_t)sd.S << sd.lrun) + sd.chunk - 1) / sd.chunk * sd.chunk;  // (re-chosen below)
       if (image) {
         sd.img = (uint32_t)smem;
         sd.img_bytes = (uint32_t)align16((uint64_t)nruns * sd.pitch);
@@ -324,6 +366,32 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
   if (kn.get(LLAMA_KNOB_WIDE_GROUP, 1)) {
     if (w.mode <= 1) w.grp = group_ok(w.mode == 0 ? d : s) ? 1 : 0;
     if (w.mode == 4) w.grp = group_ok(s) && group_ok(d) ? 1 : 0;
+  }
+  // image pitches by simulated bank conflicts of warp 0's move accesses
+  // (before the images are placed: a pitch changes the image size)
+  {
+    uint64_t off = 0;
+    for (int X = 0; X < 2; ++X) {
+      WideSide& sd = w.side[X];
+      if (!sd.A || sd.img_bytes == 0) continue;
+      const uint32_t nruns = 1u << (lt - sd.lrun);
+      const uint32_t ord = w.mode == 1 ? w.side[0].lin : w.side[1].lin;  // the order the lanes run along
+      const bool g = w.grp && w.mode <= 1;
+      auto lanes = [&](int i) {
+        std::vector<uint32_t> v;
+        for (uint32_t l = 0; l < 32 && l < (g ? n / 4 : n); ++l) {
+          uint32_t r, c;
+          h_t_rc(ord, g ? 4 * l + i : l, lty, ltx, r, c);
+          v.push_back(h_rc_t(sd.lin, r, c, lty, ltx));
+        }
+        return v;
+      };
+      sd.pitch = wide_pitch((uint64_t)sd.S << sd.lrun, sd.chunk, nruns, sd.S, sd.lrun, g ? 4 : 1, lanes);
+      sd.img = (uint32_t)off;
+      sd.img_bytes = (uint32_t)align16((uint64_t)nruns * sd.pitch);
+      off += sd.img_bytes;
+    }
+    if (w.mode != 4) smem = off;
   }
   // leaf positions in class order: size, then unit, then the group vector flag, descending
   struct LeafInfo { int k; uint32_t size, unit; };
