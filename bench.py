@@ -435,15 +435,12 @@ class Ctx:
         self.rdev = "cpu" if getattr(args, "test_one_device", False) else "cuda"  # reduction tensors (gloo: host)
 
     def barrier(self):
-        if self.world > 1:
-            self.dist.barrier()
+        from paper_2106_04284_b200 import dist as D
+        D.barrier()
 
     def max_over_ranks(self, v):
-        if self.world == 1:
-            return float(v)
-        t = self.torch.tensor([float(v)], device=self.rdev, dtype=self.torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return float(t.item())
+        from paper_2106_04284_b200 import dist as D
+        return D.max_over_ranks(v, device=self.rdev)
 
     def min_over_ranks(self, v):
         return -self.max_over_ranks(-v)
@@ -607,11 +604,8 @@ def measure_config(ctx, name, steps, warmup, headline=False):
 
 
 def sum_over_ranks(ctx, v):
-    if ctx.world == 1:
-        return float(v)
-    t = ctx.torch.tensor([float(v)], device=ctx.rdev, dtype=ctx.torch.float64)
-    ctx.dist.all_reduce(t)
-    return float(t.item())
+    from paper_2106_04284_b200 import dist as D
+    return D.sum_over_ranks(v, device=ctx.rdev)
 
 
 def e2e_leg(ctx, maps, src, dst, pairs, steps):
