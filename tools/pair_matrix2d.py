@@ -18,6 +18,7 @@ KINDS = ["aos", "aos_aligned", "soa_mb", "soa_sb", "aosoa8"]
 LINS = [("row", "col"), ("col", "row"), ("row", "morton"), ("morton", "row"), ("col", "morton")]
 rows = []
 SIZES = {"particle7": 4096, "listing1": 4096, "hep100": 1024}
+KN = dict((k, int(v)) for k, v in (x.split("=") for x in sys.argv[2].split(","))) if len(sys.argv) > 2 else None
 for schema in (sys.argv[1].split(",") if len(sys.argv) > 1 else list(SIZES)):
     e = SIZES[schema]
     sch = W.SCHEMAS[schema]
@@ -38,17 +39,17 @@ for schema in (sys.argv[1].split(",") if len(sys.argv) > 1 else list(SIZES)):
         for a in KINDS:
             for b in KINDS:
                 sm, dm = maps_s[a], maps_d[b]
-                llama.copy(sm, src[a], dm, dst[b])
+                llama.copy(sm, src[a], dm, dst[b], knobs=KN)
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 for _ in range(5):
-                    llama.copy(sm, src[a], dm, dst[b])
+                    llama.copy(sm, src[a], dm, dst[b], knobs=KN)
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / 5
                 g = (sm.footprint() + dm.footprint()) / ms / 1e6
-                pl = llama.plan(sm, dm)
+                pl = llama.plan(sm, dm, knobs=KN)
                 rows.append((g / PEAK, g, schema, e, f"{a}/{sl}", f"{b}/{dl}", pl["path"],
                              " jit" if pl["jit"] else " wide" if pl["wide"] else ""))
         del src, dst
