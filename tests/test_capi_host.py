@@ -381,8 +381,10 @@ def test_wide_transpose_plans():
     p = pl("aos", "row", "soa_mb", "col")
     assert p["path"] == "transpose" and p["wide"] and p["tile_records"] == 128 and p["moves"] == 0
     assert pl("soa_mb", "col", "aos_aligned", "row")["moves"] == 1
-    p = pl("aos", "row", "aos_aligned", "col")
+    p = pl("aos", "row", "aos_aligned", "col", knobs={"jit": 0})
     assert p["moves"] == 2 and p["tile_records"] == 64
+    p = pl("aos", "row", "aos_aligned", "col")  # the JIT transpose with 4-row tiles (per-record programs)
+    assert p["jit"] and p["tile_records"] == 128
     assert pl("aos", "row", "aos", "morton")["moves"] == 3
     assert pl("aos_aligned", "row", "aos_aligned", "col")["moves"] == 2  # padding: never copied from the source
     p = pl("soa_mb", "row", "soa_sb", "col")

@@ -23,8 +23,9 @@ def _check(llama, oracle, schema, ext, a, slin, b, dlin, knobs=None, expect_wide
     sspec, dspec = W.resolve_spec(a), W.resolve_spec(b)
     sm = llama.Mapping.from_spec(schema, ext, sspec, lin=slin)
     dm = llama.Mapping.from_spec(schema, ext, dspec, lin=dlin)
-    if expect_wide:
-        assert llama.plan(sm, dm, knobs=knobs)["wide"], (a, slin, b, dlin)
+    if expect_wide:  # the wide kernel, or the JIT transpose's 4- / 8-row tiles (AoS images of different layouts)
+        pl = llama.plan(sm, dm, knobs=knobs)
+        assert pl["wide"] or (pl["jit"] and pl["path"] == "transpose"), (a, slin, b, dlin)
     so = oracle.mapping_from_spec(schema, ext, sspec, lin=slin)
     do = oracle.mapping_from_spec(schema, ext, dspec, lin=dlin)
     sb = sm.alloc("cuda")
@@ -106,3 +107,16 @@ def test_hep100_full_size(llama, oracle_mod):
     for a, sl, b, dl in [("aos", "row", "soa_mb", "col"), ("soa_mb", "col", "aos_aligned", "row"),
                          ("aos", "row", "aos_aligned", "morton"), ("soa_sb", "morton", "soa_mb", "row")]:
         _check(llama, oracle_mod, W.HEP100, [1024, 1024], a, sl, b, dl)
+
+
+@pytest.mark.parametrize("ext", [[64, 64], [8, 96], [1024, 1024]])
+def test_hep100_jit_short_tiles(llama, oracle_mod, ext):
+    """Packed <-> aligned AoS transposes of 380 / 480-byte records through the
+    JIT transpose with 8- / 4-row tiles (per-record programs)."""
+    for a, sl, b, dl in [("aos", "row", "aos_aligned", "col"), ("aos_aligned", "col", "aos", "row"),
+                         ("aos", "col", "aos_aligned", "row"), ("aos_aligned", "row", "aos", "col")]:
+        sm = llama.Mapping.from_spec(W.HEP100, ext, W.resolve_spec(a), lin=sl)
+        dm = llama.Mapping.from_spec(W.HEP100, ext, W.resolve_spec(b), lin=dl)
+        pl = llama.plan(sm, dm)
+        assert pl["jit"] and pl["tile_records"] in (128, 256), pl
+        _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl)
