@@ -279,6 +279,8 @@ typedef enum {
                                   the JIT / 32 x 32 transposes do not apply (HEP100-sized records), 2 first (1) */
   LLAMA_KNOB_WIDE_GROUP,       /* wide transpose, AoS <-> element-wise side: a thread moves 4 records along the
                                   element-wise side's order, one vector per leaf there (1) */
+  LLAMA_KNOB_WIDE_STAGE,       /* wide transpose, element-wise -> AoS: the element-wise side lands by cp.async in a
+                                  shared-memory staging area before the image is written (0: measured slower, 0.46 -> 0.39) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

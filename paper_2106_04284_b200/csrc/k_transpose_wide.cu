@@ -456,6 +456,59 @@ struct GroupAE {
   }
 };
 
+// E -> A staged (stage): phase 1 moves every leaf's groups of the tile by
+// cp.async into a staging area (leaf j: the tile's elements in E order at
+// stg + buf_j), so all of a thread's loads are in flight at once; phase 2
+// scatters them from shared memory into the image.
+struct StageEA {
+  const WideParams& p;
+  uint8_t* stg;
+  uint64_t qB, rem;
+  uint32_t gi, nv, j0, j1, kl, nl;
+  template <int SZ, int U, bool VEC>
+  __device__ __forceinline__ void run() {
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl) {
+      const WideLeaf& l = p.leaf[j];
+      const uint8_t* s = l.sp + qB + rem * SZ;
+      uint8_t* d = stg + l.buf + gi * 4 * SZ;
+      if (VEC && nv == 4) {
+        if constexpr (SZ == 8) {
+          cp_async(d, s, 16);
+          cp_async(d + 16, s + 16, 16);
+        } else {
+          cp_async(d, s, 4 * SZ);
+        }
+      } else {
+        each4([&](auto I) {
+          if (I.v < (int)nv) st<SZ, SZ>(d + I.v * SZ, ld<SZ, U>(s + I.v * SZ));
+        });
+      }
+    }
+  }
+};
+
+struct ScatterEA {
+  const WideParams& p;
+  const uint8_t* stg;
+  uint8_t* img;
+  uint32_t ro0, ro1, ro2, ro3;
+  uint32_t gi, nv, j0, j1, kl, nl;
+  template <int SZ, int U, bool VEC>
+  __device__ __forceinline__ void run() {
+    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+#pragma unroll 1
+    for (uint32_t j = j0 + kl; j < j1; j += nl) {
+      const WideLeaf& l = p.leaf[j];
+      Pk k{};
+      vld<SZ>(stg + l.buf + gi * 4 * SZ, k);  // (the staging group is 4 * s_k-aligned)
+      each4([&](auto I) {
+        if (I.v < (int)nv) st<SZ, U>(img + ro[I.v] + l.doff, pk_get<SZ, I.v>(k));
+      });
+    }
+  }
+};
+
 // E -> A: one E vector per leaf -> image scalars (two leaves' loads in flight)
 struct GroupEA {
   const WideParams& p;
@@ -750,6 +803,15 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
             uint64_t qB, rem;
             esplit(E, storage2(E.lin, tl.y0 + r0, tl.x0 + c0, p.H, p.W), qB, rem);
             const uint32_t kl2 = tid / ng < gl ? tid / ng : 0;
+            if (MODE == 1 && p.stage) {  // phase 1: cp.async into the staging area
+#pragma unroll 1
+              for (uint32_t q = 0; q < p.n_cls; ++q) {
+                const WideClass& cl = p.cls[q];
+                StageEA m{p, smem + p.buf, qB, rem, gi, nv, cl.j0, cl.j1, kl2, gl};
+                dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
+              }
+              continue;
+            }
 #pragma unroll 1
             for (uint32_t q = 0; q < p.n_cls; ++q) {
               const WideClass& cl = p.cls[q];
@@ -758,6 +820,28 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
                 dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
               } else {
                 GroupEA m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], qB, rem, nv, cl.j0, cl.j1, kl2, gl};
+                dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
+              }
+            }
+          }
+          if (MODE == 1 && p.stage) {  // phase 2: staging -> image
+            cp_async_wait_all();
+            __syncthreads();
+            for (uint32_t gi = tid % ng; gi < ng; gi += kWT) {
+              uint32_t ro[4], nv = 0;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                uint32_t r, c;
+                t_rc(E.lin, 4 * gi + i, p.lty, p.ltx, r, c);
+                ro[i] = img_off(A, rc_t(A.lin, r, c, p.lty, p.ltx));
+                if (r < tl.h && c < tl.w && nv == (uint32_t)i) ++nv;
+              }
+              if (!nv) continue;
+              const uint32_t kl2 = tid / ng < gl ? tid / ng : 0;
+#pragma unroll 1
+              for (uint32_t q = 0; q < p.n_cls; ++q) {
+                const WideClass& cl = p.cls[q];
+                ScatterEA m{p, smem + p.buf, smem + A.img, ro[0], ro[1], ro[2], ro[3], gi, nv, cl.j0, cl.j1, kl2, gl};
                 dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
               }
             }

@@ -364,8 +364,8 @@ struct WideParams {
   uint32_t buf;         // E -> E: shared-memory offset of the batch area
   uint32_t n_cls;
   uint32_t u3;          // mode 3: bytes per access of a record copy (16, 8, 4)
-  uint32_t grp;         // modes 0 / 1: threads move 4-record groups along the E side's order
-  uint32_t pad2_;
+  uint32_t grp;         // modes 0 / 1 / 4: threads move 4-record groups along the E side's order
+  uint32_t stage;       // mode 1, grp: the E side lands by cp.async in a staging area at buf first
   uint16_t bstart[kMaxLeaves + 1];   // E -> E: batch b = positions [bstart[b], bstart[b+1])
   uint16_t order[kMaxLeaves];        // leaf id at each position
   WideClass cls[16];

@@ -288,6 +288,13 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     // the E side's storage runs span the tile: 32 records along a row /
     // column side; a Morton tile is 2^a x 2^a or 2^a x 2^(a+1) (contiguous codes)
     const Mapping* e = !sA ? &s : !dA ? &d : nullptr;
+    // E -> A staged through shared memory (knob wide_stage, off: measured
+    // over the 30 HEP100 E -> A pairs, median 0.46 -> 0.39 -- the scatter out
+    // of the staging area into a packed image costs more than the register
+    // loads it replaces): 64-record tiles keep image + staging area <= 64 KB
+    if (!sA && dA && kn.get(LLAMA_KNOB_WIDE_STAGE, 0) && s.uniform && (s.L >= s.N || s.L % 4 == 0) &&
+        (s.lin != LLAMA_ROW_MAJOR || W % 4 == 0) && (s.lin != LLAMA_COL_MAJOR || H % 4 == 0))
+      lt = std::min<uint32_t>(lt, 6);
     if (morton || !e) lty = lt / 2, ltx = lt - lt / 2;
     else if (e->lin == LLAMA_ROW_MAJOR) ltx = 5, lty = lt - 5;
     else lty = 5, ltx = lt - 5;
@@ -447,6 +454,16 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     }
     w.bstart[++w.nbatch] = (uint16_t)li.size();
     if (lt != 10) { *why = "E -> E tiles are 32 x 32 records"; return false; }  // 4 records per thread
+  }
+  if (w.mode == 1 && w.grp && kn.get(LLAMA_KNOB_WIDE_STAGE, 0)) {  // staging area: leaf j's n elements in E order
+    w.stage = 1;
+    w.buf = (uint32_t)align16(smem);
+    uint64_t off = 0;
+    for (size_t j = 0; j < li.size(); ++j) {
+      w.leaf[j].buf = (uint32_t)off;
+      off += align16((uint64_t)n * li[j].size);
+    }
+    smem = w.buf + off;
   }
   w.n_items = n_tiles * (w.mode == 4 ? w.nbatch : 1);
   if (w.n_items >= (1ull << 31)) { *why = "more than 2^31 tiles"; return false; }  // 32-bit tile loop

@@ -120,3 +120,15 @@ def test_hep100_jit_short_tiles(llama, oracle_mod, ext):
         pl = llama.plan(sm, dm)
         assert pl["jit"] and pl["tile_records"] in (128, 256), pl
         _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl)
+
+
+def test_hep100_staged_knob(llama, oracle_mod):
+    """Knob wide_stage=1 (measured slower, off by default): element-wise -> AoS
+    through a cp.async staging area."""
+    kn = {"wide_stage": 1}
+    for a, sl, b, dl in [("soa_mb", "col", "aos", "row"), ("soa_sb", "morton", "aos_aligned", "row"),
+                         ("aosoa8", "row", "aos", "col")]:
+        for ext in ([64, 64], [36, 68]):
+            if "morton" in (sl, dl) and ext[0] != ext[1]:
+                continue
+            _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl, knobs=kn)
