@@ -281,6 +281,10 @@ typedef enum {
                                   element-wise side's order, one vector per leaf there (1) */
   LLAMA_KNOB_WIDE_STAGE,       /* wide transpose, element-wise -> AoS: the element-wise side lands by cp.async in a
                                   shared-memory staging area before the image is written (0: measured slower, 0.46 -> 0.39) */
+  LLAMA_KNOB_WIDE_CHUNK4,      /* wide transpose: an image may take 4-byte chunks for an odd-word run pitch when that
+                                  takes fewer simulated shared-memory wavefronts (0: measured slower) */
+  LLAMA_KNOB_WIDE_TORDER,      /* wide transpose tile order: 0 x fastest, 1 y fastest, 2 along a column-major
+                                  element-wise side (2) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

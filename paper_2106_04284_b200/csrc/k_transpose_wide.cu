@@ -241,7 +241,16 @@ __device__ __forceinline__ void flush_image(const WideParams& p, const WideSide&
 
 __device__ __forceinline__ Tile tile_of(const WideParams& p, uint32_t tile) {
   Tile tl;
-  const uint32_t ntx = (uint32_t)p.ntx, ty = tile / ntx, tx = tile - ty * ntx;  // (32-bit: no division call)
+  uint32_t ty, tx;  // (32-bit: no division call)
+  if (p.yfast) {
+    const uint32_t nty = (uint32_t)p.nty;
+    tx = tile / nty;
+    ty = tile - tx * nty;
+  } else {
+    const uint32_t ntx = (uint32_t)p.ntx;
+    ty = tile / ntx;
+    tx = tile - ty * ntx;
+  }
   tl.y0 = ty << p.lty;
   tl.x0 = tx << p.ltx;
   const uint64_t hh = p.H - tl.y0, ww = p.W - tl.x0;
@@ -537,14 +546,19 @@ struct GroupEA {
   template <int SZ, int U, bool VEC>
   __device__ __forceinline__ void run() {
     const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+    // LG leaves' loads in flight before their stores (4 while a pack is <= 16 bytes)
+    constexpr int LG = SZ == 8 ? 2 : 4;
 #pragma unroll 1
-    for (uint32_t j = j0 + kl; j < j1; j += 2 * nl) {
-      Pk k0{}, k1{};
-      const bool two = j + nl < j1;
-      ld_group<SZ, U, VEC>(j, k0);
-      if (two) ld_group<SZ, U, VEC>(j + nl, k1);
-      st_group<SZ, U>(j, k0, ro);
-      if (two) st_group<SZ, U>(j + nl, k1, ro);
+    for (uint32_t j = j0 + kl; j < j1; j += LG * nl) {
+      Pk k[LG];
+#pragma unroll
+      for (int g = 0; g < LG; ++g) {
+        k[g] = Pk{};
+        if (j + g * nl < j1) ld_group<SZ, U, VEC>(j + g * nl, k[g]);
+      }
+#pragma unroll
+      for (int g = 0; g < LG; ++g)
+        if (j + g * nl < j1) st_group<SZ, U>(j + g * nl, k[g], ro);
     }
   }
 };

@@ -354,6 +354,9 @@ struct WideClass {      // positions [j0, j1) share size, unit and (grp) the E-s
 struct WideParams {
   uint64_t H, W;
   uint64_t ntx;         // tiles along x
+  uint64_t nty;         // tiles along y
+  uint32_t yfast;       // tile order: y fastest (along a column-major side)
+  uint32_t pad3_;
   uint64_t n_items;     // tiles (x nbatch for E -> E)
   uint32_t lty, ltx;    // log2 tile rows / columns
   uint32_t mode;        // 0 A -> E, 1 E -> A, 2 A -> A (leaf moves), 3 A -> A (same record layout), 4 E -> E

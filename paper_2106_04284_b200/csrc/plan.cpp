@@ -393,7 +393,26 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
         }
         return v;
       };
-      sd.pitch = wide_pitch((uint64_t)sd.S << sd.lrun, sd.chunk, nruns, sd.S, sd.lrun, g ? 4 : 1, lanes);
+      // (r2) a 4-byte chunk allows odd-word pitches: the 4 records of a group
+      // sit in runs 4 apart, which a 16-byte multiple pitch folds onto 8 banks
+      // (4-way conflicts); take the chunk with the fewest wavefronts, the
+      // larger on a tie (fewer cp.async / store instructions)
+      uint32_t best_p = 0, best_c = sd.chunk, best_w = ~0u;
+      for (uint32_t c : {sd.chunk, 4u}) {
+        if (c > sd.chunk) continue;
+        const uint32_t pc = wide_pitch((uint64_t)sd.S << sd.lrun, c, nruns, sd.S, sd.lrun, g ? 4 : 1, lanes);
+        uint32_t wf = 0;
+        for (int i = 0; i < (g ? 4 : 1); ++i) {
+          std::vector<uint64_t> o;
+          for (uint32_t t : lanes(i)) o.push_back((t >> sd.lrun) * (uint64_t)pc + (t & ((1u << sd.lrun) - 1)) * (uint64_t)sd.S);
+          wf += wavefronts(o);
+        }
+        if (wf < best_w) best_w = wf, best_p = pc, best_c = c;
+      }
+      if (kn.get(LLAMA_KNOB_WIDE_CHUNK4, 0) == 0) best_p = wide_pitch((uint64_t)sd.S << sd.lrun, sd.chunk, nruns, sd.S,
+                                                                     sd.lrun, g ? 4 : 1, lanes), best_c = sd.chunk;
+      sd.pitch = best_p;
+      sd.chunk = best_c;
       sd.img = (uint32_t)off;
       sd.img_bytes = (uint32_t)align16((uint64_t)nruns * sd.pitch);
       off += sd.img_bytes;
@@ -464,6 +483,15 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
       off += align16((uint64_t)n * li[j].size);
     }
     smem = w.buf + off;
+  }
+  // tile order (knob wide_torder: 0 x fastest, 1 y fastest, 2 auto): auto runs
+  // the tiles along a column-major E side's storage order, so consecutive
+  // tiles continue the same columns (contiguous DRAM streams on that side)
+  {
+    const int64_t to = kn.get(LLAMA_KNOB_WIDE_TORDER, 2);
+    const Mapping& e = w.mode == 0 ? d : s;  // (mode 4: the source)
+    w.yfast = to == 1 || (to == 2 && (w.mode == 0 || w.mode == 1 || w.mode == 4) && e.lin == LLAMA_COL_MAJOR);
+    w.nty = ceil_div(H, 1ull << lty);
   }
   w.n_items = n_tiles * (w.mode == 4 ? w.nbatch : 1);
   if (w.n_items >= (1ull << 31)) { *why = "more than 2^31 tiles"; return false; }  // 32-bit tile loop
