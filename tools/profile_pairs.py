@@ -24,18 +24,27 @@ ap.add_argument("--path", default=None)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--records", type=int, default=0)
 ap.add_argument("--knobs", default="")
+ap.add_argument("--subcfg", default="", help="schema and extents of a bench sub-config (bench.SUBCFG); views may be kind/lin")
 ap.add_argument("--stagger", type=int, default=0, help="allocate blob k at a k * STAGGER byte offset (alignment study)")
 ap.add_argument("--pool", action="store_true", help="all blobs of a side in one allocation, back to back")
 a = ap.parse_args()
 knobs = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)} or None
-cfg = W.CONFIGS[a.config]
+if a.subcfg:
+    import bench
+    cfg = bench.SUBCFG[a.subcfg]
+else:
+    cfg = W.CONFIGS[a.config]
 schema = W.SCHEMAS[cfg["schema"]]
 ext = [a.records] if a.records else list(cfg["extents"])
+
+
+def view(spec):
+    kind, _, lin = spec.partition("/")
+    return llama.Mapping.from_spec(schema, ext, W.resolve_spec(kind), lin=lin or "row")
 warmed = False
 for pair in a.pairs.split(","):
     s, d = pair.split(":")
-    sm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(s))
-    dm = llama.Mapping.from_spec(schema, ext, W.resolve_spec(d))
+    sm, dm = view(s), view(d)
     def alloc(m):
         if a.pool:
             sizes = [(x + 255) // 256 * 256 for x in m.blob_sizes()]

@@ -20,8 +20,8 @@ C3_BYTES = {"aos:aos_aligned": 57713623040, "aos_aligned:soa_mb": 57713623040, "
 
 
 def short(name):
-    for k in ("llb_jit_permute", "k_permute_ws", "k_permute_direct", "k_bulkcopy", "k_run", "k_naive",
-              "k_transpose2d", "k_gen", "k_fill", "k_move_runs", "k_move_aos_tma"):
+    for k in ("llb_jit_permute", "llb_jit_transpose", "k_transpose_wide", "k_permute_ws", "k_permute_direct",
+              "k_bulkcopy", "k_run", "k_naive", "k_transpose2d", "k_gen", "k_fill", "k_move_runs", "k_move_aos_tma"):
         if k in name:
             return k
     return name.split("(")[0]
@@ -60,10 +60,11 @@ def pair_bytes(cfg):
     sc = bench.SUBCFG[cfg]
     schema = W.SCHEMAS[sc["schema"]]
     out = []
+    def view(spec):  # kind or kind/linearisation (F4 sub-configs)
+        kind, _, lin = spec.partition("/")
+        return llama.Mapping.from_spec(schema, sc["extents"], W.resolve_spec(kind), lin=lin or "row")
     for a, b in bench.pairs_of(cfg):
-        sm = llama.Mapping.from_spec(schema, sc["extents"], W.resolve_spec(a))
-        dm = llama.Mapping.from_spec(schema, sc["extents"], W.resolve_spec(b))
-        out.append(sm.footprint() + dm.footprint())
+        out.append(view(a).footprint() + view(b).footprint())
     return out
 
 
