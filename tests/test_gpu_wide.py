@@ -111,10 +111,13 @@ def test_hep100_full_size(llama, oracle_mod):
 
 @pytest.mark.parametrize("ext", [[64, 64], [8, 96], [1024, 1024]])
 def test_hep100_jit_short_tiles(llama, oracle_mod, ext):
-    """Packed <-> aligned AoS transposes of 380 / 480-byte records through the
+    """Packed <-> aligned AoS transposes of 380 / 480-byte records, and AoS into
+    row-major SoA (incl. the aligned single blob's zeroed gaps), through the
     JIT transpose with 8- / 4-row tiles (per-record programs)."""
     for a, sl, b, dl in [("aos", "row", "aos_aligned", "col"), ("aos_aligned", "col", "aos", "row"),
-                         ("aos", "col", "aos_aligned", "row"), ("aos_aligned", "row", "aos", "col")]:
+                         ("aos", "col", "aos_aligned", "row"), ("aos_aligned", "row", "aos", "col"),
+                         ("aos", "col", "soa_mb", "row"), ("aos_aligned", "col", "soa_sb", "row"),
+                         ("aos", "col", "soa_sb_aligned", "row"), ("aos_aligned", "col", "soa_mb", "row")]:
         sm = llama.Mapping.from_spec(W.HEP100, ext, W.resolve_spec(a), lin=sl)
         dm = llama.Mapping.from_spec(W.HEP100, ext, W.resolve_spec(b), lin=dl)
         pl = llama.plan(sm, dm)

@@ -15,11 +15,14 @@ import paper_2106_04284_b200 as llama  # noqa: E402
 import workloads as W  # noqa: E402
 
 PEAK = 6550.0
-PAIRS = [("aos", "col", "soa_mb", "row"), ("aos", "row", "aos", "col"), ("aos", "row", "aos_aligned", "col"),
-         ("aos_aligned", "col", "soa_sb", "row"), ("aos_aligned", "col", "aos", "row"), ("soa_mb", "col", "aos", "row"),
-         ("aos", "col", "soa_sb", "row"), ("aos_aligned", "row", "aos_aligned", "col")]
+PAIRS = [tuple(x.split(":")) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [
+    ("aos", "col", "soa_mb", "row"), ("aos", "row", "aos", "col"), ("aos", "row", "aos_aligned", "col"),
+    ("aos_aligned", "col", "soa_sb", "row"), ("aos_aligned", "col", "aos", "row"), ("soa_mb", "col", "aos", "row"),
+    ("aos", "col", "soa_sb", "row"), ("aos_aligned", "row", "aos_aligned", "col")]
+KNOBS = [None] + [dict((k, int(v)) for k, v in (kv.split("=") for kv in ks.split("+"))) for ks in sys.argv[2].split(",")] \
+    if len(sys.argv) > 2 else [None, {"jit_tile": 128}, {"jit_tile": 256}]
 for a, sl, b, dl in PAIRS:
-    for kn in (None, {"jit_tile": 128}, {"jit_tile": 256}):
+    for kn in KNOBS:
         try:
             e = 256
             sm = llama.Mapping.from_spec(W.HEP100, [e, e], W.resolve_spec(a), lin=sl)
