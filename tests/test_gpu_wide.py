@@ -135,3 +135,42 @@ def test_hep100_staged_knob(llama, oracle_mod):
             if "morton" in (sl, dl) and ext[0] != ext[1]:
                 continue
             _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl, knobs=kn)
+
+
+def _wide_schema(rng):
+    """A random record of 40-110 leaves (1- to 8-byte, arrays, nesting): too
+    wide for the JIT transpose's 16 x 32 tiles."""
+    types = ["i8", "u8", "bool", "i16", "u16", "i32", "u32", "f32", "i64", "u64", "f64"]
+    fields = []
+    while len(fields) < rng.randint(40, 100):
+        t = rng.choice(types)
+        if rng.random() < 0.1:
+            t += f"[{rng.randint(2, 4)}]"
+        fields.append(f"f{len(fields)}:{t}")
+    fields.append("n{" + ",".join(f"g{j}:{rng.choice(types)}" for j in range(rng.randint(1, 6))) + "}")
+    return "R{" + ",".join(fields) + "}"
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_wide_transpose_fuzz(llama, oracle_mod, seed):
+    """Random wide schemas x kinds (packed / aligned AoS, SoA SB / MB, aligned
+    SB, AoSoA with 3 / 4 / 8 / 16 lanes) x storage orders x ragged extents,
+    random wide-kernel knobs; the default plan (wide kernel, JIT short tiles
+    or naive) against the oracle byte for byte."""
+    import random
+    rng = random.Random(9000 + seed)
+    schema = _wide_schema(rng)
+    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False), ("soa_sb", 1, True),
+             ("aosoa", 3, False), ("aosoa", 4, True), ("aosoa", 8, False), ("aosoa", 16, False)]
+    for _ in range(4):
+        ext = rng.choice([[32, 32], [64, 64], [16, 16], [40, 72], [33, 65], [128, 8], [8, 128], [64, 36]])
+        lins = ["row", "col"] + (["morton"] if ext[0] == ext[1] else [])
+        slin = rng.choice(lins)
+        dlin = rng.choice([x for x in lins if x != slin])
+        knobs = {}
+        for name, choices in (("wide_group", [0, 1]), ("wide_torder", [0, 1, 2]), ("wide_stage", [0, 1]),
+                              ("wide_chunk4", [0, 1]), ("wide", [1, 2])):
+            if rng.random() < 0.4:
+                knobs[name] = rng.choice(choices)
+        _check(llama, oracle_mod, schema, ext, rng.choice(kinds), slin, rng.choice(kinds), dlin, knobs=knobs or None,
+               expect_wide=False, seed=seed)
