@@ -285,6 +285,7 @@ typedef enum {
                                   takes fewer simulated shared-memory wavefronts (0: measured slower) */
   LLAMA_KNOB_WIDE_TORDER,      /* wide transpose tile order: 0 x fastest, 1 y fastest, 2 along a column-major
                                   element-wise side (2) */
+  LLAMA_KNOB_WIDE_TMA,         /* wide transpose: AoS images loaded / stored as one tensor-map TMA box per tile (1) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

@@ -158,6 +158,32 @@ __device__ __forceinline__ void cp_async(uint8_t* s, const uint8_t* g, uint32_t 
 
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Tensor-map TMA (SASS UTMALDG / UTMASTG): the tile's runs of an A side as one box.
+__device__ __forceinline__ void tma_load(uint8_t* sdst, const CUtensorMap* m, uint32_t rank, uint32_t c0, uint32_t c1,
+                                         uint32_t c2, uint64_t* bar) {
+  if (rank == 2)
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(smem_u32(sdst)), "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(sdst)), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store(const CUtensorMap* m, uint32_t rank, uint32_t c0, uint32_t c1, uint32_t c2,
+                                          const uint8_t* ssrc) {
+  if (rank == 2)
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0),
+                 "r"(c1), "r"(smem_u32(ssrc))
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(m), "r"(c0),
+                 "r"(c1), "r"(c2), "r"(smem_u32(ssrc))
+                 : "memory");
+}
+
 struct Tile {
   uint64_t y0, x0;
   uint32_t h, w;  // valid rows / columns (ragged edge tiles)
@@ -257,6 +283,60 @@ __device__ __forceinline__ Tile tile_of(const WideParams& p, uint32_t tile) {
   tl.h = (uint32_t)(hh < (1ull << p.lty) ? hh : (1ull << p.lty));
   tl.w = (uint32_t)(ww < (1ull << p.ltx) ? ww : (1ull << p.ltx));
   return tl;
+}
+
+// box coordinates of a tile on an A side (row-major: {x0 * S / e, y0};
+// column-major: {0, y0 / g, x0})
+__device__ __forceinline__ void box_coords(const WideSide& s, const Tile& tl, uint32_t& c0, uint32_t& c1,
+                                           uint32_t& c2) {
+  if (s.tma == 2) {
+    c0 = (uint32_t)(tl.x0 * s.S / s.elsz);
+    c1 = (uint32_t)tl.y0;
+    c2 = 0;
+  } else {
+    c0 = 0;
+    c1 = (uint32_t)(tl.y0 / s.g);
+    c2 = (uint32_t)tl.x0;
+  }
+}
+
+// A source image: one TMA box (thread 0 issues, every thread waits on the
+// mbarrier's phase) or the cp.async run copies
+__device__ __forceinline__ void load_src(const WideParams& p, const Tile& tl, uint8_t* smem, uint32_t& phase) {
+  const WideSide& s = p.side[0];
+  if (s.tma) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.bar);
+    if (threadIdx.x == 0) {
+      uint32_t c0, c1, c2;
+      box_coords(s, tl, c0, c1, c2);
+      mbar_arrive_expect_tx(bar, s.box_bytes);
+      tma_load(smem + s.img, &p.tmap[0], s.tma, c0, c1, c2, bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+  } else {
+    load_image(p, s, tl, smem + s.img);
+    cp_async_wait_all();
+  }
+}
+
+// A destination image -> global: one TMA box store (thread 0; the image is
+// reused only after its read-out, hence wait_group.read before the barrier
+// that ends the tile), or vector run stores.  The writers fenced their
+// generic-proxy shared-memory writes before the preceding barrier.
+__device__ __forceinline__ void flush_dst(const WideParams& p, const Tile& tl, uint8_t* smem) {
+  const WideSide& s = p.side[1];
+  if (s.tma) {
+    if (threadIdx.x == 0) {
+      uint32_t c0, c1, c2;
+      box_coords(s, tl, c0, c1, c2);
+      tma_store(&p.tmap[1], s.tma, c0, c1, c2, smem + s.img);
+      bulk_commit();
+      bulk_wait_read<0>();
+    }
+  } else {
+    flush_image(p, s, tl, smem + s.img);
+  }
 }
 
 // ---------------------------------------------------------------- moves
@@ -676,10 +756,18 @@ struct StoreEE {
 
 template <int MODE, bool UNI, bool GRP, int MINB>
 __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_constant__ WideParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const WideSide& S0 = p.side[0];
   const WideSide& S1 = p.side[1];
   const uint32_t tid = threadIdx.x, lt = p.lty + p.ltx, n = 1u << lt;
+  uint32_t phase = 0;  // of the TMA mbarrier (source box loads)
+  if (S0.tma) {
+    if (tid == 0) {
+      mbar_init(reinterpret_cast<uint64_t*>(smem + p.bar), 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   if ((MODE == 1 || MODE == 2) && p.dzero) {  // padding bytes of the destination image stay 0
     for (uint32_t u = tid * 16; u < S1.img_bytes; u += kWT * 16)
       *reinterpret_cast<uint4*>(smem + S1.img + u) = make_uint4(0, 0, 0, 0);
@@ -774,8 +862,7 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
     } else {
       const Tile tl = tile_of(p, item);
       if constexpr (MODE == 0 || MODE == 2 || MODE == 3) {
-        load_image(p, S0, tl, smem + S0.img);
-        cp_async_wait_all();
+        load_src(p, tl, smem, phase);
         __syncthreads();
       }
       if constexpr (MODE == 3) {  // same record layout: flush the destination runs from the source image
@@ -860,9 +947,10 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
               }
             }
           }
+          if constexpr (MODE == 1) fence_proxy_async_smem();  // image writes -> the TMA store
           __syncthreads();
           if constexpr (MODE == 1) {
-            flush_image(p, S1, tl, smem + S1.img);
+            flush_dst(p, tl, smem);
             __syncthreads();
           }
           continue;
@@ -904,9 +992,10 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
           }
         }
       }
+      if constexpr (MODE == 1 || MODE == 2) fence_proxy_async_smem();
       __syncthreads();
       if constexpr (MODE == 1 || MODE == 2) {
-        flush_image(p, S1, tl, smem + S1.img);
+        flush_dst(p, tl, smem);
         __syncthreads();
       }
     }
@@ -915,8 +1004,72 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
 
 }  // namespace
 
-int launch_transpose_wide(const WideParams& p, void* stream) {
-  if (p.n_items == 0) return 0;
+namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = []() -> EncodeFn {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeFn>(f);
+  }();  // (a function-local static: initialised once, thread-safe)
+  return fn;
+}
+
+// the box of side X over its blob: row-major [H][W * S] or column-major
+// [W][H / g][g * S] in elsz-byte elements (WideSide)
+int encode_side(WideParams& q, int X, uint8_t* blob) {
+  const WideSide& s = q.side[X];
+  EncodeFn fn = encode_fn();
+  if (!fn) return (int)cudaErrorNotSupported;
+  const CUtensorMapDataType dt = s.elsz == 8   ? CU_TENSOR_MAP_DATA_TYPE_UINT64
+                                 : s.elsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                 : s.elsz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                               : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const uint64_t S = s.S, H = q.H, W = q.W, TY = 1ull << q.lty, TX = 1ull << q.ltx;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], estr[3] = {1, 1, 1};
+  cuuint32_t rank;
+  if (s.tma == 2) {
+    rank = 2;
+    dims[0] = W * S / s.elsz, dims[1] = H;
+    strides[0] = W * S;
+    box[0] = (cuuint32_t)(TX * S / s.elsz), box[1] = (cuuint32_t)TY;
+  } else {
+    rank = 3;
+    dims[0] = s.g * S / s.elsz, dims[1] = H / s.g, dims[2] = W;
+    strides[0] = s.g * S, strides[1] = H * S;
+    box[0] = (cuuint32_t)(s.g * S / s.elsz), box[1] = (cuuint32_t)(TY / s.g), box[2] = (cuuint32_t)TX;
+  }
+  const CUresult r = fn(&q.tmap[X], dt, rank, blob + s.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int launch_transpose_wide(const WideParams& p0, void* stream) {
+  if (p0.n_items == 0) return 0;
+  const WideParams* pp = &p0;
+  WideParams q;
+  if (p0.side[0].tma || p0.side[1].tma) {  // the blob addresses are part of the tensor maps
+    q = p0;
+    for (int X = 0; X < 2; ++X)
+      if (q.side[X].tma) {
+        uint8_t* blob = X == 0 ? const_cast<uint8_t*>(q.sb[q.side[0].blob]) : q.db[q.side[1].blob];
+        if (int e = encode_side(q, X, blob)) return e;
+      }
+    pp = &q;
+  }
+  const WideParams& p = *pp;
   static LaunchCache cache[13][64];
   // index: mode + 5 * (every E side uniform: block split hoisted, no per-leaf
   // division); 10 / 11 / 12: modes 0 / 1 / 4 in 4-record groups.  Minimum CTAs per SM

@@ -3,6 +3,7 @@
 // both compile it.  Every kernel receives one of these by value as a
 // __grid_constant__ parameter (<= 32 KB kernel parameter space, CUDA >= 12.1).
 #pragma once
+#include <cuda.h>  // CUtensorMap (a plain C struct)
 #include <stdint.h>
 
 #include "llama_b200.h"
@@ -333,6 +334,13 @@ struct WideSide {
   uint32_t lshift;  // E, uni: log2(L) or kNoShift
   uint32_t mshift;  // E, uni, L not a power of two: ceil(log2 L); q = (t + ((p - t) >> 1)) >> (mshift - 1),
   uint64_t magic;   //   t = umulhi(p, magic), magic = floor(2^64 (2^mshift - L) / L) + 1
+  // A, tensor-map TMA (knob wide_tma): the tile's runs are one box of the
+  // side's blob viewed as a 2-d (row-major: [H][W * S]) or 3-d (column-major:
+  // [W][H / g][g * S]) array of elsz-byte elements; the image is the dense box
+  uint32_t tma;     // 0 cp.async / vector copies, 2 / 3: box dimensions
+  uint32_t elsz;    // element bytes of the tensor map (1, 2, 4, 8)
+  uint32_t g;       // 3-d: records per innermost row of the box
+  uint32_t box_bytes;
 };
 
 // Leaf j of the class order (positions, not leaf ids: the kernel walks them in order).
@@ -352,6 +360,7 @@ struct WideClass {      // positions [j0, j1) share size, unit and (grp) the E-s
 };
 
 struct WideParams {
+  CUtensorMap tmap[2];  // per side when side[X].tma (encoded per launch: the blob address is part of it)
   uint64_t H, W;
   uint64_t ntx;         // tiles along x
   uint64_t nty;         // tiles along y
@@ -367,6 +376,8 @@ struct WideParams {
   uint32_t buf;         // E -> E: shared-memory offset of the batch area
   uint32_t n_cls;
   uint32_t u3;          // mode 3: bytes per access of a record copy (16, 8, 4)
+  uint32_t bar;         // shared-memory offset of the TMA mbarrier (8 bytes)
+  uint32_t pad4_;
   uint32_t grp;         // modes 0 / 1 / 4: threads move 4-record groups along the E side's order
   uint32_t stage;       // mode 1, grp: the E side lands by cp.async in a staging area at buf first
   uint16_t bstart[kMaxLeaves + 1];   // E -> E: batch b = positions [bstart[b], bstart[b+1])

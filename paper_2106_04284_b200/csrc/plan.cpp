@@ -382,6 +382,36 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
       WideSide& sd = w.side[X];
       if (!sd.A || sd.img_bytes == 0) continue;
       const uint32_t nruns = 1u << (lt - sd.lrun);
+      // (r2) tensor-map TMA (knob wide_tma): one box op per tile and side
+      // (SASS UTMALDG / UTMASTG); the image is the dense box
+      const Mapping& m = X == 0 ? s : d;
+      if (kn.get(LLAMA_KNOB_WIDE_TMA, 1) && m.lin != LLAMA_MORTON && m.base[0] % 16 == 0) {
+        const uint64_t S = sd.S;
+        uint32_t g = 1, e = 0;
+        uint64_t inner = 0;  // bytes of the box's innermost row
+        if (m.lin == LLAMA_ROW_MAJOR) {
+          inner = S << ltx;
+          if ((W * S) % 16) inner = 0;
+        } else {
+          for (uint32_t gg = 1u << lty; gg >= 1; gg >>= 1)
+            if ((gg * S) % 16 == 0 && gg * S <= 2048 && H % gg == 0) { g = gg; break; }
+          inner = (g * S) % 16 == 0 && g * S <= 2048 && H % g == 0 && (H * S) % 16 == 0 ? g * S : 0;
+        }
+        if (inner && inner % 16 == 0)
+          for (uint32_t ee : {8u, 4u, 2u, 1u})
+            if (inner % ee == 0 && inner / ee <= 256) { e = ee; break; }
+        if (e) {
+          sd.tma = m.lin == LLAMA_ROW_MAJOR ? 2 : 3;
+          sd.elsz = e;
+          sd.g = g;
+          sd.pitch = (uint32_t)(S << sd.lrun);  // dense runs
+          off = (off + 127) & ~127ull;          // (the TMA destination / source in shared memory)
+          sd.img = (uint32_t)off;
+          sd.img_bytes = sd.box_bytes = nruns * sd.pitch;
+          off += align16(sd.img_bytes);
+          continue;
+        }
+      }
       const uint32_t ord = w.mode == 1 ? w.side[0].lin : w.side[1].lin;  // the order the lanes run along
       const bool g = w.grp && w.mode <= 1;
       auto lanes = [&](int i) {
@@ -419,6 +449,8 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     }
     if (w.mode != 4) smem = off;
   }
+  w.bar = (uint32_t)((smem + 7) & ~7ull);  // the TMA mbarrier
+  smem = w.bar + 8;
   // leaf positions in class order: size, then unit, then the group vector flag, descending
   struct LeafInfo { int k; uint32_t size, unit; };
   std::vector<LeafInfo> li;
@@ -457,7 +489,7 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
   }
   if (w.mode == 4) {  // leaf batches of element buffers (n + n / 32 elements each) within 40 KB
     const uint64_t budget = 40 * 1024;
-    w.buf = (uint32_t)smem;
+    w.buf = (uint32_t)align16(smem);
     uint64_t used = 0;
     w.nbatch = 0;
     w.bstart[0] = 0;
