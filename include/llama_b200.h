@@ -286,6 +286,8 @@ typedef enum {
   LLAMA_KNOB_WIDE_TORDER,      /* wide transpose tile order: 0 x fastest, 1 y fastest, 2 along a column-major
                                   element-wise side (2) */
   LLAMA_KNOB_WIDE_TMA,         /* wide transpose: AoS images loaded / stored as one tensor-map TMA box per tile (1) */
+  LLAMA_KNOB_WIDE_ASYNC,       /* wide transpose, element-wise -> AoS: 4- / 8-byte leaves aligned on both sides land in
+                                  the image by cp.async element copies (0: measured 1-5% slower) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

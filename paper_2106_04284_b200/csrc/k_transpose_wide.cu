@@ -626,6 +626,19 @@ struct GroupEA {
   template <int SZ, int U, bool VEC>
   __device__ __forceinline__ void run() {
     const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+    if constexpr (SZ >= 4 && U == SZ) {
+      if (p.async) {  // (knob wide_async) 4- / 8-byte elements aligned on both sides: cp.async element copies
+#pragma unroll 1
+        for (uint32_t j = j0 + kl; j < j1; j += nl) {
+          const uint8_t* s = p.leaf[j].sp + qB + rem * SZ;
+          const uint32_t doff = p.leaf[j].doff;
+          each4([&](auto I) {
+            if (I.v < (int)nv) cp_async(img + ro[I.v] + doff, s + I.v * SZ, SZ);
+          });
+        }
+        return;
+      }
+    }
     // LG leaves' loads in flight before their stores (4 while a pack is <= 16 bytes)
     constexpr int LG = SZ == 8 ? 2 : 4;
 #pragma unroll 1
@@ -947,7 +960,10 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
               }
             }
           }
-          if constexpr (MODE == 1) fence_proxy_async_smem();  // image writes -> the TMA store
+          if constexpr (MODE == 1) {
+            if (p.async) cp_async_wait_all();  // (the cp.async element copies into the image)
+            fence_proxy_async_smem();          // image writes -> the TMA store
+          }
           __syncthreads();
           if constexpr (MODE == 1) {
             flush_dst(p, tl, smem);

@@ -377,7 +377,7 @@ struct WideParams {
   uint32_t n_cls;
   uint32_t u3;          // mode 3: bytes per access of a record copy (16, 8, 4)
   uint32_t bar;         // shared-memory offset of the TMA mbarrier (8 bytes)
-  uint32_t pad4_;
+  uint32_t async;       // mode 1, grp: 4- / 8-byte elements aligned on both sides move by cp.async
   uint32_t grp;         // modes 0 / 1 / 4: threads move 4-record groups along the E side's order
   uint32_t stage;       // mode 1, grp: the E side lands by cp.async in a staging area at buf first
   uint16_t bstart[kMaxLeaves + 1];   // E -> E: batch b = positions [bstart[b], bstart[b+1])
