@@ -169,8 +169,19 @@ def test_wide_transpose_fuzz(llama, oracle_mod, seed):
         dlin = rng.choice([x for x in lins if x != slin])
         knobs = {}
         for name, choices in (("wide_group", [0, 1]), ("wide_torder", [0, 1, 2]), ("wide_stage", [0, 1]),
-                              ("wide_chunk4", [0, 1]), ("wide", [1, 2])):
+                              ("wide_chunk4", [0, 1]), ("wide", [1, 2]), ("wide_tma", [0, 1]), ("wide_async", [0, 1])):
             if rng.random() < 0.4:
                 knobs[name] = rng.choice(choices)
         _check(llama, oracle_mod, schema, ext, rng.choice(kinds), slin, rng.choice(kinds), dlin, knobs=knobs or None,
                expect_wide=False, seed=seed)
+
+
+@pytest.mark.parametrize("knobs", [{"wide_tma": 0}, {"wide_async": 1}, {"wide_chunk4": 1}, {"wide_torder": 1}])
+def test_hep100_knob_variants(llama, oracle_mod, knobs):
+    """Every wide-kernel variant a knob selects, on ragged and full tiles, each
+    mode: byte-exact like the defaults."""
+    for ext in ([64, 64], [37, 68]):
+        for a, sl, b, dl in [("aos", "row", "soa_mb", "col"), ("soa_mb", "col", "aos_aligned", "row"),
+                             ("soa_sb", "row", "aos", "col"), ("aos", "col", "aos", "row"),
+                             ("aos_aligned", "row", "aos_aligned", "col"), ("soa_mb", "row", "soa_sb", "col")]:
+            _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl, knobs=knobs)
