@@ -231,3 +231,41 @@ def test_f4_transposes_full_size(llama, oracle_mod, case):
     exp = oracle_mod.copy(so, src, do, nthreads=threads)
     for j, t in enumerate(db):
         assert np.array_equal(t.cpu().numpy(), exp[j]), ("dst", j)
+
+
+F4_HEP = [("aos", "row", "soa_mb", "col"), ("soa_mb", "col", "aos", "row"), ("aos", "row", "aos_aligned", "col"),
+          ("aos", "col", "aos", "morton"), ("soa_sb", "row", "soa_mb", "col")]
+
+
+@pytest.mark.parametrize("case", range(len(F4_HEP)))
+def test_f4_hep100_transposes_bench_size(llama, oracle_mod, case):
+    """The bench's F4_hep pairs (bench.pairs_of("F4_hep")) at its 2048 x 2048
+    HEP100 size and launch configuration (default plans: the wide kernel and
+    the JIT's short tiles): whole blobs against the oracle, source padding
+    poisoned."""
+    import bench
+    assert [(a + "/" + sl, b + "/" + dl) for a, sl, b, dl in F4_HEP] == bench.pairs_of("F4_hep")
+    a, slin, b, dlin = F4_HEP[case]
+    sspec, dspec = W.resolve_spec(a), W.resolve_spec(b)
+    ext = list(bench.SUBCFG["F4_hep"]["extents"])
+    n = ext[0] * ext[1]
+    sm = llama.Mapping.from_spec(W.HEP100, ext, sspec, lin=slin)
+    dm = llama.Mapping.from_spec(W.HEP100, ext, dspec, lin=dlin)
+    assert llama.plan(sm, dm)["path"] == "transpose"
+    sb = sm.alloc()
+    llama.generate(sm, sb, 13, pad_byte=0xCD)
+    db = dm.alloc()
+    for t in db:
+        t.fill_(0x5A)
+    llama.copy(sm, sb, dm, db)
+    torch.cuda.synchronize()
+    so = oracle_mod.mapping_from_spec(W.HEP100, ext, sspec, lin=slin)
+    do = oracle_mod.mapping_from_spec(W.HEP100, ext, dspec, lin=dlin)
+    threads = _threads(64 << 20)
+    src = so.alloc()
+    _par_generate(oracle_mod, so, src, 13, n, threads, pad=0xCD)
+    for j, t in enumerate(sb):
+        assert np.array_equal(t.cpu().numpy(), src[j]), ("src", j)
+    exp = oracle_mod.copy(so, src, do, nthreads=threads)
+    for j, t in enumerate(db):
+        assert np.array_equal(t.cpu().numpy(), exp[j]), ("dst", j)
