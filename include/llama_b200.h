@@ -288,6 +288,9 @@ typedef enum {
   LLAMA_KNOB_WIDE_TMA,         /* wide transpose: AoS images loaded / stored as one tensor-map TMA box per tile (1) */
   LLAMA_KNOB_WIDE_ASYNC,       /* wide transpose, element-wise -> AoS: 4- / 8-byte leaves aligned on both sides land in
                                   the image by cp.async element copies (0: measured 1-5% slower) */
+  LLAMA_KNOB_WIDE_AOSOA_IMG,    /* wide transpose: AoSoA-L sides whose tile runs hold whole blocks are staged as
+                                  shared-memory images (else element-wise), except an AoSoA destination of a plain AoS
+                                  source (2: that too) (1) */
   LLAMA_KNOB_COUNT
 } llama_knob;
 

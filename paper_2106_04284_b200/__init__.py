@@ -69,7 +69,7 @@ KNOBS = ["tile_bytes", "smem_budget", "stages", "dst_bufs", "ws_order", "no_tma"
          "word_mode", "direct", "direct_stages", "direct_async", "direct_phase", "direct_staging",
          "direct_chunks", "direct_mix", "bulk_chunk", "bulk_stages", "blobcopy_lsu", "transpose_raw",
          "transpose_linear", "transpose_raw1", "transpose_fixed", "transpose_table", "transpose_raw_typed",
-         "jit", "jit_tile", "jit_stages", "jit_dst_bufs", "jit_chunks", "jit_lanes", "jit_soa_tma", "jit_pad", "jit_block", "jit_bmap", "jit_torder", "jit_dst_lsu", "jit_swizzle", "jit_group", "jit_ctas", "jit_ablate", "wide", "wide_group", "wide_stage", "wide_chunk4", "wide_torder", "wide_tma", "wide_async"]
+         "jit", "jit_tile", "jit_stages", "jit_dst_bufs", "jit_chunks", "jit_lanes", "jit_soa_tma", "jit_pad", "jit_block", "jit_bmap", "jit_torder", "jit_dst_lsu", "jit_swizzle", "jit_group", "jit_ctas", "jit_ablate", "wide", "wide_group", "wide_stage", "wide_chunk4", "wide_torder", "wide_tma", "wide_async", "wide_aosoa_img"]
 
 
 class _PlanInfo(ctypes.Structure):

@@ -76,10 +76,13 @@ __device__ __forceinline__ uint64_t storage2(uint32_t lin, uint64_t y, uint64_t 
   return spread64(x) | (spread64(y) << 1);
 }
 
-// image offset of the record at index t along the A side's own order
+// image offset of the block of the record at index t along the A side's own
+// order (runs hold whole AoSoA-L blocks; plain AoS: L = 1), and its lane:
+// leaf k of the record sits at img_off + F_k + lane * s_k
 __device__ __forceinline__ uint32_t img_off(const WideSide& s, uint32_t t) {
-  return (t >> s.lrun) * s.pitch + (t & ((1u << s.lrun) - 1)) * s.S;
+  return (t >> s.lrun) * s.pitch + ((t & ((1u << s.lrun) - 1)) >> s.lL) * (uint32_t)s.B;
 }
+__device__ __forceinline__ uint32_t img_lane(const WideSide& s, uint32_t t) { return t & ((1u << s.lL) - 1); }
 
 // hoisted block split of a uniform E side: off = leaf ptr + qB + rem * s_k
 __device__ __forceinline__ void esplit(const WideSide& s, uint64_t p, uint64_t& qB, uint64_t& rem) {
@@ -346,9 +349,9 @@ __device__ __forceinline__ void flush_dst(const WideParams& p, const Tile& tl, u
 template <bool UNI>
 struct MovesAE {
   const WideParams& p;
-  const uint8_t* src;  // src image + record offset
+  const uint8_t* src;  // src image + block offset
   uint64_t qB, rem, pos;
-  uint32_t j0, j1, kl, nl;
+  uint32_t j0, j1, kl, nl, ln;  // ln: the record's lane in its block
   template <int SZ, int U>
   __device__ __forceinline__ void run() {
     constexpr int KG = 1;
@@ -357,7 +360,7 @@ struct MovesAE {
       uint64_t v[KG];
 #pragma unroll
       for (int g = 0; g < KG; ++g)
-        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff);
+        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff + ln * SZ);
 #pragma unroll
       for (int g = 0; g < KG; ++g) {
         const uint32_t jj = j + g * nl;
@@ -373,9 +376,9 @@ struct MovesAE {
 template <bool UNI>
 struct MovesEA {
   const WideParams& p;
-  uint8_t* dst;  // dst image + record offset
+  uint8_t* dst;  // dst image + block offset
   uint64_t qB, rem, pos;
-  uint32_t j0, j1, kl, nl;
+  uint32_t j0, j1, kl, nl, ln;
   template <int SZ, int U>
   __device__ __forceinline__ void run() {
     constexpr int KG = 2;
@@ -392,7 +395,7 @@ struct MovesEA {
       }
 #pragma unroll
       for (int g = 0; g < KG; ++g)
-        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff, v[g]);
+        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff + ln * SZ, v[g]);
     }
   }
 };
@@ -402,7 +405,7 @@ struct MovesAA {
   const WideParams& p;
   const uint8_t* src;
   uint8_t* dst;
-  uint32_t j0, j1, kl, nl;
+  uint32_t j0, j1, kl, nl, sln, dln;
   template <int SZ, int U>
   __device__ __forceinline__ void run() {
     constexpr int KG = 2;
@@ -411,10 +414,10 @@ struct MovesAA {
       uint64_t v[KG];
 #pragma unroll
       for (int g = 0; g < KG; ++g)
-        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff);
+        if (j + g * nl < j1) v[g] = ld<SZ, U>(src + p.leaf[j + g * nl].soff + sln * SZ);
 #pragma unroll
       for (int g = 0; g < KG; ++g)
-        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff, v[g]);
+        if (j + g * nl < j1) st<SZ, U>(dst + p.leaf[j + g * nl].doff + dln * SZ, v[g]);
     }
   }
 };
@@ -520,12 +523,12 @@ __device__ __forceinline__ void dispatch_vec(uint32_t size, uint32_t unit, bool 
 struct GroupAE {
   const WideParams& p;
   const uint8_t* img;
-  uint32_t ro0, ro1, ro2, ro3;
+  uint32_t ro0, ro1, ro2, ro3, ln0, ln1, ln2, ln3;
   uint64_t qB, rem;
   uint32_t nv, j0, j1, kl, nl;
   template <int SZ, int U, bool VEC>
   __device__ __forceinline__ void run() {
-    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+    const uint32_t ro[4] = {ro0 + ln0 * SZ, ro1 + ln1 * SZ, ro2 + ln2 * SZ, ro3 + ln3 * SZ};  // (+ lanes)
 #pragma unroll 1
     for (uint32_t j = j0 + kl; j < j1; j += nl) {
       const uint32_t so = p.leaf[j].soff;
@@ -581,11 +584,11 @@ struct ScatterEA {
   const WideParams& p;
   const uint8_t* stg;
   uint8_t* img;
-  uint32_t ro0, ro1, ro2, ro3;
+  uint32_t ro0, ro1, ro2, ro3, ln0, ln1, ln2, ln3;
   uint32_t gi, nv, j0, j1, kl, nl;
   template <int SZ, int U, bool VEC>
   __device__ __forceinline__ void run() {
-    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+    const uint32_t ro[4] = {ro0 + ln0 * SZ, ro1 + ln1 * SZ, ro2 + ln2 * SZ, ro3 + ln3 * SZ};  // (+ lanes)
 #pragma unroll 1
     for (uint32_t j = j0 + kl; j < j1; j += nl) {
       const WideLeaf& l = p.leaf[j];
@@ -602,7 +605,7 @@ struct ScatterEA {
 struct GroupEA {
   const WideParams& p;
   uint8_t* img;
-  uint32_t ro0, ro1, ro2, ro3;
+  uint32_t ro0, ro1, ro2, ro3, ln0, ln1, ln2, ln3;
   uint64_t qB, rem;
   uint32_t nv, j0, j1, kl, nl;
   template <int SZ, int U, bool VEC>
@@ -625,7 +628,7 @@ struct GroupEA {
   }
   template <int SZ, int U, bool VEC>
   __device__ __forceinline__ void run() {
-    const uint32_t ro[4] = {ro0, ro1, ro2, ro3};
+    const uint32_t ro[4] = {ro0 + ln0 * SZ, ro1 + ln1 * SZ, ro2 + ln2 * SZ, ro3 + ln3 * SZ};  // (+ lanes)
     if constexpr (SZ >= 4 && U == SZ) {
       if (p.async) {  // (knob wide_async) 4- / 8-byte elements aligned on both sides: cp.async element copies
 #pragma unroll 1
@@ -904,13 +907,15 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
           const WideSide& A = MODE == 0 ? S0 : S1;
           const uint32_t ng = n >> 2, gl = ng >= kWT ? 1 : kWT / ng;
           for (uint32_t gi = tid % ng; gi < ng; gi += kWT) {
-            uint32_t ro[4], nv = 0, r0 = 0, c0 = 0;
+            uint32_t ro[4], ln[4], nv = 0, r0 = 0, c0 = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               uint32_t r, c;
               t_rc(E.lin, 4 * gi + i, p.lty, p.ltx, r, c);
               if (i == 0) r0 = r, c0 = c;
-              ro[i] = img_off(A, rc_t(A.lin, r, c, p.lty, p.ltx));
+              const uint32_t ta = rc_t(A.lin, r, c, p.lty, p.ltx);
+              ro[i] = img_off(A, ta);
+              ln[i] = img_lane(A, ta);
               if (r < tl.h && c < tl.w && nv == (uint32_t)i) ++nv;
             }
             if (!nv) continue;
@@ -930,10 +935,12 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
             for (uint32_t q = 0; q < p.n_cls; ++q) {
               const WideClass& cl = p.cls[q];
               if constexpr (MODE == 0) {
-                GroupAE m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], qB, rem, nv, cl.j0, cl.j1, kl2, gl};
+                GroupAE m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], ln[0], ln[1], ln[2], ln[3], qB, rem, nv, cl.j0, cl.j1,
+                          kl2, gl};
                 dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
               } else {
-                GroupEA m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], qB, rem, nv, cl.j0, cl.j1, kl2, gl};
+                GroupEA m{p, smem + A.img, ro[0], ro[1], ro[2], ro[3], ln[0], ln[1], ln[2], ln[3], qB, rem, nv, cl.j0, cl.j1,
+                          kl2, gl};
                 dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
               }
             }
@@ -942,12 +949,14 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
             cp_async_wait_all();
             __syncthreads();
             for (uint32_t gi = tid % ng; gi < ng; gi += kWT) {
-              uint32_t ro[4], nv = 0;
+              uint32_t ro[4], ln[4], nv = 0;
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 uint32_t r, c;
                 t_rc(E.lin, 4 * gi + i, p.lty, p.ltx, r, c);
-                ro[i] = img_off(A, rc_t(A.lin, r, c, p.lty, p.ltx));
+                const uint32_t ta = rc_t(A.lin, r, c, p.lty, p.ltx);
+                ro[i] = img_off(A, ta);
+                ln[i] = img_lane(A, ta);
                 if (r < tl.h && c < tl.w && nv == (uint32_t)i) ++nv;
               }
               if (!nv) continue;
@@ -955,7 +964,8 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
 #pragma unroll 1
               for (uint32_t q = 0; q < p.n_cls; ++q) {
                 const WideClass& cl = p.cls[q];
-                ScatterEA m{p, smem + p.buf, smem + A.img, ro[0], ro[1], ro[2], ro[3], gi, nv, cl.j0, cl.j1, kl2, gl};
+                ScatterEA m{p, smem + p.buf, smem + A.img, ro[0], ro[1], ro[2], ro[3], ln[0], ln[1], ln[2], ln[3], gi, nv,
+                            cl.j0, cl.j1, kl2, gl};
                 dispatch_vec(cl.size, cl.unit & 0xFF, cl.unit >> 8, m);
               }
             }
@@ -978,7 +988,8 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
         t_rc(ord, t, p.lty, p.ltx, r, c);
         if (r >= tl.h || c >= tl.w) continue;
         if constexpr (MODE == 0) {
-          MovesAE<UNI> m{p, smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx)), 0, 0, 0, 0, 0, kl, nl};
+          const uint32_t ts = rc_t(S0.lin, r, c, p.lty, p.ltx);
+          MovesAE<UNI> m{p, smem + S0.img + img_off(S0, ts), 0, 0, 0, 0, 0, kl, nl, img_lane(S0, ts)};
           m.pos = storage2(S1.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
           if (UNI) esplit(S1, m.pos, m.qB, m.rem);
 #pragma unroll 1
@@ -988,7 +999,8 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
             dispatch(p.cls[q].size, p.cls[q].unit & 0xFF, m);
           }
         } else if constexpr (MODE == 1) {
-          MovesEA<UNI> m{p, smem + S1.img + img_off(S1, rc_t(S1.lin, r, c, p.lty, p.ltx)), 0, 0, 0, 0, 0, kl, nl};
+          const uint32_t td = rc_t(S1.lin, r, c, p.lty, p.ltx);
+          MovesEA<UNI> m{p, smem + S1.img + img_off(S1, td), 0, 0, 0, 0, 0, kl, nl, img_lane(S1, td)};
           m.pos = storage2(S0.lin, tl.y0 + r, tl.x0 + c, p.H, p.W);
           if (UNI) esplit(S0, m.pos, m.qB, m.rem);
 #pragma unroll 1
@@ -998,8 +1010,9 @@ __global__ void __launch_bounds__(kWT, MINB) k_transpose_wide(const __grid_const
             dispatch(p.cls[q].size, p.cls[q].unit & 0xFF, m);
           }
         } else {
-          MovesAA m{p, smem + S0.img + img_off(S0, rc_t(S0.lin, r, c, p.lty, p.ltx)),
-                    smem + S1.img + img_off(S1, t), 0, 0, kl, nl};
+          const uint32_t ts = rc_t(S0.lin, r, c, p.lty, p.ltx);
+          MovesAA m{p, smem + S0.img + img_off(S0, ts), smem + S1.img + img_off(S1, t), 0, 0, kl, nl,
+                    img_lane(S0, ts), img_lane(S1, t)};
 #pragma unroll 1
           for (uint32_t q = 0; q < p.n_cls; ++q) {
             m.j0 = p.cls[q].j0;

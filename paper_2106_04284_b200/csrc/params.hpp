@@ -330,13 +330,15 @@ struct WideSide {
   uint32_t img;     // A: shared-memory offset of the image
   uint32_t img_bytes;
   uint32_t uni;     // E: every leaf shares L / B below (the block split is hoisted out of the leaf loop)
-  uint64_t L, B;    // E, uni: lanes per block, block stride
+  uint64_t L, B;    // E, uni: lanes per block, block stride (A: block stride too)
   uint32_t lshift;  // E, uni: log2(L) or kNoShift
   uint32_t mshift;  // E, uni, L not a power of two: ceil(log2 L); q = (t + ((p - t) >> 1)) >> (mshift - 1),
   uint64_t magic;   //   t = umulhi(p, magic), magic = floor(2^64 (2^mshift - L) / L) + 1
   // A, tensor-map TMA (knob wide_tma): the tile's runs are one box of the
   // side's blob viewed as a 2-d (row-major: [H][W * S]) or 3-d (column-major:
   // [W][H / g][g * S]) array of elsz-byte elements; the image is the dense box
+  uint32_t lL;      // A: log2 of the lanes per block (AoSoA-L images: record t of a run sits in block
+  uint32_t pad5_;   //   (t >> lL) at B bytes per block (the B above), lane t & (L - 1); plain AoS: lL = 0, B = S)
   uint32_t tma;     // 0 cp.async / vector copies, 2 / 3: box dimensions
   uint32_t elsz;    // element bytes of the tensor map (1, 2, 4, 8)
   uint32_t g;       // 3-d: records per innermost row of the box

@@ -177,9 +177,12 @@ bool plan_transpose(const Mapping& s, const Mapping& d, const Knobs& kn, Plan* p
 // one part, L = 1, stride S % 4 == 0) or "E" (anything else, element-wise).
 namespace {
 
+// (r2) AoSoA-L sides (L a power of two <= 64) are image sides too when the
+// tile's runs hold whole blocks (checked against the tile shape below)
 bool wide_a_side(const Mapping& m) {
-  return m.uniform && m.parts.size() == 1 && (m.kind == LLAMA_AOS || m.kind == LLAMA_AOSOA) && m.L == 1 &&
-         m.B > 0 && m.B % 4 == 0 && m.B <= 4096;
+  const bool pow2 = m.L >= 1 && (m.L & (m.L - 1)) == 0;
+  return m.uniform && m.parts.size() == 1 && (m.kind == LLAMA_AOS || m.kind == LLAMA_AOSOA) && pow2 && m.L <= 64 &&
+         m.B > 0 && m.B % 4 == 0 && m.B / m.L <= 4096 && (m.B / m.L) * m.L == m.B;
 }
 
 // alignment (power of two <= 16) of every element address of leaf k on an E side
@@ -274,15 +277,17 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
   if (s.lin == d.lin) { *why = "equal linearisations"; return false; }
   if (s.extents.size() != 2) { *why = "the wide transposing copy is for 2-d views"; return false; }
   if (!kn.get(LLAMA_KNOB_WIDE, 1)) { *why = "knob wide = 0"; return false; }
-  const bool sA = wide_a_side(s), dA = wide_a_side(d);
+  bool sA = wide_a_side(s), dA = wide_a_side(d);
   const uint64_t H = (uint64_t)s.extents[0], W = (uint64_t)s.extents[1];
   const bool morton = s.lin == LLAMA_MORTON || d.lin == LLAMA_MORTON;
   uint32_t lty = 5, ltx = 5;  // E -> E: 32 x 32
+  for (int pass = 0; pass < 3; ++pass) {  // (an AoSoA side whose runs would split blocks is demoted to E)
+  lty = 5, ltx = 5;
   if (sA || dA) {
     // 128 records per tile while the images stay <= 64 KB (HEP100 aligned: 61 KB)
-    bool same = sA && dA && s.B == d.B && !d.has_padding();
+    bool same = sA && dA && s.B == d.B && s.L == 1 && d.L == 1 && !d.has_padding();
     for (int k = 0; k < s.K() && same; ++k) same = s.F[k] == d.F[k];
-    const uint64_t S = (sA ? s.B : 0) + (dA && !same ? d.B : 0);
+    const uint64_t S = (sA ? s.B / s.L : 0) + (dA && !same ? d.B / d.L : 0);
     uint32_t lt = 7;
     while (lt > 5 && (S << lt) > 64 * 1024) --lt;
     // the E side's storage runs span the tile: 32 records along a row /
@@ -304,6 +309,26 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     lty = std::min(lty, b);
     ltx = std::min(ltx, b);
   }
+  // AoSoA-L image sides: every run of the tile starts at a multiple of L and
+  // holds whole blocks
+  bool demoted = false;
+  for (int X = 0; X < 2; ++X) {
+    const Mapping& m = X == 0 ? s : d;
+    bool& A = X == 0 ? sA : dA;
+    if (!A || m.L == 1) continue;
+    const uint64_t run = m.lin == LLAMA_ROW_MAJOR ? 1ull << ltx : m.lin == LLAMA_COL_MAJOR ? 1ull << lty
+                                                                                      : 1ull << (lty + ltx);
+    bool ok = run % m.L == 0 && kn.get(LLAMA_KNOB_WIDE_AOSOA_IMG, 1);
+    // an AoSoA destination next to a plain AoS source image stays element-wise
+    // (measured, 1024^2 HEP100: AoS -> AoSoA8 median 0.92x as image -> image
+    // moves; AoSoA8 <-> SoA 1.16-1.57x, AoSoA8 -> AoSoA8 1.7x, AoSoA8 -> AoS 1.11x)
+    if (X == 1 && sA && s.L == 1 && kn.get(LLAMA_KNOB_WIDE_AOSOA_IMG, 1) < 2) ok = false;
+    if (m.lin == LLAMA_ROW_MAJOR) ok = ok && W % m.L == 0;
+    if (m.lin == LLAMA_COL_MAJOR) ok = ok && H % m.L == 0;
+    if (!ok) A = false, demoted = true;
+  }
+  if (!demoted) break;
+  }
   const uint32_t lt = lty + ltx, n = 1u << lt;
   p->wide.reset(new WideParams);
   WideParams& w = *p->wide;
@@ -316,7 +341,7 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
   w.ntx = ceil_div(W, 1ull << ltx);
   const uint64_t n_tiles = ceil_div(H, 1ull << lty) * w.ntx;
   if (sA && dA) {
-    bool same = s.B == d.B && !d.has_padding();
+    bool same = s.B == d.B && s.L == 1 && d.L == 1 && !d.has_padding();
     for (int k = 0; k < s.K() && same; ++k) same = s.F[k] == d.F[k];
     w.mode = same ? 3 : 2;
   } else {
@@ -330,7 +355,9 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     sd.A = (X == 0 ? sA : dA) ? 1 : 0;
     if (sd.A) {
       const bool image = !(X == 1 && sA && w.mode == 3);  // mode 3 flushes from the source image
-      sd.S = (uint32_t)m.B;
+      sd.S = (uint32_t)(m.B / m.L);  // bytes per record position of a run (AoSoA: B / L)
+      sd.B = (uint32_t)m.B;
+      sd.lL = ilog2(m.L);
       sd.blob = m.blob[0];
       sd.base = m.base[0];
       sd.lrun = m.lin == LLAMA_ROW_MAJOR ? ltx : m.lin == LLAMA_COL_MAJOR ? lty : lt;
@@ -459,7 +486,7 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
     for (int X = 0; X < 2; ++X) {
       const Mapping& m = X == 0 ? s : d;
       const WideSide& sd = w.side[X];
-      const uint32_t a = sd.A ? (uint32_t)gcd64(gcd64(16, sd.pitch), gcd64(sd.S, m.F[k])) : wide_e_align(m, k);
+      const uint32_t a = sd.A ? (uint32_t)gcd64(gcd64(16, sd.pitch), gcd64(sd.B, m.F[k])) : wide_e_align(m, k);
       u = std::min(u, a);
     }
     if (w.grp && w.mode <= 1 && group_vec(w.mode == 0 ? d : s, k)) u |= 256;  // (f64: two 16-byte pieces)

@@ -185,3 +185,22 @@ def test_hep100_knob_variants(llama, oracle_mod, knobs):
                              ("soa_sb", "row", "aos", "col"), ("aos", "col", "aos", "row"),
                              ("aos_aligned", "row", "aos_aligned", "col"), ("soa_mb", "row", "soa_sb", "col")]:
             _check(llama, oracle_mod, W.HEP100, ext, a, sl, b, dl, knobs=knobs)
+
+
+@pytest.mark.parametrize("ext", [[64, 64], [37, 64], [64, 40], [16, 16]])
+def test_hep100_aosoa_images(llama, oracle_mod, ext):
+    """AoSoA-L sides staged as images when the tile's runs hold whole blocks
+    (L = 4 / 8 / 16, aligned AoSoA with padding inside the blocks), on full and
+    ragged tiles; knob wide_aosoa_img=0 keeps them element-wise."""
+    kinds = [("aosoa", 8, False), ("aosoa", 4, True), ("aosoa", 16, False)]
+    others = ["aos", "aos_aligned", "soa_mb"]
+    lins = [("row", "col"), ("col", "row")] + ([("row", "morton"), ("morton", "col")] if ext[0] == ext[1] else [])
+    for sl, dl in lins:  # (small Morton views between element-wise sides take the naive kernel)
+        for k in kinds:
+            for o in others:
+                _check(llama, oracle_mod, W.HEP100, ext, k, sl, o, dl, expect_wide=False)
+                _check(llama, oracle_mod, W.HEP100, ext, o, sl, k, dl, expect_wide=False)
+                _check(llama, oracle_mod, W.HEP100, ext, o, sl, k, dl, knobs={"wide_aosoa_img": 2}, expect_wide=False)
+            _check(llama, oracle_mod, W.HEP100, ext, k, sl, kinds[0], dl, expect_wide=False)
+    _check(llama, oracle_mod, W.HEP100, ext, kinds[0], "row", "aos", "col", knobs={"wide_aosoa_img": 0},
+           expect_wide=False)
