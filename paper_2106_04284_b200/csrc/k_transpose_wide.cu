@@ -310,10 +310,14 @@ __device__ __forceinline__ void load_src(const WideParams& p, const Tile& tl, ui
   if (s.tma) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.bar);
     if (threadIdx.x == 0) {
-      uint32_t c0, c1, c2;
-      box_coords(s, tl, c0, c1, c2);
       mbar_arrive_expect_tx(bar, s.box_bytes);
-      tma_load(smem + s.img, &p.tmap[0], s.tma, c0, c1, c2, bar);
+      if (s.tma == 1) {  // a Morton tile: one contiguous run, one bulk copy (UBLKCP)
+        bulk_g2s(smem + s.img, p.sb[s.blob] + run_start(p, s, tl, 0), s.box_bytes, bar);
+      } else {
+        uint32_t c0, c1, c2;
+        box_coords(s, tl, c0, c1, c2);
+        tma_load(smem + s.img, &p.tmap[0], s.tma, c0, c1, c2, bar);
+      }
     }
     mbar_wait(bar, phase);
     phase ^= 1;
@@ -331,9 +335,13 @@ __device__ __forceinline__ void flush_dst(const WideParams& p, const Tile& tl, u
   const WideSide& s = p.side[1];
   if (s.tma) {
     if (threadIdx.x == 0) {
-      uint32_t c0, c1, c2;
-      box_coords(s, tl, c0, c1, c2);
-      tma_store(&p.tmap[1], s.tma, c0, c1, c2, smem + s.img);
+      if (s.tma == 1) {
+        bulk_s2g(p.db[s.blob] + run_start(p, s, tl, 0), smem + s.img, s.box_bytes);
+      } else {
+        uint32_t c0, c1, c2;
+        box_coords(s, tl, c0, c1, c2);
+        tma_store(&p.tmap[1], s.tma, c0, c1, c2, smem + s.img);
+      }
       bulk_commit();
       bulk_wait_read<0>();
     }
@@ -1089,10 +1097,10 @@ int launch_transpose_wide(const WideParams& p0, void* stream) {
   if (p0.n_items == 0) return 0;
   const WideParams* pp = &p0;
   WideParams q;
-  if (p0.side[0].tma || p0.side[1].tma) {  // the blob addresses are part of the tensor maps
+  if (p0.side[0].tma >= 2 || p0.side[1].tma >= 2) {  // the blob addresses are part of the tensor maps
     q = p0;
     for (int X = 0; X < 2; ++X)
-      if (q.side[X].tma) {
+      if (q.side[X].tma >= 2) {  // (tma == 1: plain bulk copies, no map)
         uint8_t* blob = X == 0 ? const_cast<uint8_t*>(q.sb[q.side[0].blob]) : q.db[q.side[1].blob];
         if (int e = encode_side(q, X, blob)) return e;
       }

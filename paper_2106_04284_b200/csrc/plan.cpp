@@ -412,6 +412,18 @@ static bool plan_wide_impl(const Mapping& s, const Mapping& d, const Knobs& kn, 
       // (r2) tensor-map TMA (knob wide_tma): one box op per tile and side
       // (SASS UTMALDG / UTMASTG); the image is the dense box
       const Mapping& m = X == 0 ? s : d;
+      if (kn.get(LLAMA_KNOB_WIDE_TMA, 1) && m.lin == LLAMA_MORTON && m.base[0] % 16 == 0 &&
+          ((uint64_t)sd.S << lt) % 16 == 0 && ((uint64_t)sd.S << lt) < (1ull << 20)) {
+        // a Morton tile is one contiguous run starting at a multiple of n
+        // records: one 1-d bulk copy (UBLKCP) per tile and side
+        sd.tma = 1;
+        sd.pitch = (uint32_t)((uint64_t)sd.S << lt);
+        off = (off + 127) & ~127ull;
+        sd.img = (uint32_t)off;
+        sd.img_bytes = sd.box_bytes = sd.pitch;
+        off += align16(sd.img_bytes);
+        continue;
+      }
       if (kn.get(LLAMA_KNOB_WIDE_TMA, 1) && m.lin != LLAMA_MORTON && m.base[0] % 16 == 0) {
         const uint64_t S = sd.S;
         uint32_t g = 1, e = 0;
