@@ -210,8 +210,11 @@ typedef enum {
   LLAMA_PATH_BLOBCOPY = 2, /* identical layout without padding: raw blob copy */
   LLAMA_PATH_RUN = 3,      /* field-run copy: common contiguous runs >= 16 B */
   LLAMA_PATH_PERMUTE = 4,  /* TMA-staged tile permute through shared memory */
-  LLAMA_PATH_TRANSPOSE = 5 /* 2-d views of different linearisations: 32x32-record tiles through
-                              shared memory, read in source and written in destination storage order */
+  LLAMA_PATH_TRANSPOSE = 5 /* 2-d views of different linearisations: record tiles through
+                              shared memory, read in source and written in destination storage order --
+                              the plan-time specialised JIT transpose (TY x 32 tiles), the 32x32 tile kernel,
+                              or for records too wide for those (HEP100) the wide-record kernel
+                              (AoS / AoSoA sides as tensor-map TMA box images, SoA sides element-wise) */
 } llama_path;
 
 /* Tuning knobs: explicit overrides of the planner's measured defaults (for
