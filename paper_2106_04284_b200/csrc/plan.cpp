@@ -196,7 +196,8 @@ uint32_t wide_e_align(const Mapping& m, int k) {
 // largest chunk (16, 8, 4) dividing every run start and full-run length of
 // an A side whose runs hold 2^lrun records
 uint32_t wide_chunk(const Mapping& m, uint32_t lrun) {
-  const uint64_t S = m.B, H = (uint64_t)m.extents[0], W = (uint64_t)m.extents[1];
+  // (bytes per record position of a run: B / L for AoSoA-L images)
+  const uint64_t S = m.B / m.L, H = (uint64_t)m.extents[0], W = (uint64_t)m.extents[1];
   for (uint32_t c : {16u, 8u, 4u}) {
     bool ok = m.base[0] % c == 0 && ((S << lrun) % c == 0);
     if (m.lin == LLAMA_ROW_MAJOR) ok = ok && (W * S) % c == 0;

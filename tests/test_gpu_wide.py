@@ -204,3 +204,25 @@ def test_hep100_aosoa_images(llama, oracle_mod, ext):
             _check(llama, oracle_mod, W.HEP100, ext, k, sl, kinds[0], dl, expect_wide=False)
     _check(llama, oracle_mod, W.HEP100, ext, kinds[0], "row", "aos", "col", knobs={"wide_aosoa_img": 0},
            expect_wide=False)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_wide_forced_small_fuzz(llama, oracle_mod, seed):
+    """Random small / medium schemas (1-24 fields, odd record sizes) forced onto
+    the wide kernel (knob wide=2) x kinds incl. AoSoA-L image sides x storage
+    orders x extents: byte-exact against the oracle (the odd per-record
+    strides exercise the image chunk / alignment rules)."""
+    import random
+
+    from test_gpu_parity import _random_schema
+    rng = random.Random(7000 + seed)
+    schema = _random_schema(rng)
+    kinds = [("aos", 1, False), ("aos", 1, True), ("soa_mb", 1, False), ("soa_sb", 1, False),
+             ("aosoa", 4, False), ("aosoa", 8, True), ("aosoa", 16, False), ("aosoa", 32, False)]
+    for _ in range(4):
+        ext = rng.choice([[32, 32], [64, 64], [48, 32], [32, 48], [36, 64], [64, 40]])
+        lins = ["row", "col"] + (["morton"] if ext[0] == ext[1] else [])
+        slin = rng.choice(lins)
+        dlin = rng.choice([x for x in lins if x != slin])
+        _check(llama, oracle_mod, schema, ext, rng.choice(kinds), slin, rng.choice(kinds), dlin, knobs={"wide": 2},
+               expect_wide=False, seed=seed)
