@@ -395,3 +395,25 @@ def test_wide_transpose_plans():
     small = llama.Mapping.from_spec(W.PARTICLE7, [64, 64], W.resolve_spec("aos"), lin="row")
     smallc = llama.Mapping.from_spec(W.PARTICLE7, [64, 64], W.resolve_spec("soa_mb"), lin="col")
     assert not llama.plan(small, smallc)["wide"] and llama.plan(small, smallc, knobs={"wide": 2})["wide"]
+
+
+def test_jit_permute_scan_rules():
+    """The JIT permute rules from the knob scan: AoS-like
+    images on both sides take 2 source stages, 256-record tiles without
+    record groups; packed misaligned AoS into all-SoA 4 stages; record groups
+    into all-SoA store from registers (soa_tma 0)."""
+    def src(schema, n, a, b, knobs=None):
+        sm = llama.Mapping(schema, [n], *W.MAPPINGS[a])
+        dm = llama.Mapping(schema, [n], *W.MAPPINGS[b])
+        return llama.plan_source(sm, dm, knobs=knobs)
+    s = src(W.LISTING1, 1 << 20, "aos", "aos_aligned")
+    assert "#define LLB_NS 2u" in s and "#define LLB_T 512u" in s and "#define LLB_G 4u" in s
+    s = src(W.LISTING1, 1 << 20, "aos_aligned", "aosoa32")
+    assert "#define LLB_NS 2u" in s and "#define LLB_T 256u" in s
+    assert "#define LLB_NS 4u" in src(W.HEP100, 1 << 16, "aos", "soa_mb")
+    assert "#define LLB_NS 3u" in src(W.HEP100, 1 << 16, "aos_aligned", "soa_mb")
+    assert "#define LLB_NS 3u" in src(W.HEP100, 1 << 16, "aos", "soa_mb", knobs={"jit_stages": 3})
+    # record groups into SoA MB: no staging image for the destination leaves
+    s0 = src(W.LISTING1, 1 << 20, "aos", "soa_mb")
+    s2 = src(W.LISTING1, 1 << 20, "aos", "soa_mb", knobs={"jit_soa_tma": 2})
+    assert s0 != s2
