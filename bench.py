@@ -784,6 +784,9 @@ def run_c5(args, world, rank, local):
 
     import paper_2106_04284_b200 as llama
     torch.cuda.set_device(local)
+    if "RANK" not in os.environ:  # `python bench.py --config C5` on one GPU: a one-rank ring (the peer is this GPU)
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(free_port()))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = Ctx(args, world, rank, local)
     n = W.C5["extents"][0]
