@@ -36,3 +36,21 @@ def test_bench_two_ranks_one_device():
     assert c2["value"] > 0 and "dp2" in c2["config"]["parallelism"]
     assert c4["local_extents"] == [4096, 8192] and "dp2" in c4["config"]["parallelism"]
     assert line["gpu_launches"] > 0
+
+
+def test_bench_c5_one_rank_ring():
+    """`bench.py --config C5` without torchrun: a one-rank ring (the peer is
+    this GPU); every leg (fused TMA stores, LSU stores, copy engines, NCCL)
+    round-trip checked on the receiving rank."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C5", "--steps", "2",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    line = json.loads(lines[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0
+    legs = line["legs"]
+    assert {"fused", "fused_lsu", "staged_ce", "staged_nccl"} <= set(legs)
+    assert all(v["parity_roundtrip"] for v in legs.values() if isinstance(v, dict) and "parity_roundtrip" in v)
