@@ -410,6 +410,7 @@ def test_jit_permute_scan_rules():
     assert "#define LLB_NS 2u" in s and "#define LLB_T 512u" in s and "#define LLB_G 4u" in s
     s = src(W.LISTING1, 1 << 20, "aos_aligned", "aosoa32")
     assert "#define LLB_NS 2u" in s and "#define LLB_T 256u" in s
+    assert "#define LLB_NS 3u" in src(W.HEP100, 1 << 16, "aos", "aosoa32")  # (wide records: the rule stays off)
     assert "#define LLB_NS 4u" in src(W.HEP100, 1 << 16, "aos", "soa_mb")
     assert "#define LLB_NS 3u" in src(W.HEP100, 1 << 16, "aos_aligned", "soa_mb")
     assert "#define LLB_NS 3u" in src(W.HEP100, 1 << 16, "aos", "soa_mb", knobs={"jit_stages": 3})
